@@ -1,0 +1,178 @@
+// Internal object model of libafem_b200 (not part of the ABI).
+//
+// HBM layout of a system (DESIGN.md §Data layout):
+//   coords   n_nodes*dim  f64   nodal coordinates (AoS, like the dofs)
+//   conn     n_elem*npe   i32   element connectivity (mesh order)
+//   phase    n_elem       u8    phase label -> material table (<= kMaxMat)
+//   inc_ptr  n_nodes+1    i64   node -> incident (element, local node) pairs, in the reference's
+//   inc      n_elem*npe   u32   (batch, element) order = (phase, element id)  (assembly.hpp:125)
+//   adj_ptr  n_nodes+1    i64   node adjacency = the CSR pattern at node granularity; the dof-level
+//   adj      sum deg      i32   pattern (sparse.hpp:68-75) is its dim x dim expansion (never stored)
+//   mask     n_dof        u8    Dirichlet constraint table (assembly.hpp:192-211)
+//   presc    n_dof        f64
+// CSR values (pattern order) are n_dof rows of dim*deg(node) entries each; row_ptr is closed-form.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "element.cuh"
+
+namespace afem {
+
+struct Constraint {
+  int node, comp;
+  double value;
+};
+
+// Kernel-side view of a system (plain pointers).
+struct SysView {
+  int dim, npe;
+  int64_t n_nodes, n_elem, n_dof;
+  const double* coords;
+  const int32_t* conn;
+  const uint8_t* phase;
+  const DMat* mats;
+  const int64_t* inc_ptr;
+  const uint32_t* inc;
+  const int64_t* adj_ptr;
+  const int32_t* adj;
+  const uint8_t* mask;
+  const double* presc;
+  int* err;
+};
+
+struct StencilPlan;  // structured fast path (stencil.cu)
+
+struct System {
+  Ctx* ctx = nullptr;
+  int dim = 2, npe = 4;
+  int64_t n_nodes = 0, n_elem = 0, n_dof = 0, nnz = 0, adj_total = 0;
+  DevArray<double> coords;
+  DevArray<int32_t> conn;
+  DevArray<uint8_t> phase;
+  std::vector<DMat> mats;
+  DevArray<DMat> d_mats;
+  std::vector<int64_t> phase_count;  // elements per phase (batches = non-empty phases)
+  DevArray<int32_t> elem_order;      // element ids in (phase, id) order
+  DevArray<int64_t> inc_ptr;
+  DevArray<uint32_t> inc;
+  DevArray<int64_t> adj_ptr;
+  DevArray<int32_t> adj;
+  DevArray<uint8_t> mask;
+  DevArray<double> presc;
+  std::vector<Constraint> constraints;
+  DevArray<int> err;
+  // structured grid metadata (afem_system_create_grid)
+  bool grid = false;
+  int nx = 0, ny = 0, nz = 0;
+  double lx = 0, ly = 0, lz = 0;
+
+  SysView view() const {
+    return SysView{dim, npe, n_nodes, n_elem, n_dof, coords.p, conn.p, phase.p, d_mats.p, inc_ptr.p, inc.p,
+                   adj_ptr.p, adj.p, mask.p, presc.p, err.p};
+  }
+  int64_t device_bytes() const {
+    return coords.bytes() + conn.bytes() + phase.bytes() + elem_order.bytes() + inc_ptr.bytes() + inc.bytes() +
+           adj_ptr.bytes() + adj.bytes() + mask.bytes() + presc.bytes();
+  }
+};
+
+struct Values {
+  System* sys = nullptr;
+  DevArray<double> v;
+};
+
+struct Buffer {
+  System* sys = nullptr;
+  DevArray<double> store;
+  int state = 0;  // 0 OwnedByAssembly, 1 LeasedToSolver
+  uint64_t epoch = 0;
+};
+
+struct Operator {
+  virtual ~Operator() = default;
+  System* sys = nullptr;
+  int kind = 0;  // 0 EXPLICIT, 1 MATRIX_FREE
+  int64_t n = 0;
+  virtual void validate() const {}
+  virtual void apply(const double* x, double* y) = 0;  // device pointers, ctx stream, async
+  virtual void diagonal(double* d) = 0;                 // device pointer
+  virtual bool uses_stencil() const { return false; }
+};
+
+struct ExplicitOp : Operator {
+  const Buffer* buf = nullptr;
+  uint64_t epoch = 0;
+  void validate() const override;
+  void apply(const double* x, double* y) override;
+  void diagonal(double* d) override;
+};
+
+struct MfOp : Operator {
+  DevArray<double> state, diag;
+  DevArray<uint8_t> mask;
+  StencilPlan* stencil = nullptr;  // owned; released by destroy_stencil_plan
+  ~MfOp() override;
+  void apply(const double* x, double* y) override;
+  void diagonal(double* d) override;
+  bool uses_stencil() const override { return stencil != nullptr; }
+};
+
+// ---- system.cu
+std::unique_ptr<System> make_system(Ctx& c, int dim, int64_t n_nodes, int64_t n_elem, const double* d_coords,
+                                    const int32_t* d_conn, const int32_t* d_phase, const std::vector<DMat>& mats);
+std::unique_ptr<System> make_grid_system(Ctx& c, int dim, int nx, int ny, int nz, double lx, double ly, double lz,
+                                         const std::vector<double>& incl_xy, double radius,
+                                         const std::vector<DMat>& mats);
+void set_dirichlet(System& s, const std::vector<Constraint>& cs);
+std::vector<Constraint> benchmark_bcs(const System& s, double strain);
+void pattern_export(System& s, int64_t* d_row_ptr, int32_t* d_rows, int32_t* d_cols);
+void batch_export(System& s, int b, int64_t* size, int32_t* h_ids, int32_t* h_dof_map);
+void check_err(System& s);
+DMat make_dmat(int model, double E, double nu);
+
+// ---- assembly.cu
+void residual(System& s, const double* u, double* r);
+void jacobian(System& s, const double* u, double* values);
+void diagonal(System& s, const double* u, double* d);
+void mf_apply_general(System& s, const double* state, const uint8_t* mask, const double* x, double* y);
+void eliminate(System& s, double* values, double* residual, const double* u);
+void constrain_residual(System& s, double* residual, const double* u);
+void csr_apply(System& s, const double* values, const double* x, double* y);
+void csr_diagonal(System& s, const double* values, double* d);
+void impose_dirichlet(System& s, double* u);
+
+// ---- blas.cu (deterministic reductions; results in device scalars or host)
+double dot(Ctx& c, const double* x, const double* y, int64_t n);
+double free_norm(Ctx& c, const double* r, const uint8_t* mask, int64_t n);
+void axpy(Ctx& c, double a, const double* x, double* y, int64_t n);
+void copy(Ctx& c, const double* x, double* y, int64_t n);
+void fill(Ctx& c, double v, double* y, int64_t n);
+void add_scaled_dev(Ctx& c, const double* alpha_dev, double scale, const double* x, double* y, int64_t n);
+void dot_dev(Ctx& c, const double* x, const double* y, int64_t n, double* out_dev);
+
+// ---- krylov.cu
+struct SolverCfg {
+  int method = 0, precond = 0;
+  double rtol = 1e-13;
+  int max_iter = 10000, restart = 30;
+};
+struct SolveReport {
+  bool converged = false;
+  int iterations = 0;
+  std::vector<double> history;
+  double wall_time = 0.0;
+  std::string failure;
+};
+void validate_cfg(const SolverCfg& c);
+void solve(Operator& op, const SolverCfg& cfg, const double* b, const double* x0, double* x, SolveReport& rep);
+
+// ---- stencil.cu
+StencilPlan* make_stencil_plan(System& s, const MfOp& op);  // nullptr when not applicable
+void stencil_apply(StencilPlan& p, const MfOp& op, const double* x, double* y);
+void destroy_stencil_plan(StencilPlan* p);
+
+}  // namespace afem

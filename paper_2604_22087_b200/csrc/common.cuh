@@ -1,0 +1,102 @@
+// Common infrastructure for libafem_b200: error types (1:1 with the reference's exception types,
+// reference errors.hpp:10-38), RAII device arrays, the context (device + stream + scratch), and a
+// counted kernel-launch helper.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace afem {
+
+struct LeaseError : std::logic_error { using std::logic_error::logic_error; };
+struct StaleEpochError : std::logic_error { using std::logic_error::logic_error; };
+struct CapabilityError : std::logic_error { using std::logic_error::logic_error; };
+struct FactorizationError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct InvertedElementError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NomemError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+[[noreturn]] inline void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e),
+                file, line, what);
+  if (e == cudaErrorMemoryAllocation) throw NomemError(buf);
+  throw CudaError(buf);
+}
+
+#define AFEM_CK(x)                                                           \
+  do {                                                                       \
+    cudaError_t e_ = (x);                                                    \
+    if (e_ != cudaSuccess) ::afem::throw_cuda(e_, #x, __FILE__, __LINE__);   \
+  } while (0)
+
+// Device array owned by the library (move-only).
+template <class T>
+struct DevArray {
+  T* p = nullptr;
+  size_t n = 0;
+  DevArray() = default;
+  explicit DevArray(size_t count) { alloc(count); }
+  DevArray(const DevArray&) = delete;
+  DevArray& operator=(const DevArray&) = delete;
+  DevArray(DevArray&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevArray& operator=(DevArray&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevArray() { release(); }
+  void alloc(size_t count) {
+    release();
+    if (count == 0) return;
+    AFEM_CK(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+  T* get() const { return p; }
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  int64_t launches = 0;
+  // scratch for deterministic two-stage reductions
+  DevArray<double> red_partials;  // kMaxBlocks * 4
+  DevArray<double> red_out;       // 64 scalars
+  DevArray<unsigned int> red_counter;
+  std::vector<double> host_scalar;
+};
+
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs: partial-sum slots for the deterministic reductions
+constexpr int kRedThreads = 256;
+
+// Counted launch on the context stream. Every kernel the library issues goes through here so
+// bench.py can report how many of OUR kernels ran in a timed region.
+template <class... KArgs, class... Args>
+inline void launch(Ctx& c, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+  if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
+  k<<<grid, block, smem, c.stream>>>(std::forward<Args>(args)...);
+  ++c.launches;
+  AFEM_CK(cudaGetLastError());
+}
+
+inline unsigned grid_for(int64_t n, int threads, int64_t cap = 1 << 30) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace afem

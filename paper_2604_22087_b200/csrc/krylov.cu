@@ -1,0 +1,350 @@
+// Krylov solvers on the device: Jacobi-preconditioned CG (krylov.hpp:350-408) and restarted,
+// left-preconditioned GMRES(m) with modified Gram-Schmidt (krylov.hpp:415-530).
+//
+// CG keeps every scalar (rz, pAp, alpha, beta, the residual history) in device memory. One
+// iteration is four launches — operator apply, pAp reduction, the fused x/r/z update with the
+// (r.r, r.z) reduction, and the p update — each of which becomes a no-op once the device-side
+// `done` flag is set, so the host enqueues chunks of iterations and synchronises once per chunk
+// while the iteration count and history stay exact. Observable semantics follow the reference:
+// convergence on the recurrence residual, then re-verification with a fresh apply and a restart
+// from the true residual if the recurrence drifted; pAp <= 0 reports a failure string;
+// b = 0 uses an absolute test.
+#include <chrono>
+#include <cmath>
+#include <string>
+
+#include "afem_impl.hpp"
+#include "reduce.cuh"
+
+namespace afem {
+
+unsigned red_grid(int64_t n);
+
+namespace {
+
+struct CgDev {
+  double rz, pap, alpha, beta, denom, rtol;
+  int it, max_iter, done, fail, conv, pad;
+};
+
+__global__ void k_residual_vec(const double* b, const double* ax, double* r, int64_t n, double* partials,
+                               unsigned int* counter, double* out) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = b[i] - ax[i];
+    if (r) r[i] = d;
+    s += d * d;
+  }
+  double v[1] = {s};
+  if (grid_reduce<1>(v, partials, counter))
+    if (threadIdx.x == 0) out[0] = sqrt(v[0]);
+}
+
+// z = M r; p = z; rz = r.z
+__global__ void k_cg_start(const double* r, const double* inv, double* z, double* p, int64_t n, double* partials,
+                           unsigned int* counter, CgDev* st) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double zi = inv ? r[i] * inv[i] : r[i];
+    z[i] = zi;
+    p[i] = zi;
+    s += r[i] * zi;
+  }
+  double v[1] = {s};
+  if (grid_reduce<1>(v, partials, counter))
+    if (threadIdx.x == 0) {
+      st->rz = v[0];
+      st->done = 0;
+    }
+}
+
+__global__ void k_cg_pap(const double* p, const double* ap, int64_t n, double* partials, unsigned int* counter,
+                         CgDev* st) {
+  if (st->done) return;
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s += p[i] * ap[i];
+  double v[1] = {s};
+  if (grid_reduce<1>(v, partials, counter))
+    if (threadIdx.x == 0) {
+      st->pap = v[0];
+      if (!(v[0] > 0.0)) {
+        st->fail = 1;
+        st->done = 1;
+      } else {
+        st->alpha = st->rz / v[0];
+      }
+    }
+}
+
+__global__ void k_cg_update(double* x, const double* p, double* r, const double* ap, const double* inv, double* z,
+                            int64_t n, double* partials, unsigned int* counter, CgDev* st, double* hist) {
+  if (st->done) return;
+  const double a = st->alpha;
+  double rr = 0.0, rz = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += a * p[i];
+    const double ri = r[i] - a * ap[i];
+    r[i] = ri;
+    const double zi = inv ? ri * inv[i] : ri;
+    z[i] = zi;
+    rr += ri * ri;
+    rz += ri * zi;
+  }
+  double v[2] = {rr, rz};
+  if (grid_reduce<2>(v, partials, counter))
+    if (threadIdx.x == 0) {
+      const int it = st->it + 1;
+      st->it = it;
+      const double h = sqrt(v[0]) / st->denom;
+      hist[it] = h;
+      if (h <= st->rtol) {
+        st->done = 1;
+        st->conv = 1;
+      } else {
+        st->beta = v[1] / st->rz;
+        st->rz = v[1];
+        if (it >= st->max_iter) st->done = 1;
+      }
+    }
+}
+
+__global__ void k_cg_p(const double* z, double* p, int64_t n, const CgDev* st) {
+  if (st->done) return;
+  const double b = st->beta;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z[i] + b * p[i];
+}
+
+__global__ void k_inv_diag(const double* d, double* inv, int64_t n, unsigned long long* first_zero) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = d[i];
+    if (v == 0.0) atomicMin(first_zero, static_cast<unsigned long long>(i));
+    inv[i] = 1.0 / v;
+  }
+}
+
+__global__ void k_precond(const double* r, const double* inv, double* z, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = inv ? r[i] * inv[i] : r[i];
+}
+
+__global__ void k_scale_into(const double* w, double inv_s, double* v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = w[i] / inv_s;
+}
+
+struct Timer {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  double seconds() const { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
+};
+
+template <class T>
+T fetch(Ctx& c, const T* d) {
+  T h{};
+  AFEM_CK(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+  AFEM_CK(cudaStreamSynchronize(c.stream));
+  return h;
+}
+
+// ||b - A x|| via a fresh apply; optionally keeps r = b - A x.
+double residual_norm(Operator& op, const double* b, const double* x, double* scratch, double* r) {
+  Ctx& c = *op.sys->ctx;
+  op.apply(x, scratch);
+  launch(c, k_residual_vec, red_grid(op.n), kRedThreads, 0, b, scratch, r, op.n, c.red_partials.p,
+         c.red_counter.p, c.red_out.p);
+  return fetch(c, c.red_out.p);
+}
+
+// JacobiPreconditioner::from_diagonal (krylov.hpp:83-92).
+void jacobi_inverse(Operator& op, DevArray<double>& inv) {
+  Ctx& c = *op.sys->ctx;
+  DevArray<double> d(op.n);
+  op.diagonal(d.p);
+  inv.alloc(op.n);
+  DevArray<unsigned long long> fz(1);
+  const unsigned long long init = ~0ull;
+  AFEM_CK(cudaMemcpyAsync(fz.p, &init, 8, cudaMemcpyHostToDevice, c.stream));
+  launch(c, k_inv_diag, grid_for(op.n, 256, 148 * 16), 256, 0, d.p, inv.p, op.n, fz.p);
+  const unsigned long long z = fetch(c, fz.p);
+  if (z != ~0ull) throw FactorizationError("jacobi: zero diagonal at row " + std::to_string(z));
+}
+
+void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const double* inv, SolveReport& rep) {
+  Ctx& c = *op.sys->ctx;
+  const int64_t n = op.n;
+  DevArray<double> r(n), z(n), p(n), ap(n), scratch(n), hist(cfg.max_iter + 2);
+  DevArray<CgDev> st(1);
+  const double bnorm = std::sqrt(dot(c, b, b, n));
+  const double denom = bnorm > 0.0 ? bnorm : 1.0;
+  double h0 = residual_norm(op, b, x, ap.p, r.p) / denom;
+  rep.history.assign(1, h0);
+  CgDev hs{};
+  hs.denom = denom;
+  hs.rtol = cfg.rtol;
+  hs.max_iter = cfg.max_iter;
+  hs.done = 1;
+  AFEM_CK(cudaMemcpyAsync(st.p, &hs, sizeof hs, cudaMemcpyHostToDevice, c.stream));
+  const unsigned rg = red_grid(n), eg = grid_for(n, 256, 148 * 16);
+  while (true) {
+    if (rep.history.back() > cfg.rtol && rep.iterations < cfg.max_iter) {
+      launch(c, k_cg_start, rg, kRedThreads, 0, r.p, inv, z.p, p.p, n, c.red_partials.p, c.red_counter.p, st.p);
+      int chunk = 4;
+      while (true) {
+        for (int k = 0; k < chunk; ++k) {
+          op.apply(p.p, ap.p);
+          launch(c, k_cg_pap, rg, kRedThreads, 0, p.p, ap.p, n, c.red_partials.p, c.red_counter.p, st.p);
+          launch(c, k_cg_update, rg, kRedThreads, 0, x, p.p, r.p, ap.p, inv, z.p, n, c.red_partials.p,
+                 c.red_counter.p, st.p, hist.p);
+          launch(c, k_cg_p, eg, 256, 0, z.p, p.p, n, st.p);
+        }
+        hs = fetch(c, st.p);
+        if (hs.done) break;
+        chunk = std::min(chunk * 2, 64);
+      }
+      const int it0 = rep.iterations;
+      rep.iterations = hs.it;
+      if (hs.it > it0) {
+        rep.history.resize(hs.it + 1);
+        AFEM_CK(cudaMemcpyAsync(rep.history.data() + it0 + 1, hist.p + it0 + 1, (hs.it - it0) * sizeof(double),
+                                cudaMemcpyDeviceToHost, c.stream));
+        AFEM_CK(cudaStreamSynchronize(c.stream));
+      }
+      if (hs.fail)
+        rep.failure = "cg: operator not positive definite (p^T A p <= 0 at iteration " +
+                      std::to_string(rep.iterations + 1) + ")";
+    }
+    const double true_rres = residual_norm(op, b, x, scratch.p, nullptr) / denom;
+    rep.history.back() = true_rres;
+    if (true_rres <= cfg.rtol) {
+      rep.converged = rep.failure.empty();
+      break;
+    }
+    if (!rep.failure.empty() || rep.iterations >= cfg.max_iter) break;
+    // recurrence drifted: restart from the fresh residual (krylov.hpp:402-404)
+    residual_norm(op, b, x, ap.p, r.p);
+    hs.done = 1;
+    hs.conv = 0;
+    AFEM_CK(cudaMemcpyAsync(&reinterpret_cast<CgDev*>(st.p)->conv, &hs.conv, sizeof(int), cudaMemcpyHostToDevice,
+                            c.stream));
+  }
+}
+
+void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const double* inv, SolveReport& rep) {
+  Ctx& c = *op.sys->ctx;
+  const int64_t n = op.n;
+  const int restart = static_cast<int>(std::min<int64_t>(cfg.restart, n));
+  const unsigned eg = grid_for(n, 256, 148 * 16);
+  DevArray<double> tmp(n), r(n), w(n), scratch(n), V(static_cast<size_t>(restart + 1) * n);
+  DevArray<double> hcol(restart + 2);
+  auto vec = [&](int k) { return V.p + static_cast<int64_t>(k) * n; };
+  const double bnorm = std::sqrt(dot(c, b, b, n));
+  const double denom = bnorm > 0.0 ? bnorm : 1.0;
+  launch(c, k_precond, eg, 256, 0, b, inv, tmp.p, n);
+  const double pnorm = std::sqrt(dot(c, tmp.p, tmp.p, n));
+  const double pdenom = pnorm > 0.0 ? pnorm : 1.0;
+  std::vector<double> h(static_cast<size_t>(restart + 1) * restart, 0.0), cs(restart), sn(restart), g(restart + 1);
+  auto H = [&](int i, int j) -> double& { return h[static_cast<size_t>(i) * restart + j]; };
+
+  double true_rres = residual_norm(op, b, x, tmp.p, r.p) / denom;
+  launch(c, k_precond, eg, 256, 0, r.p, inv, w.p, n);
+  rep.history.push_back(std::sqrt(dot(c, w.p, w.p, n)) / pdenom);
+
+  while (true_rres > cfg.rtol && rep.iterations < cfg.max_iter && rep.failure.empty()) {
+    launch(c, k_precond, eg, 256, 0, r.p, inv, w.p, n);
+    const double beta = std::sqrt(dot(c, w.p, w.p, n));
+    if (beta == 0.0) break;
+    const double target_est = beta * std::min(1.0, 0.5 * cfg.rtol / true_rres);  // krylov.hpp:454
+    launch(c, k_scale_into, eg, 256, 0, w.p, beta, vec(0), n);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int j = 0, cols = 0;
+    for (; j < restart && rep.iterations < cfg.max_iter; ++j) {
+      op.apply(vec(j), tmp.p);
+      launch(c, k_precond, eg, 256, 0, tmp.p, inv, w.p, n);
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, scalars stay on the device
+        dot_dev(c, vec(i), w.p, n, hcol.p + i);
+        add_scaled_dev(c, hcol.p + i, -1.0, vec(i), w.p, n);
+      }
+      dot_dev(c, w.p, w.p, n, hcol.p + j + 1);
+      std::vector<double> hc(j + 2);
+      AFEM_CK(cudaMemcpyAsync(hc.data(), hcol.p, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+      AFEM_CK(cudaStreamSynchronize(c.stream));
+      for (int i = 0; i <= j; ++i) H(i, j) = hc[i];
+      const double hnext = std::sqrt(hc[j + 1]);
+      H(j + 1, j) = hnext;
+      const bool happy = hnext <= beta * 1e-16;
+      if (!happy) launch(c, k_scale_into, eg, 256, 0, w.p, hnext, vec(j + 1), n);
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * H(i, j) + sn[i] * H(i + 1, j);
+        H(i + 1, j) = -sn[i] * H(i, j) + cs[i] * H(i + 1, j);
+        H(i, j) = t;
+      }
+      const double rr = std::hypot(H(j, j), H(j + 1, j));
+      if (rr == 0.0) {
+        cs[j] = 1.0;
+        sn[j] = 0.0;
+      } else {
+        cs[j] = H(j, j) / rr;
+        sn[j] = H(j + 1, j) / rr;
+      }
+      H(j, j) = rr;
+      H(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] *= cs[j];
+      ++rep.iterations;
+      cols = j + 1;
+      const double est = std::abs(g[j + 1]);
+      rep.history.push_back(est / pdenom);
+      if (est <= target_est || happy) {
+        ++j;
+        break;
+      }
+    }
+    std::vector<double> y(cols, 0.0);
+    for (int i = cols - 1; i >= 0; --i) {
+      double s = g[i];
+      for (int k = i + 1; k < cols; ++k) s -= H(i, k) * y[k];
+      if (H(i, i) == 0.0) {
+        rep.failure = "gmres: singular least-squares system in restart cycle";
+        break;
+      }
+      y[i] = s / H(i, i);
+    }
+    if (!rep.failure.empty()) break;
+    for (int k = 0; k < cols; ++k) axpy(c, y[k], vec(k), x, n);
+    true_rres = residual_norm(op, b, x, tmp.p, r.p) / denom;
+  }
+  true_rres = residual_norm(op, b, x, scratch.p, nullptr) / denom;
+  rep.history.push_back(true_rres);
+  rep.converged = rep.failure.empty() && true_rres <= cfg.rtol;
+}
+
+}  // namespace
+
+void validate_cfg(const SolverCfg& c) {  // SolverConfig::validate (krylov.hpp:50-54)
+  if (!(c.rtol > 0.0)) throw std::invalid_argument("solver config: rtol must be > 0");
+  if (c.max_iter < 1) throw std::invalid_argument("solver config: max_iter must be >= 1");
+  if (c.restart < 1) throw std::invalid_argument("solver config: gmres_restart must be >= 1");
+}
+
+// run_solver (backend.hpp:241-286), iterative methods. x0 may alias x.
+void solve(Operator& op, const SolverCfg& cfg, const double* b, const double* x0, double* x, SolveReport& rep) {
+  validate_cfg(cfg);
+  if (cfg.method != 0 && cfg.method != 1)
+    throw CapabilityError("run_solver: only CG and GMRES are provided on the device");
+  if (cfg.precond != 0 && cfg.precond != 1) throw CapabilityError("run_solver: ILU0 is not provided on the device");
+  op.validate();
+  Timer timer;
+  Ctx& c = *op.sys->ctx;
+  DevArray<double> inv;
+  if (cfg.precond == 1) jacobi_inverse(op, inv);
+  if (x0) copy(c, x0, x, op.n);
+  else fill(c, 0.0, x, op.n);
+  if (cfg.method == 0) cg(op, cfg, b, x, inv.p, rep);
+  else gmres(op, cfg, b, x, inv.p, rep);
+  AFEM_CK(cudaStreamSynchronize(c.stream));
+  rep.wall_time = timer.seconds();
+}
+
+}  // namespace afem

@@ -1,0 +1,284 @@
+"""GPU parity tests: the CUDA path through the C ABI against the oracle.
+
+2D quad4 cases are checked against golden vectors produced by the REFERENCE itself
+(tests/golden/*.npz, see make_golden.py); 3D hex8 cases against the CPU restatement (oracle/).
+Tolerances: integer outputs bit-exact; residuals, tangents, operator actions
+<= 1e-12 normwise-relative; converged displacements <= 1e-8 relative at equal solver tolerance.
+"""
+import numpy as np
+import pytest
+
+from oracle.pyoracle import Oracle
+from tests.helpers import LINEAR, SVK_MIX, bc_state, golden_cases, load, random_vector, rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+TOL_U = 1e-8
+
+
+@pytest.fixture(scope="module")
+def afem():
+    import paper_2604_22087_b200 as m
+    m.load()
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(afem):
+    return afem.Context(0)
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle("restate")
+
+
+def golden_system(afem, ctx, g):
+    mats = [(int(m[0]), m[1], m[2]) for m in g["mats"]]
+    n = int(g["n"])
+    s = afem.System.grid(ctx, 2, n, n, materials=mats)
+    s.set_dirichlet(g["bc_node"], g["bc_comp"], g["bc_val"])
+    return s
+
+
+# ----------------------------------------------------------------------------- 2D vs the reference
+
+@pytest.mark.parametrize("path", golden_cases())
+def test_golden_integer_outputs_bit_exact(afem, ctx, path):
+    g = load(path)
+    s = golden_system(afem, ctx, g)
+    coords, conn, phase = s.mesh()
+    assert np.array_equal(coords, g["coords"])
+    assert np.array_equal(conn, g["conn"]) and np.array_equal(phase, g["phase"])
+    rp, rows, cols = s.pattern()
+    assert np.array_equal(rp, g["row_ptr"]) and np.array_equal(rows, g["rows"]) and np.array_equal(cols, g["cols"])
+    # the same system built from host arrays (afem_system_create) gives the same pattern
+    s2 = afem.System(ctx, 2, g["coords"], g["conn"], g["phase"], [(int(m[0]), m[1], m[2]) for m in g["mats"]])
+    assert all(np.array_equal(a, b) for a, b in zip(s2.pattern(), (rp, rows, cols)))
+
+
+@pytest.mark.parametrize("path", golden_cases())
+def test_golden_assembly(afem, ctx, path):
+    g = load(path)
+    s = golden_system(afem, ctx, g)
+    u, x = g["u"], g["x"]
+    assert rel_err(s.residual(u), g["residual"]) <= TOL
+    assert rel_err(s.jacobian(u), g["jacobian"]) <= TOL
+    assert rel_err(s.diagonal(u), g["diagonal"]) <= TOL
+    v, r = s.eliminate(g["jacobian"], g["residual"], u)
+    assert rel_err(v, g["elim_values"]) <= TOL and rel_err(r, g["elim_rhs"]) <= TOL
+    assert rel_err(s.csr_apply(g["elim_values"], x), g["csr_apply"]) <= TOL
+    op = afem.matrix_free_operator(s, u)
+    assert not op.uses_stencil  # SVK state: general node-centric kernel
+    assert rel_err(op.apply(x), g["mf_apply"]) <= TOL
+    assert rel_err(op.diagonal(), g["mf_diagonal"]) <= TOL
+
+
+@pytest.mark.parametrize("path", golden_cases())
+def test_golden_solvers(afem, ctx, path):
+    g = load(path)
+    s = golden_system(afem, ctx, g)
+    vals = afem.Values(s).assemble(g["u"])
+    rhs = vals.eliminate(g["residual"], g["u"])
+    assert rel_err(rhs, g["elim_rhs"]) <= TOL
+    buf = afem.HandoffBuffer(s)
+    buf.handoff(vals)
+    op = afem.explicit_operator(buf)
+    x, rep = afem.run_solver(op, -g["elim_rhs"], method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
+    assert rep["converged"]
+    assert abs(rep["iterations"] - int(g["cg_iterations"])) <= 2
+    assert rel_err(x, g["x_cg"]) <= TOL_U
+    xg, repg = afem.run_solver(op, -g["elim_rhs"], method=afem.GMRES, precond=afem.JACOBI, rtol=1e-10)
+    assert repg["converged"] and rel_err(xg, g["x_gmres"]) <= TOL_U
+    buf.release()
+    u, rb = s.solve_bvp(rtol=1e-10, lin_rtol=1e-12)
+    assert rb["converged"] and rb["iterations"] == int(g["bvp_iterations"])
+    assert rel_err(u, g["u_bvp"]) <= TOL_U
+    um, rm = s.solve_bvp(rtol=1e-10, lin_rtol=1e-12, operator_kind=afem.MATRIX_FREE)
+    assert rm["converged"] and rel_err(um, g["u_bvp_mf"]) <= TOL_U
+
+
+def test_config1_against_reference_library(afem, ctx):
+    """Config 1 (64x64 quad4, linear E 1/10): GPU vs the reference compiled in place (or restatement)."""
+    from oracle.pyoracle import available
+    R = Oracle("ref" if available("ref") else "restate")
+    mesh = R.mesh2d(64, 64)
+    bc = R.bcs(2, 64, 64, 0, 1.0, 0.01)
+    rs = R.system(2, *mesh, LINEAR, grid=(64, 64, 0, 1.0, 1.0, 1.0))
+    rs.set_dirichlet(*bc)
+    s = afem.System.grid(ctx, 2, 64, 64, materials=LINEAR)
+    s.set_benchmark_dirichlet(0.01)
+    assert all(np.array_equal(a, b) for a, b in zip(s.pattern(), rs.pattern()))
+    u = bc_state(s.n, 2, *bc)
+    x = random_vector(s.n, 1.0, 12345)
+    op = afem.matrix_free_operator(s, u)
+    assert rel_err(op.apply(x), rs.mf_apply(u, x)) <= TOL
+    ur, rr = rs.solve_bvp(rtol=1e-10, lin_rtol=1e-8)
+    ug, rg = s.solve_bvp(rtol=1e-10, lin_rtol=1e-8)
+    assert rg["converged"] and rel_err(ug, ur) <= TOL_U
+    um, rm = s.solve_bvp(rtol=1e-10, lin_rtol=1e-8, operator_kind=afem.MATRIX_FREE)
+    assert rm["converged"] and rel_err(um, ur) <= TOL_U
+
+
+# ----------------------------------------------------------------------------- 3D vs the restatement
+
+def hex_case(afem, ctx, orc, n, mats, n_fibres=4, radius=0.2, strain=0.01):
+    fib = afem.fibres(12345, n_fibres)
+    s = afem.System.grid(ctx, 3, n, n, n, inclusions=fib, radius=radius, materials=mats)
+    s.set_benchmark_dirichlet(strain)
+    coords, conn, phase = s.mesh()
+    oc, on, op_ = orc.mesh3d(n, n, n, fib, radius)
+    assert np.array_equal(coords, oc) and np.array_equal(conn, on) and np.array_equal(phase, op_)
+    o = orc.system(3, coords, conn, phase, mats, grid=(n, n, n, 1.0, 1.0, 1.0))
+    o.set_dirichlet(*orc.bcs(3, n, n, n, 1.0, strain))
+    return s, o
+
+
+@pytest.mark.parametrize("mats", [SVK_MIX, LINEAR], ids=["svk", "linear"])
+def test_hex8_assembly_parity(afem, ctx, orc, mats):
+    s, o = hex_case(afem, ctx, orc, 5, mats)
+    assert all(np.array_equal(a, b) for a, b in zip(s.pattern(), o.pattern()))
+    for (ia, da), (ib, db) in zip(s.batches(), o.batches()):
+        assert np.array_equal(ia, ib) and np.array_equal(da, db)
+    u = s.impose_dirichlet(random_vector(s.n, 0.01, 3))
+    x = random_vector(s.n, 1.0, 4)
+    assert rel_err(s.residual(u), o.residual(u)) <= TOL
+    K = s.jacobian(u)
+    assert rel_err(K, o.jacobian(u)) <= TOL
+    assert rel_err(s.diagonal(u), o.diagonal(u)) <= TOL
+    v, r = s.eliminate(K, s.residual(u), u)
+    vo, ro = o.eliminate(o.jacobian(u), o.residual(u), u)
+    assert rel_err(v, vo) <= TOL and rel_err(r, ro) <= TOL
+    assert rel_err(s.csr_apply(v, x), o.csr_apply(vo, x)) <= TOL
+    op = afem.matrix_free_operator(s, u)
+    assert rel_err(op.apply(x), o.mf_apply(u, x)) <= TOL
+    assert rel_err(op.diagonal(), o.mf_diagonal(u)) <= TOL
+
+
+def test_hex8_newton_parity(afem, ctx, orc):
+    s, o = hex_case(afem, ctx, orc, 4, SVK_MIX, strain=0.02)
+    for kind in (0, 1):
+        ug, rg = s.solve_bvp(rtol=1e-10, lin_rtol=1e-12, operator_kind=kind)
+        uo, ro = o.solve_bvp(rtol=1e-10, lin_rtol=1e-12, operator_kind=kind)
+        assert rg["converged"] and ro["converged"]
+        assert rg["iterations"] == ro["iterations"]
+        assert rel_err(ug, uo) <= TOL_U
+
+
+def test_hex8_gmres_and_load_stepping(afem, ctx, orc):
+    s, o = hex_case(afem, ctx, orc, 4, SVK_MIX, strain=0.03)
+    ug, rg = s.load_stepping(0.03, 3, method=afem.GMRES, lin_rtol=1e-12)
+    uo, ro = o.load_stepping(0.03, 3, method=1, lin_rtol=1e-12)
+    assert rg["converged"] and ro["converged"]
+    assert list(rg["step_iterations"]) == list(ro["step_iterations"])
+    assert rel_err(ug, uo) <= TOL_U
+
+
+# ----------------------------------------------------------------------------- semantics
+
+def test_determinism_bitwise(afem, ctx, orc):
+    """Repeated assembly is bitwise identical (reference test_assembly.cpp:262-276)."""
+    s, _ = hex_case(afem, ctx, orc, 6, SVK_MIX)
+    u = s.impose_dirichlet(random_vector(s.n, 0.01, 8))
+    r1, r2 = s.residual(u), s.residual(u)
+    k1, k2 = s.jacobian(u), s.jacobian(u)
+    assert r1.tobytes() == r2.tobytes() and k1.tobytes() == k2.tobytes()
+    op = afem.matrix_free_operator(s, u)
+    x = random_vector(s.n, 1.0, 9)
+    assert op.apply(x).tobytes() == op.apply(x).tobytes()
+
+
+def test_lease_protocol(afem, ctx):
+    """backend.hpp:33-111 / test_backend.cpp:36-168."""
+    s = afem.System.grid(ctx, 2, 3, 3, materials=SVK_MIX)
+    s.set_benchmark_dirichlet(0.01)
+    u = s.impose_dirichlet(np.zeros(s.n))
+    buf = afem.HandoffBuffer(s)
+    assert buf.epoch == 0 and buf.state == buf.OwnedByAssembly
+    with pytest.raises(afem.LeaseError):
+        afem.explicit_operator(buf)
+    for cycle in range(1, 4):
+        v = afem.Values(s).assemble(u)
+        ptr = v.device_ptr()
+        buf.handoff(v)
+        assert buf.epoch == cycle and buf.state == buf.LeasedToSolver
+        assert buf.solver_values() == ptr  # aliased, not copied
+        with pytest.raises(afem.LeaseError):
+            buf.assembly_values()
+        buf.release()
+        with pytest.raises(afem.LeaseError):
+            buf.solver_values()
+    with pytest.raises(afem.LeaseError):
+        buf.release()
+    buf.handoff(afem.Values(s).assemble(u))
+    op = afem.explicit_operator(buf)
+    op.apply(np.ones(s.n))
+    with pytest.raises(afem.LeaseError):
+        buf.handoff(afem.Values(s).assemble(u))
+    buf.release()
+    with pytest.raises(afem.LeaseError):
+        op.apply(np.ones(s.n))
+    buf.handoff(afem.Values(s).assemble(u))
+    with pytest.raises(afem.StaleEpochError):
+        op.apply(np.ones(s.n))
+    mf = afem.matrix_free_operator(s, u)
+    with pytest.raises(afem.CapabilityError):
+        mf.csr_values_ptr()
+
+
+def test_error_semantics(afem, ctx):
+    with pytest.raises(afem.InvalidArgument):
+        afem.System.grid(ctx, 2, 0, 3)
+    s = afem.System.grid(ctx, 2, 2, 2, materials=SVK_MIX)
+    with pytest.raises(afem.OutOfRange):
+        s.set_dirichlet([99], [0], [0.0])
+    with pytest.raises(afem.InvalidArgument):
+        s.set_dirichlet([0, 0], [1, 1], [0.0, 0.0])
+    with pytest.raises(afem.InvalidArgument):  # no material for phase 1
+        afem.System.grid(ctx, 2, 4, 4, materials=[(0, 1.0, 0.3)])
+    # inverted element under SVK -> InvertedElementError (material.hpp:51-52)
+    u = np.zeros(s.n)
+    coords = s.mesh()[0]
+    u[0::2] = -3.0 * coords[0::2]
+    with pytest.raises(afem.InvertedElementError):
+        s.residual(u)
+    # degenerate geometry -> invalid_argument (element.hpp:87-88)
+    bad = np.array([0, 0, 1, 0, 1, 1, 0, 1], np.float64)
+    sb = afem.System(ctx, 2, bad, np.array([0, 3, 2, 1], np.int32), np.array([0], np.int32), [(0, 1.0, 0.3)])
+    with pytest.raises(afem.InvalidArgument):
+        sb.residual(np.zeros(8))
+    # zero diagonal -> FactorizationError naming the row (krylov.hpp:87-88)
+    s2 = afem.System.grid(ctx, 2, 2, 2, materials=SVK_MIX)
+    buf = afem.HandoffBuffer(s2)
+    buf.handoff(afem.Values(s2))  # all-zero values
+    op = afem.explicit_operator(buf)
+    with pytest.raises(afem.FactorizationError, match="row 0"):
+        afem.run_solver(op, np.ones(s2.n), precond=afem.JACOBI)
+    # indefinite operator -> failure string, not an exception (krylov.hpp:377-381)
+    buf.release()
+    s2.set_benchmark_dirichlet(0.0)
+    u0 = np.zeros(s2.n)
+    vals, _ = s2.eliminate(s2.jacobian(u0), s2.residual(u0), u0)
+    neg = afem.Values(s2).set(-vals)
+    buf2 = afem.HandoffBuffer(s2)
+    buf2.handoff(neg)
+    x, rep = afem.run_solver(afem.explicit_operator(buf2), np.ones(s2.n), method=afem.CG)
+    assert not rep["converged"] and "not positive definite" in rep["failure"]
+
+
+def test_zero_rhs_converges_immediately(afem, ctx):
+    s = afem.System.grid(ctx, 2, 4, 4, materials=LINEAR)
+    s.set_benchmark_dirichlet(0.01)
+    op = afem.matrix_free_operator(s, np.zeros(s.n))
+    x, rep = afem.run_solver(op, np.zeros(s.n), precond=afem.JACOBI)
+    assert rep["converged"] and rep["iterations"] == 0 and np.all(x == 0)
+
+
+def test_linear_newton_takes_one_iteration(afem, ctx):
+    """test_newton.cpp:32-42."""
+    s = afem.System.grid(ctx, 2, 8, 8, materials=LINEAR)
+    s.set_benchmark_dirichlet(0.01)
+    u, rep = s.solve_bvp(rtol=1e-10, lin_rtol=1e-13)
+    assert rep["converged"] and rep["iterations"] == 1
+    assert rep["residual_norms"][-1] <= 10 * 1e-13 * rep["residual_norms"][0]
