@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""bench.py — BASELINE.json metric: matrix-free operator DOFs/s & CG solve time.
+
+Workload (BASELINE.json configs[1], "config 2"): 3D linear-elastic hex8 RVE, 128^3 elements
+(6.44 M dofs), random z-parallel fibres from mt19937_64(12345) (E_m = 1, E_f = 10, nu = 0.3),
+benchmark BCs at 1% strain, state u0 = BC-consistent; fp64 matrix-free K(u0) x and Jacobi-PCG.
+
+  step      one matrix-free operator apply y = K x over the whole mesh (inputs resident in HBM);
+            L2 is flushed (256 MiB write) between timed applies, outside the timed events
+  value     whole-job DOFs/s = n_dof * steps * n_gpus / max-over-ranks(sum of apply times)
+  e2e       the same metric through the C ABI (afem_op_apply) with pinned HOST x/y buffers:
+            H2D of x and D2H of y inside every step
+  cg        one Jacobi-PCG solve (rtol 1e-8) of K du = -R(u0) on the device: solve time,
+            iterations, true relative residual
+  roofline  HBM: SURVEY §8(d) algorithmic bytes B_MF = 17 n_dof + 33 n_elem per apply; FP64:
+            F_MF = 2 nnz(K) per apply against the live-probed DFMA peak
+  cpu_baseline  the CPU restatement (oracle/, the reference has no hex8) timed on this host's
+            cores on a z-slab sample of the same mesh (min over 3 reps)
+
+--impl reference runs the CPU path only (oracle port, all host threads) on the same metric/config.
+Multi-GPU (torchrun, N > 1): each rank owns one 128^3 subdomain replica (weak scaling; the slab
+halo exchange is not yet on this path — see DESIGN.md §Multi-GPU).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "matrix-free operator DOFs/s & CG solve time at 1/2/4/8 B200 vs host-CPU ref"
+UNIT = "DOF/s"
+SEED = 12345
+N_FIBRES = 40
+RADIUS = 0.05
+MATS = [(0, 1.0, 0.3), (0, 10.0, 0.3)]
+STRAIN = 0.01
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=128, help="elements per axis")
+    p.add_argument("--no-cg", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=10)
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(n):
+    """dram bytes per apply of the dominant kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    rec = d.get(f"n{n}")
+    return None if rec is None else rec.get("dram_bytes_per_apply")
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,utilization.gpu")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 6]
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        sm, mx, reasons, loaded = [], None, set(), []
+        for r in rows:
+            try:
+                c, m, util = float(r[0]), float(r[1]), float(r[6])
+            except ValueError:
+                continue
+            mx = m
+            sm.append(c)
+            if util > 0:
+                loaded.append(c)
+            for k, nm in enumerate(names):
+                if "Active" == r[2 + k].strip():
+                    reasons.add(nm)
+        use = loaded or sm
+        return {"sm_mhz": float(np.median(use)) if use else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "samples_under_load": len(loaded)}
+
+
+def host_mesh_slab(sys_, n, nz_s):
+    """First nz_s element layers of the GPU-generated mesh (node / element arrays are k-major)."""
+    coords, conn, phase = sys_.mesh()
+    nn = (n + 1) * (n + 1) * (nz_s + 1)
+    ne = n * n * nz_s
+    return coords[: 3 * nn], conn[: 8 * ne], phase[:ne]
+
+
+def cpu_sample(n, nz_s, threads, reps, mesh_arrays=None):
+    """Time the CPU restatement's matrix-free apply on a z-slab sample; returns (DOF/s, seconds, n_dof)."""
+    from oracle.pyoracle import Oracle, build
+    build()
+    orc = Oracle("restate")
+    if mesh_arrays is None:
+        fib = orc.fibres(SEED, N_FIBRES)
+        coords, conn, phase = orc.mesh3d(n, n, nz_s, fib, RADIUS, lz=nz_s / n)
+    else:
+        coords, conn, phase = mesh_arrays
+    s = orc.system(3, coords, conn, phase, MATS, lite=True)
+    node, comp, val = orc.bcs(3, n, n, nz_s, 1.0, STRAIN)
+    s.set_dirichlet(node, comp, val)
+    u = np.zeros(s.n)
+    u[3 * node + comp] = val
+    x = np.random.default_rng(SEED).uniform(-1.0, 1.0, s.n)
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        s.mf_apply(u, x, nthreads=threads)
+        best = min(best, time.perf_counter() - t0)
+    return s.n / best, best, s.n
+
+
+def pick_slab(n, threads, target_s):
+    """Calibrate the slab thickness so one CPU apply takes about target_s seconds."""
+    _, t, _ = cpu_sample(n, 1, threads, 1)
+    return max(1, min(n, int(target_s / max(t, 1e-6))))
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the CPU path (oracle port) on this host's cores, rank 0 only."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    nz_s = pick_slab(args.n, threads, 1.0)
+    for _ in range(args.warmup):
+        cpu_sample(args.n, nz_s, threads, 1)
+    times = []
+    dofs = 0
+    for _ in range(args.steps):
+        _, t, dofs = cpu_sample(args.n, nz_s, threads, 1)
+        times.append(t)
+    T = sum(times)
+    value = dofs * len(times) / T
+    sample = f"z-slab {args.n}x{args.n}x{nz_s} elements ({dofs} dofs) of the {args.n}^3 workload, one MF apply per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C2 hex8 {args.n}^3 linear-elastic fibre RVE, matrix-free K(u0)x (CPU port)",
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2604_22087_b200 as afem
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    stream = torch.cuda.current_stream()
+    ctx = afem.Context(local_rank, stream=stream)
+    n = args.n
+    fib = afem.fibres(SEED, N_FIBRES)
+    sys_ = afem.System.grid(ctx, 3, n, n, n, inclusions=fib, radius=RADIUS, materials=MATS)
+    sys_.set_benchmark_dirichlet(STRAIN)
+    n_dof, n_elem = sys_.n, sys_.info.n_elem
+    u0 = sys_.impose_dirichlet(np.zeros(n_dof))
+    op = afem.matrix_free_operator(sys_, u0)
+    assert op.uses_stencil, "structured stencil path not selected"
+    vf = float(sys_.mesh()[2].mean())
+
+    g = torch.Generator(device="cuda").manual_seed(SEED + rank)
+    x = torch.rand(n_dof, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    y = torch.empty_like(x)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+
+    for _ in range(args.warmup):
+        op.apply_device(x.data_ptr(), y.data_ptr())
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    l0 = ctx.launches
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        evs[k][0].record(stream)
+        op.apply_device(x.data_ptr(), y.data_ptr())
+        evs[k][1].record(stream)
+    launches = ctx.launches - l0
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    T = sum(ms)
+    if dist:
+        t = torch.tensor([T], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        T = float(t.item())
+        dist.barrier()
+    t_apply = T / args.steps * 1e-3  # s per apply (max over ranks)
+    value = world * n_dof * args.steps / (T * 1e-3)
+
+    # CG solve time (device-resident, Jacobi-PCG, rtol 1e-8): K du = -R(u0)
+    cg = None
+    if not args.no_cg:
+        r0 = torch.from_numpy(sys_.constrain_residual(sys_.residual(u0), u0)).cuda()
+        b = -r0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        du, rep = afem.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        solve_s = e0.elapsed_time(e1) * 1e-3
+        cg = {"solve_s": solve_s, "iterations": rep["iterations"], "converged": rep["converged"],
+              "true_rel_residual": float(rep["residual_history"][-1]), "rtol": 1e-8, "precond": "jacobi",
+              "ms_per_iteration": 1e3 * solve_s / max(rep["iterations"], 1)}
+    clk = clocks.stop()
+
+    # end to end through the C ABI with pinned host buffers
+    xh = x.cpu().pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    lib = afem.load()
+    import ctypes as C
+    for _ in range(2):
+        lib.afem_op_apply(op.h, C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr()))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        st = lib.afem_op_apply(op.h, C.c_void_p(xh.data_ptr()), C.c_void_p(yh.data_ptr()))
+        assert st == 0, lib.afem_last_error()
+    te = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([te], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        te = float(t.item())
+    e2e = {"value": world * n_dof * args.e2e_steps / te, "unit": UNIT, "h2d_bytes_per_step": 8 * n_dof,
+           "d2h_bytes_per_step": 8 * n_dof, "path": "afem_op_apply(op, pinned host x, pinned host y)"}
+    if cg is not None:
+        bh = b.cpu().numpy()
+        t0 = time.perf_counter()
+        _, rep2 = afem.run_solver(op, bh, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
+        e2e["cg_solve_s"] = time.perf_counter() - t0
+        e2e["cg_iterations"] = rep2["iterations"]
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    hbm_peak, peak_src = peaks()
+    b_mf = 17 * n_dof + 33 * n_elem
+    achieved = b_mf / t_apply / 1e9
+    fp64_peak = ctx.probe_fp64_tflops()
+    f_mf = 2.0 * sys_.nnz
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "traffic": ncu_traffic(n), "peak_source": peak_src,
+            "algorithmic_bytes_per_apply": b_mf, "kernel": "matrix-free apply (k_stencil_main + edge + fix)",
+            "fp64": {"achieved_tflops": f_mf / t_apply / 1e12, "peak_tflops": fp64_peak,
+                     "frac": f_mf / t_apply / 1e12 / fp64_peak, "flops_per_apply": f_mf,
+                     "peak_source": "measured live (afem_probe_fp64 DFMA chains)"}}
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        nz_s = pick_slab(n, threads, 2.0)
+        val, t, dofs = cpu_sample(n, nz_s, threads, 3, mesh_arrays=host_mesh_slab(sys_, n, nz_s))
+        cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"z-slab {n}x{n}x{nz_s} elements ({dofs} dofs) of the same mesh, MF apply, min of 3"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_apply, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C2 hex8 {n}^3 linear-elastic fibre RVE, matrix-free K(u0)x + Jacobi-PCG",
+                   "elements": n_elem, "n_dof": n_dof, "nnz_K": sys_.nnz, "fibres": N_FIBRES, "radius": RADIUS,
+                   "fibre_volume_fraction": vf, "E": [1.0, 10.0], "nu": 0.3, "strain": STRAIN,
+                   "l2": "flushed (256 MiB write) between timed applies",
+                   "parallelism": f"{world} independent subdomain(s), one per GPU"},
+        "cg": cg, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+    else:
+        ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -125,6 +125,8 @@ afem_status afem_ctx_set_stream(afem_ctx ctx, void* cuda_stream);
 afem_status afem_ctx_synchronize(afem_ctx ctx);
 /* Number of kernels this context has launched (evidence counter for bench.py). */
 afem_status afem_ctx_launch_count(afem_ctx ctx, int64_t* count);
+/* Measured FP64 FMA throughput of this device in TFLOP/s (the FP64 roofline denominator). */
+afem_status afem_probe_fp64(afem_ctx ctx, double* tflops);
 
 /* ------------------------------------------------------------------ mesh / system (L2-L3) */
 /* Fibre centres U(0,lx)xU(0,ly) from mt19937_64(seed) (SURVEY §8d config 2 generator). Host only. */

@@ -95,8 +95,21 @@ int64_t orc_bcs(int32_t dim, int32_t nx, int32_t ny, int32_t nz, double lx, doub
   return st == ORC_OK ? n : -(int64_t)st;
 }
 
+static void* create(int32_t dim, int64_t n_nodes, int64_t n_elem, const double* coords, const int32_t* conn,
+                    const int32_t* phase, int32_t n_mat, const orc_material* mats, bool pattern);
+
 void* orc_system_create(int32_t dim, int64_t n_nodes, int64_t n_elem, const double* coords, const int32_t* conn,
                         const int32_t* phase, int32_t n_mat, const orc_material* mats) {
+  return create(dim, n_nodes, n_elem, coords, conn, phase, n_mat, mats, true);
+}
+
+void* orc_system_create_lite(int32_t dim, int64_t n_nodes, int64_t n_elem, const double* coords,
+                             const int32_t* conn, const int32_t* phase, int32_t n_mat, const orc_material* mats) {
+  return create(dim, n_nodes, n_elem, coords, conn, phase, n_mat, mats, false);
+}
+
+static void* create(int32_t dim, int64_t n_nodes, int64_t n_elem, const double* coords, const int32_t* conn,
+                    const int32_t* phase, int32_t n_mat, const orc_material* mats, bool pattern) {
   orc::System* out = nullptr;
   guarded([&] {
     if (dim != 2 && dim != 3) throw std::invalid_argument("system: dim must be 2 or 3");
@@ -112,7 +125,7 @@ void* orc_system_create(int32_t dim, int64_t n_nodes, int64_t n_elem, const doub
       s->materials.push_back(m);
     }
     s->batches = orc::build_batches(s->mesh, s->materials);
-    s->pattern = orc::precompute_sparsity(s->batches, s->n_dof(), dim);
+    if (pattern) s->pattern = orc::precompute_sparsity(s->batches, s->n_dof(), dim);
     s->table = orc::constraint_table({}, s->n_dof(), dim);
     out = s.release();
   });

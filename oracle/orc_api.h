@@ -100,6 +100,11 @@ int64_t orc_bcs(int32_t dim, int32_t nx, int32_t ny, int32_t nz, double lx, doub
 void* orc_system_create(int32_t dim, int64_t n_nodes, int64_t n_elem, const double* coords,
                         const int32_t* conn, const int32_t* phase, int32_t n_mat,
                         const orc_material* mats);
+/* Same, without the sparsity pattern (sort of 576 pairs/element is infeasible at 128^3): only the
+ * residual / matrix-free entry points are valid. Used for bench.py's CPU baseline. */
+void* orc_system_create_lite(int32_t dim, int64_t n_nodes, int64_t n_elem, const double* coords,
+                             const int32_t* conn, const int32_t* phase, int32_t n_mat,
+                             const orc_material* mats);
 /* structured-grid metadata so benchmark_bcs / load_stepping can regenerate loads */
 int32_t orc_system_set_grid(void* sys, int32_t nx, int32_t ny, int32_t nz, double lx, double ly,
                             double lz);

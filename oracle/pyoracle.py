@@ -89,6 +89,8 @@ class Oracle:
         L.orc_system_create.restype = C.c_void_p
         L.orc_system_create.argtypes = [C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
                                         C.c_void_p, C.c_int32, C.c_void_p]
+        L.orc_system_create_lite.restype = C.c_void_p
+        L.orc_system_create_lite.argtypes = L.orc_system_create.argtypes
         for name in ["orc_system_destroy"]:
             getattr(L, name).argtypes = [C.c_void_p]
             getattr(L, name).restype = None
@@ -166,12 +168,12 @@ class Oracle:
         self.lib.orc_bcs(dim, nx, ny, nz, lx, strain, _p(node, C.c_int32), _p(comp, C.c_int32), _p(val))
         return node, comp, val
 
-    def system(self, dim, coords, conn, phase, mats, grid=None):
-        return OracleSystem(self, dim, coords, conn, phase, mats, grid)
+    def system(self, dim, coords, conn, phase, mats, grid=None, lite=False):
+        return OracleSystem(self, dim, coords, conn, phase, mats, grid, lite)
 
 
 class OracleSystem:
-    def __init__(self, orc: Oracle, dim, coords, conn, phase, mats, grid=None):
+    def __init__(self, orc: Oracle, dim, coords, conn, phase, mats, grid=None, lite=False):
         self.o = orc
         L = orc.lib
         self.dim = dim
@@ -181,8 +183,9 @@ class OracleSystem:
         n_nodes = len(self.coords) // dim
         n_elem = len(self.phase)
         m = materials_array(mats)
-        h = L.orc_system_create(dim, n_nodes, n_elem, _p(self.coords), _p(self.conn, C.c_int32),
-                                _p(self.phase, C.c_int32), len(mats), m)
+        create = L.orc_system_create_lite if lite else L.orc_system_create
+        h = create(dim, n_nodes, n_elem, _p(self.coords), _p(self.conn, C.c_int32),
+                   _p(self.phase, C.c_int32), len(mats), m)
         if not h:
             raise OracleError(-1, L.orc_last_error().decode())
         self.h = h

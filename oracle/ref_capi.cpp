@@ -163,6 +163,11 @@ void* orc_system_create(int32_t dim, int64_t n_nodes, int64_t n_elem, const doub
   return out;
 }
 
+void* orc_system_create_lite(int32_t dim, int64_t n_nodes, int64_t n_elem, const double* coords,
+                             const int32_t* conn, const int32_t* phase, int32_t n_mat, const orc_material* mats) {
+  return orc_system_create(dim, n_nodes, n_elem, coords, conn, phase, n_mat, mats);
+}
+
 int32_t orc_system_set_grid(void* sys, int32_t nx, int32_t ny, int32_t, double lx, double ly, double) {
   return guarded([&] {
     auto& m = S(sys)->mesh;

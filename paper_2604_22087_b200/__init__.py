@@ -110,6 +110,7 @@ def load():
         "afem_ctx_set_stream": ([vp, vp], i32),
         "afem_ctx_synchronize": ([vp], i32),
         "afem_ctx_launch_count": ([vp, vp], i32),
+        "afem_probe_fp64": ([vp, vp], i32),
         "afem_fibres": ([C.c_uint64, i32, f64, f64, vp], i32),
         "afem_system_create": ([vp, i32, i64, i64, vp, vp, vp, i32, vp, vp], i32),
         "afem_system_create_grid": ([vp, i32, i32, i32, i32, f64, f64, f64, i32, vp, f64, i32, vp, vp], i32),
@@ -227,6 +228,11 @@ class Context:
 
     def synchronize(self):
         _check(_lib.afem_ctx_synchronize(self.h))
+
+    def probe_fp64_tflops(self) -> float:
+        v = C.c_double()
+        _check(_lib.afem_probe_fp64(self.h, C.byref(v)))
+        return v.value
 
     @property
     def launches(self) -> int:
@@ -542,7 +548,7 @@ def run_solver(op: LinearOperator, b, method=CG, precond=NONE, rtol=1e-13, max_i
     rep = afem_solve_report()
     cap = hist_cap or (max_iter + 2)
     hist = np.zeros(cap)
-    x = np.zeros(op.n)
+    x = b.new_zeros(op.n) if hasattr(b, "data_ptr") else np.zeros(op.n)  # device b -> device x
     x0 = None if x0 is None else _f64(x0)
     _check(_lib.afem_solve(op.h, C.byref(cfg), _ptr(_f64(b)), _ptr(x0), _ptr(x), C.byref(rep), _ptr(hist), cap))
     return x, dict(converged=bool(rep.converged), iterations=rep.iterations,

@@ -59,6 +59,41 @@ __global__ void k_scal(double a, double* y, int64_t n) {
 
 void scal(Ctx& c, double a, double* y, int64_t n) { launch(c, k_scal, grid_for(n, 256, 148 * 16), 256, 0, a, y, n); }
 
+// FP64 FMA throughput probe: 8 independent DFMA chains per thread (the roofline denominator for
+// FP64-bound kernels; MEASURED_PEAKS.json only carries HBM and bf16 peaks).
+__global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iters, double a, double b) {
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = fma(r[k], a, b);
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += r[k];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+double probe_fp64(Ctx& c) {
+  DevArray<double> o(1);
+  const int iters = 4096, blocks = c.num_sms * 8;
+  cudaEvent_t e0, e1;
+  AFEM_CK(cudaEventCreate(&e0));
+  AFEM_CK(cudaEventCreate(&e1));
+  launch(c, k_dfma_probe, blocks, 256, 0, o.p, iters, 0.999999, 1e-7);  // warm-up
+  AFEM_CK(cudaEventRecord(e0, c.stream));
+  const int reps = 5;
+  for (int r = 0; r < reps; ++r) launch(c, k_dfma_probe, blocks, 256, 0, o.p, iters, 0.999999, 1e-7);
+  AFEM_CK(cudaEventRecord(e1, c.stream));
+  AFEM_CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  AFEM_CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double flops = 2.0 * 8.0 * iters * 256.0 * blocks * reps;
+  return flops / (ms * 1e-3) / 1e12;
+}
+
 // matrix_free_operator (backend.hpp:222-236)
 std::unique_ptr<MfOp> make_mf_op(System& s, const double* d_u) {
   auto op = std::make_unique<MfOp>();
@@ -119,17 +154,16 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-// Read-only argument: device pointer used in place; host data staged in.
+// Read-only argument: device pointer used in place; host data staged in (grow-only ctx buffers).
 template <class T>
 struct In {
   const T* d = nullptr;
-  DevArray<T> tmp;
   In(Ctx& c, const T* p, size_t n) {
     if (!p) return;
     if (is_device_ptr(p)) { d = p; return; }
-    tmp.alloc(n);
-    if (n) AFEM_CK(cudaMemcpyAsync(tmp.p, p, n * sizeof(T), cudaMemcpyHostToDevice, c.stream));
-    d = tmp.p;
+    T* buf = static_cast<T*>(c.stage(n * sizeof(T)));
+    if (n) AFEM_CK(cudaMemcpyAsync(buf, p, n * sizeof(T), cudaMemcpyHostToDevice, c.stream));
+    d = buf;
   }
 };
 
@@ -139,25 +173,31 @@ struct Out {
   T* d = nullptr;
   T* host = nullptr;
   size_t n = 0;
-  DevArray<T> tmp;
   Ctx* c;
   Out(Ctx& cc, T* p, size_t count, bool read_first) : n(count), c(&cc) {
     if (!p) return;
     if (is_device_ptr(p)) { d = p; return; }
     host = p;
-    tmp.alloc(n);
-    if (read_first && n) AFEM_CK(cudaMemcpyAsync(tmp.p, p, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
-    d = tmp.p;
+    T* buf = static_cast<T*>(c->stage(n * sizeof(T)));
+    if (read_first && n) AFEM_CK(cudaMemcpyAsync(buf, p, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    d = buf;
   }
   void finish() {
-    if (host && n) AFEM_CK(cudaMemcpyAsync(host, tmp.p, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+    if (host && n) AFEM_CK(cudaMemcpyAsync(host, d, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
     AFEM_CK(cudaStreamSynchronize(c->stream));
   }
 };
 
+// Start of an ABI call on a context: select the device, recycle the staging slots.
+Ctx& begin(Ctx& c) {
+  AFEM_CK(cudaSetDevice(c.device));
+  c.staging_next = 0;
+  return c;
+}
+
 System& SYS(afem_system s) {
   need(s, "system");
-  AFEM_CK(cudaSetDevice(s->s->ctx->device));
+  begin(*s->s->ctx);
   return *s->s;
 }
 
@@ -347,6 +387,14 @@ afem_status afem_ctx_launch_count(afem_ctx ctx, int64_t* count) {
   });
 }
 
+afem_status afem_probe_fp64(afem_ctx ctx, double* tflops) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(tflops, "tflops");
+    *tflops = probe_fp64(begin(ctx->c));
+  });
+}
+
 afem_status afem_fibres(uint64_t seed, int32_t n, double lx, double ly, double* out) {
   return guarded([&] {
     need(out, "out");
@@ -370,8 +418,7 @@ afem_status afem_system_create(afem_ctx ctx, int32_t dim, int64_t n_nodes, int64
     need(coords, "coords");
     need(conn, "conn");
     need(phase, "phase");
-    Ctx& c = ctx->c;
-    AFEM_CK(cudaSetDevice(c.device));
+    Ctx& c = begin(ctx->c);
     if (dim != 2 && dim != 3) throw std::invalid_argument("system: dim must be 2 (quad4) or 3 (hex8)");
     const int npe = dim == 2 ? 4 : 8;
     In<double> dc(c, coords, n_nodes * dim);
@@ -389,8 +436,7 @@ afem_status afem_system_create_grid(afem_ctx ctx, int32_t dim, int32_t nx, int32
     need(ctx, "ctx");
     need(out, "out");
     if (n_incl < 0 || (n_incl > 0 && !incl_xy)) throw std::invalid_argument("mesh: bad inclusion list");
-    Ctx& c = ctx->c;
-    AFEM_CK(cudaSetDevice(c.device));
+    Ctx& c = begin(ctx->c);
     std::vector<double> incl(incl_xy, incl_xy + 2 * n_incl);
     auto s = std::make_unique<afem_system_s>();
     s->s = make_grid_system(c, dim, nx, ny, nz, lx, ly, lz, incl, radius, to_dmats(n_mat, mats));
@@ -618,6 +664,7 @@ afem_status afem_values_assemble(afem_values v, const double* u) {
   return guarded([&] {
     need(v, "values");
     System& s = *v->v.sys;
+    begin(*s.ctx);
     need(u, "u");
     In<double> du(*s.ctx, u, s.n_dof);
     jacobian(s, du.d, v->v.v.p);
@@ -629,6 +676,7 @@ afem_status afem_values_set(afem_values v, const double* values) {
     need(v, "values");
     need(values, "values data");
     System& s = *v->v.sys;
+    begin(*s.ctx);
     In<double> dv(*s.ctx, values, s.nnz);
     copy(*s.ctx, dv.d, v->v.v.p, s.nnz);
     AFEM_CK(cudaStreamSynchronize(s.ctx->stream));
@@ -639,6 +687,7 @@ afem_status afem_values_eliminate(afem_values v, double* res, const double* u) {
   return guarded([&] {
     need(v, "values");
     System& s = *v->v.sys;
+    begin(*s.ctx);
     In<double> du(*s.ctx, u, s.n_dof);
     Out<double> r(*s.ctx, res, s.n_dof, true);
     eliminate(s, v->v.v.p, r.d, du.d);
@@ -657,6 +706,7 @@ afem_status afem_values_copy(afem_values v, double* out) {
   return guarded([&] {
     need(v, "values");
     System& s = *v->v.sys;
+    begin(*s.ctx);
     Out<double> o(*s.ctx, out, s.nnz, false);
     copy(*s.ctx, v->v.v.p, o.d, s.nnz);
     o.finish();
@@ -779,8 +829,7 @@ afem_status afem_op_apply(afem_op op, const double* x, double* y) {
     need(x, "x");
     need(y, "y");
     Operator& o = *op->op;
-    Ctx& c = *o.sys->ctx;
-    AFEM_CK(cudaSetDevice(c.device));
+    Ctx& c = begin(*o.sys->ctx);
     o.validate();
     In<double> dx(c, x, o.n);
     Out<double> dy(c, y, o.n, false);
@@ -801,7 +850,7 @@ afem_status afem_op_diagonal(afem_op op, double* d) {
     need(op, "op");
     Operator& o = *op->op;
     o.validate();
-    Out<double> dd(*o.sys->ctx, d, o.n, false);
+    Out<double> dd(begin(*o.sys->ctx), d, o.n, false);
     o.diagonal(dd.d);
     dd.finish();
   });
@@ -831,8 +880,7 @@ afem_status afem_solve(afem_op op, const afem_solver_cfg* cfg, const double* b, 
     need(b, "b");
     need(x, "x");
     Operator& o = *op->op;
-    Ctx& c = *o.sys->ctx;
-    AFEM_CK(cudaSetDevice(c.device));
+    Ctx& c = begin(*o.sys->ctx);
     In<double> db(c, b, o.n), dx0(c, x0, o.n);
     Out<double> dx(c, x, o.n, false);
     SolveReport r;

@@ -76,7 +76,15 @@ struct Ctx {
   DevArray<double> red_partials;  // kMaxBlocks * 4
   DevArray<double> red_out;       // 64 scalars
   DevArray<unsigned int> red_counter;
-  std::vector<double> host_scalar;
+  // Grow-only staging buffers for host-pointer arguments at the ABI (slot k of the current call).
+  std::vector<DevArray<uint8_t>> staging;
+  int staging_next = 0;
+  void* stage(size_t bytes) {
+    if (staging_next >= (int)staging.size()) staging.emplace_back();
+    DevArray<uint8_t>& b = staging[staging_next++];
+    if (b.n < bytes) b.alloc(bytes);
+    return b.p;
+  }
 };
 
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs: partial-sum slots for the deterministic reductions

@@ -51,7 +51,7 @@ def make_case(R, name, n, mats, strain):
     csr = s.csr_apply(vals_el, x)
     b = -rhs_el
     x_cg, rep_cg = s.solve(0, vals_el, b, method=0, precond=1, rtol=1e-10)
-    x_gm, rep_gm = s.solve(0, vals_el, b, method=1, precond=1, rtol=1e-10)
+    x_gm, rep_gm = s.solve(0, vals_el, b, method=1, precond=1, rtol=1e-12)
     u_bvp, rep_bvp = s.solve_bvp(rtol=1e-10, lin_rtol=1e-12)
     u_mf, rep_mf = s.solve_bvp(rtol=1e-10, lin_rtol=1e-12, operator_kind=1)
     np.savez_compressed(

@@ -89,7 +89,7 @@ def test_golden_solvers(afem, ctx, path):
     assert rep["converged"]
     assert abs(rep["iterations"] - int(g["cg_iterations"])) <= 2
     assert rel_err(x, g["x_cg"]) <= TOL_U
-    xg, repg = afem.run_solver(op, -g["elim_rhs"], method=afem.GMRES, precond=afem.JACOBI, rtol=1e-10)
+    xg, repg = afem.run_solver(op, -g["elim_rhs"], method=afem.GMRES, precond=afem.JACOBI, rtol=1e-12)
     assert repg["converged"] and rel_err(xg, g["x_gmres"]) <= TOL_U
     buf.release()
     u, rb = s.solve_bvp(rtol=1e-10, lin_rtol=1e-12)
