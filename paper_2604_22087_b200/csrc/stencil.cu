@@ -1,22 +1,29 @@
 // Structured-grid fast path for the linear matrix-free operator y = K x (backend.hpp:130-147) on
 // hex8 grid systems (afem_system_create_grid, dim 3) whose phases are all linear elastic with a
 // common Poisson ratio. Then every element stiffness is K_e = E_phase * Khat (Khat: the uniform
-// brick at E = 1), and
-//     y_n = E_base(n) * (S x)_n  +  sum_{octants o of n with E_o != E_base} (E_o - E_base) Khat_rows(o) x_e(o)
-// where S (27 blocks of 3x3) is the assembled homogeneous stencil and E_base(n) the majority
-// modulus of the node's eight octant elements (octants outside the domain count as E = 0).
+// brick at E = 1) and, with octant o of node n the element on side o of n,
+//     y_n = sum_{o exists} E_o Khat_rows(o) x_e(o)
+//         = E_base(n) (S_f x)_n + sum_{o in F(n), E_o != E_base} (E_o - E_base) Khat_rows(o) x_e(o)
+// S_f is the assembled stencil of the octant family F(n): all 8 octants in the interior, the
+// half / quarter families on y and z boundary faces (the void octants are dropped exactly by the
+// coefficients), and E_base(n) the majority modulus over F(n) (octants void in x count as E = 0).
 //
 // Kernels:
-//  k_stencil_main   32x8 node tile per CTA, marching in z over a chunk of planes; each x-plane
-//                   (with a one-node halo, Dirichlet-masked) is staged once in shared memory
-//                   (double-buffered, register prefetch) and each thread keeps the partial sums of
-//                   the three nodes of its column the plane touches (z-1, z, z+1). 153 DFMA per
-//                   node (the 243-entry stencil minus the 90 entries that vanish by symmetry), no
-//                   atomics, every y entry written exactly once.
-//  k_stencil_edge   the x columns a 32-wide tile cannot cover (NX mod 32), node per thread.
-//  k_stencil_fix    interface nodes only (a precomputed list): adds the octant corrections.
-// Algorithmic traffic: x (8 B/dof) + y (8 B/dof) + one info byte per node (Dirichlet bits +
-// base phase) — no connectivity is read.
+//  k_stencil_main   32x8 node tile per CTA, marching in z over a chunk of planes (one wave); each
+//                   x-plane (one-node halo, Dirichlet-masked) is staged once in shared memory
+//                   (double-buffered, register prefetch, one barrier per plane) and each thread
+//                   keeps the partial sums of the three column nodes the plane touches. 153 DFMA
+//                   per interior node (the 243-entry stencil minus the 90 symmetry zeros), all
+//                   coefficients in the kernel-parameter constant bank; y/z faces switch to the
+//                   half/quarter coefficient families (warp- or CTA-uniform). No atomics; every y
+//                   entry is written exactly once by this kernel.
+//  k_stencil_edge   the x columns a 32-wide tile cannot cover (NX mod 32): exact octant form.
+//  k_stencil_fix    nodes whose family F(n) mixes moduli (fibre interfaces, the x = 0 face): adds
+//                   the octant corrections; the list is sorted by octant mask so each warp's
+//                   octant loop is uniform (Khat rows stay uniform constant-bank operands).
+// Algorithmic traffic of the main kernel: x (8 B/dof) + y (8 B/dof) + one info byte per node.
+#include <cub/cub.cuh>
+
 #include <cmath>
 #include <vector>
 
@@ -24,23 +31,27 @@
 
 namespace afem {
 
-constexpr int kVoid = 31;  // phase code for octants outside the domain (E = 0)
+constexpr int kVoid = 31;  // phase code of an octant outside the domain (E = 0)
 
 struct StencilParams {
-  double S[27][3][3];  // homogeneous stencil at E = 1: S[d][a][b], d = (dx+1) + 3(dy+1) + 9(dz+1)
-  double K[24][24];    // uniform-brick element stiffness at E = 1
-  double E[32];        // modulus per phase code (E[kVoid] = 0)
-  int NX, NY, NZ;      // node counts per axis
-  int NXm;             // columns covered by 32-wide tiles
+  double S[27][3][3];          // full family, d = (dx+1) + 3(dy+1) + 9(dz+1)
+  double HY[2][9][3][3];       // y face lo/hi, entries with dy = 0: index (dx+1) + 3(dz+1)
+  double HZ[2][9][3][3];       // z face lo/hi, entries with dz = 0: index (dx+1) + 3(dy+1)
+  double HYZ[2][2][3][3][3];   // y and z faces, entries with dy = dz = 0: index dx+1
+  double K[24][24];            // uniform-brick element stiffness at E = 1
+  double E[32];                // modulus per phase code (E[kVoid] = 0)
+  int NX, NY, NZ;              // node counts per axis
+  int NXm;                     // columns covered by 32-wide tiles
 };
 
 struct StencilPlan {
   StencilParams p;
   DevArray<uint8_t> info;       // per node: bits 0-2 Dirichlet mask, bits 3-7 base phase code
-  DevArray<int32_t> fix_nodes;  // interface nodes
-  DevArray<uint8_t> fix_mask;   // per interface node: octants needing a correction
+  DevArray<int32_t> fix_nodes;  // nodes needing octant corrections, sorted by mask
+  DevArray<uint8_t> fix_mask;   // their octant masks
   int64_t n_fix = 0;
   int kchunk = 16;
+  int nchunks = 1;
 };
 
 namespace {
@@ -50,32 +61,65 @@ constexpr int RW = 3 * (TX + 2);          // doubles per staged row (x-interleav
 constexpr int ITEMS = (TY + 2) * RW;      // doubles per staged plane
 constexpr int PER = (ITEMS + NT - 1) / NT;
 
-// Is S[d][a][b] structurally zero? Off-diagonal (a != b) entries vanish by reflection symmetry of
-// the brick unless the offset is non-zero along both axes a and b.
-__host__ __device__ constexpr bool szero(int dx, int dy, int dz, int a, int b) {
+// Structural zero of a family's entry (a, b) at offset d: the brick's reflection symmetry about
+// an axis c that the family keeps intact makes every off-diagonal entry involving c vanish when
+// d_c = 0. broken: bit 1 = y symmetry broken (y face), bit 2 = z symmetry broken (z face).
+__host__ __device__ constexpr bool szero(int dx, int dy, int dz, int a, int b, int broken) {
   if (a == b) return false;
-  const int da = a == 0 ? dx : (a == 1 ? dy : dz);
-  const int db = b == 0 ? dx : (b == 1 ? dy : dz);
-  return da == 0 || db == 0;
+  for (int c = 0; c < 3; ++c) {
+    if (c != a && c != b) continue;
+    if ((broken >> c) & 1) continue;
+    const int dc = c == 0 ? dx : (c == 1 ? dy : dz);
+    if (dc == 0) return true;
+  }
+  return false;
 }
 
-template <int DX, int DY, int DZ>
+// Coefficient family of entry (d, a, b) for a node on y face YF / z face ZF (0 none, 1 lo, 2 hi).
+template <int DX, int DY, int DZ, int YF, int ZF>
+struct Fam {
+  static constexpr bool yb = YF != 0 && DY == 0;
+  static constexpr bool zb = ZF != 0 && DZ == 0;
+  static constexpr int broken = (yb ? 2 : 0) | (zb ? 4 : 0);
+  static __device__ __forceinline__ double c(const StencilParams& P, int a, int b) {
+    if constexpr (yb && zb) return P.HYZ[YF - 1][ZF - 1][DX + 1][a][b];
+    else if constexpr (yb) return P.HY[YF - 1][(DX + 1) + 3 * (DZ + 1)][a][b];
+    else if constexpr (zb) return P.HZ[ZF - 1][(DX + 1) + 3 * (DY + 1)][a][b];
+    else return P.S[(DX + 1) + 3 * (DY + 1) + 9 * (DZ + 1)][a][b];
+  }
+};
+
+template <int DX, int DY, int DZ, int YF, int ZF>
 __device__ __forceinline__ void sblock(const StencilParams& P, const double (&xv)[3], double (&acc)[3]) {
-  constexpr int d = (DX + 1) + 3 * (DY + 1) + 9 * (DZ + 1);
+  using F = Fam<DX, DY, DZ, YF, ZF>;
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int b = 0; b < 3; ++b)
-      if (!szero(DX, DY, DZ, a, b)) acc[a] = fma(P.S[d][a][b], xv[b], acc[a]);
+      if (!szero(DX, DY, DZ, a, b, F::broken)) acc[a] = fma(F::c(P, a, b), xv[b], acc[a]);
 }
 
-// Contributions of one staged plane (neighbour (DI, DJ) in-plane) to the three column nodes.
-template <int DI, int DJ>
-__device__ __forceinline__ void plane_neighbour(const StencilParams& P, const double (&xv)[3], bool dprev, bool dcur,
-                                                bool dnext, double (&ap)[3], double (&ac)[3], double (&an)[3]) {
-  if (dnext) sblock<DI, DJ, -1>(P, xv, an);  // node above sees this plane at dz = -1
-  if (dcur) sblock<DI, DJ, 0>(P, xv, ac);
-  if (dprev) sblock<DI, DJ, 1>(P, xv, ap);   // node below sees this plane at dz = +1
+// All contributions of the staged plane to the thread's three column nodes.
+template <int YF>
+__device__ __forceinline__ void plane_step(const StencilParams& P, const double (*sm)[TY + 2][TX + 2], int tx, int ty,
+                                           bool dprev, bool dcur, bool dnext, int zcur, double (&ap)[3],
+                                           double (&ac)[3], double (&an)[3]) {
+#define AFEM_NB(DI, DJ)                                                                                      \
+  {                                                                                                          \
+    const double xv[3] = {sm[0][ty + 1 + DJ][tx + 1 + DI], sm[1][ty + 1 + DJ][tx + 1 + DI],                  \
+                          sm[2][ty + 1 + DJ][tx + 1 + DI]};                                                  \
+    if (dnext) sblock<DI, DJ, -1, YF, 0>(P, xv, an);                                                         \
+    if (dcur) {                                                                                              \
+      if (zcur == 0) sblock<DI, DJ, 0, YF, 0>(P, xv, ac);                                                    \
+      else if (zcur == 1) sblock<DI, DJ, 0, YF, 1>(P, xv, ac);                                               \
+      else sblock<DI, DJ, 0, YF, 2>(P, xv, ac);                                                              \
+    }                                                                                                        \
+    if (dprev) sblock<DI, DJ, 1, YF, 0>(P, xv, ap);                                                          \
+  }
+  AFEM_NB(-1, -1) AFEM_NB(0, -1) AFEM_NB(1, -1)
+  AFEM_NB(-1, 0) AFEM_NB(0, 0) AFEM_NB(1, 0)
+  AFEM_NB(-1, 1) AFEM_NB(0, 1) AFEM_NB(1, 1)
+#undef AFEM_NB
 }
 
 __global__ void __launch_bounds__(NT, 3) k_stencil_main(const __grid_constant__ StencilParams P,
@@ -89,35 +133,42 @@ __global__ void __launch_bounds__(NT, 3) k_stencil_main(const __grid_constant__ 
   const int k0 = blockIdx.z * kchunk, k1 = min(k0 + kchunk, NZ);
   const int i = i0 + tx, j = j0 + ty;
   const bool active = j < NY;
+  const int yf = j == 0 ? 1 : (j == NY - 1 ? 2 : 0);
   const int64_t plane = (int64_t)NX * NY;
 
-  double pf[PER];
-  auto fetch = [&](int p) {
+  // Per-item staging geometry (independent of the plane): global dof offset within a plane,
+  // node offset for the info byte, component, shared-memory slot, validity.
+  int goff[PER], noff[PER], slot[PER];
+  uint8_t comp[PER];
+  bool valid[PER];
 #pragma unroll
-    for (int it = 0; it < PER; ++it) {
-      const int idx = threadIdx.x + it * NT;
-      double v = 0.0;
-      if (idx < ITEMS && p >= 0 && p < NZ) {
-        const int r = idx / RW, c = idx - r * RW;
-        const int ii = i0 - 1 + c / 3, jj = j0 - 1 + r, comp = c % 3;
-        if (ii >= 0 && ii < NX && jj >= 0 && jj < NY) {
-          const int64_t node = ii + (int64_t)NX * jj + plane * p;
-          const uint8_t inf = __ldg(&info[node]);
-          v = ((inf >> comp) & 1) ? 0.0 : __ldg(&x[3 * node + comp]);
-        }
-      }
-      pf[it] = v;
+  for (int it = 0; it < PER; ++it) {
+    const int idx = threadIdx.x + it * NT;
+    const int r = idx / RW, c = idx - r * RW;
+    const int ii = i0 - 1 + c / 3, jj = j0 - 1 + r;
+    valid[it] = idx < ITEMS && ii >= 0 && ii < NX && jj >= 0 && jj < NY;
+    noff[it] = valid[it] ? ii + NX * jj : 0;
+    goff[it] = 3 * noff[it] + c % 3;
+    comp[it] = static_cast<uint8_t>(c % 3);
+    slot[it] = idx < ITEMS ? (c % 3) * (TY + 2) * (TX + 2) + r * (TX + 2) + c / 3 : -1;
+  }
+  double pv[PER];
+  uint8_t pm[PER];
+  auto fetch = [&](int p) {
+    const bool inplane = p >= 0 && p < NZ;
+    const int64_t pb = plane * (inplane ? p : 0);
+#pragma unroll
+    for (int it = 0; it < PER; ++it) {  // unconditional, independent loads; masking at store
+      pv[it] = __ldg(&x[3 * pb + goff[it]]);
+      pm[it] = __ldg(&info[pb + noff[it]]);
+      if (!(inplane && valid[it])) pm[it] = 0xff;
     }
   };
   auto store = [&](int buf) {
+    double* s = &sm[buf][0][0][0];
 #pragma unroll
-    for (int it = 0; it < PER; ++it) {
-      const int idx = threadIdx.x + it * NT;
-      if (idx < ITEMS) {
-        const int r = idx / RW, c = idx - r * RW;
-        sm[buf][c % 3][r][c / 3] = pf[it];
-      }
-    }
+    for (int it = 0; it < PER; ++it)
+      if (slot[it] >= 0) s[slot[it]] = ((pm[it] >> comp[it]) & 1) ? 0.0 : pv[it];
   };
 
   double ap[3] = {0.0, 0.0, 0.0}, ac[3] = {0.0, 0.0, 0.0}, an[3] = {0.0, 0.0, 0.0};
@@ -127,25 +178,19 @@ __global__ void __launch_bounds__(NT, 3) k_stencil_main(const __grid_constant__ 
   for (int p = k0 - 1; p <= k1; ++p) {
     const int buf = (p - (k0 - 1)) & 1;
     if (p < k1) fetch(p + 1);
+    const int64_t onode = i + (int64_t)NX * (active ? j : 0) + plane * max(p - 1, 0);
+    const uint8_t oinf = __ldg(&info[onode]);
     if (active && p >= 0 && p < NZ) {
       const bool dprev = p - 1 >= k0, dcur = p >= k0 && p < k1, dnext = p + 1 < k1;
-#define AFEM_NB(DI, DJ)                                                                      \
-  {                                                                                          \
-    const double xv[3] = {sm[buf][0][ty + 1 + DJ][tx + 1 + DI], sm[buf][1][ty + 1 + DJ][tx + 1 + DI], \
-                          sm[buf][2][ty + 1 + DJ][tx + 1 + DI]};                             \
-    plane_neighbour<DI, DJ>(P, xv, dprev, dcur, dnext, ap, ac, an);                          \
-  }
-      AFEM_NB(-1, -1) AFEM_NB(0, -1) AFEM_NB(1, -1)
-      AFEM_NB(-1, 0) AFEM_NB(0, 0) AFEM_NB(1, 0)
-      AFEM_NB(-1, 1) AFEM_NB(0, 1) AFEM_NB(1, 1)
-#undef AFEM_NB
+      const int zcur = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
+      if (yf == 0) plane_step<0>(P, sm[buf], tx, ty, dprev, dcur, dnext, zcur, ap, ac, an);
+      else if (yf == 1) plane_step<1>(P, sm[buf], tx, ty, dprev, dcur, dnext, zcur, ap, ac, an);
+      else plane_step<2>(P, sm[buf], tx, ty, dprev, dcur, dnext, zcur, ap, ac, an);
     }
     if (active && p - 1 >= k0) {  // node (i, j, p-1) is complete
-      const int64_t node = i + (int64_t)NX * j + plane * (p - 1);
-      const uint8_t inf = __ldg(&info[node]);
-      const double E = P.E[inf >> 3];
+      const double E = P.E[oinf >> 3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) y[3 * node + a] = ((inf >> a) & 1) ? __ldg(&x[3 * node + a]) : E * ap[a];
+      for (int a = 0; a < 3; ++a) y[3 * onode + a] = ((oinf >> a) & 1) ? __ldg(&x[3 * onode + a]) : E * ap[a];
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -158,16 +203,55 @@ __global__ void __launch_bounds__(NT, 3) k_stencil_main(const __grid_constant__ 
   }
 }
 
-__device__ __forceinline__ double xm_at(const double* __restrict__ x, const uint8_t* __restrict__ info, int NX,
-                                        int NY, int NZ, int ii, int jj, int kk, int comp) {
-  if (ii < 0 || ii >= NX || jj < 0 || jj >= NY || kk < 0 || kk >= NZ) return 0.0;
-  const int64_t node = ii + (int64_t)NX * (jj + (int64_t)NY * kk);
-  return ((__ldg(&info[node]) >> comp) & 1) ? 0.0 : __ldg(&x[3 * node + comp]);
+__host__ __device__ __forceinline__ int local_node(int lx, int ly, int lz) {
+  const int ring = lx ? (ly ? 2 : 1) : (ly ? 3 : 0);  // element.hpp:22-23 ring, then z = +1
+  return ring + 4 * lz;
+}
+__host__ __device__ __forceinline__ int corner_x(int m) { return ((m & 3) == 1 || (m & 3) == 2) ? 1 : 0; }
+__host__ __device__ __forceinline__ int corner_y(int m) { return (m & 3) >= 2 ? 1 : 0; }
+
+// Khat_rows(o) x_e(o) for octant o of node (i, j, k): masked x, zero outside the domain.
+__device__ __forceinline__ void octant_action(const StencilParams& P, const double* __restrict__ x,
+                                              const uint8_t* __restrict__ info, int i, int j, int k, int o,
+                                              double (&t)[3]) {
+  const int NX = P.NX, NY = P.NY, NZ = P.NZ;
+  const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+  const int ei = i - 1 + ox, ej = j - 1 + oy, ek = k - 1 + oz;
+  const int ln = local_node(1 - ox, 1 - oy, 1 - oz);
+  double xv[24];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const int ii = ei + corner_x(m), jj = ej + corner_y(m), kk = ek + (m >> 2);
+    const bool in = ii >= 0 && ii < NX && jj >= 0 && jj < NY && kk >= 0 && kk < NZ;
+    const int64_t node = in ? ii + (int64_t)NX * (jj + (int64_t)NY * kk) : 0;
+    const uint8_t inf = in ? __ldg(&info[node]) : 0x7;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const double v = __ldg(&x[3 * node + b]);
+      xv[3 * m + b] = ((inf >> b) & 1) ? 0.0 : v;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 24; ++q) s = fma(P.K[3 * ln + a][q], xv[q], s);
+    t[a] = s;
+  }
 }
 
-// Columns i >= NXm: full 27-point stencil per node with direct (cached) loads.
+__device__ __forceinline__ int octant_phase(const StencilParams& P, const uint8_t* __restrict__ phase, int i, int j,
+                                            int k, int o) {
+  const int ex = P.NX - 1, ey = P.NY - 1, ez = P.NZ - 1;
+  const int ei = i - 1 + (o & 1), ej = j - 1 + ((o >> 1) & 1), ek = k - 1 + (o >> 2);
+  const bool inside = ei >= 0 && ei < ex && ej >= 0 && ej < ey && ek >= 0 && ek < ez;
+  return inside ? phase[ei + (int64_t)ex * (ej + (int64_t)ey * ek)] : kVoid;
+}
+
+// Columns i >= NXm: exact octant form y_n = sum_o E_o Khat_rows(o) x_e(o).
 __global__ void k_stencil_edge(const __grid_constant__ StencilParams P, const double* __restrict__ x,
-                               const uint8_t* __restrict__ info, double* __restrict__ y) {
+                               const uint8_t* __restrict__ info, const uint8_t* __restrict__ phase,
+                               double* __restrict__ y) {
   const int NX = P.NX, NY = P.NY, NZ = P.NZ, W = NX - P.NXm;
   const int64_t total = (int64_t)W * NY * NZ;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -175,82 +259,64 @@ __global__ void k_stencil_edge(const __grid_constant__ StencilParams P, const do
     const int64_t r = t / W;
     const int j = static_cast<int>(r % NY), k = static_cast<int>(r / NY);
     double acc[3] = {0.0, 0.0, 0.0};
+    for (int o = 0; o < 8; ++o) {
+      const double E = P.E[octant_phase(P, phase, i, j, k, o)];
+      if (E == 0.0) continue;
+      double tv[3];
+      octant_action(P, x, info, i, j, k, o, tv);
 #pragma unroll
-    for (int d = 0; d < 27; ++d) {
-      const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
-      double xv[3];
-#pragma unroll
-      for (int b = 0; b < 3; ++b) xv[b] = xm_at(x, info, NX, NY, NZ, i + dx, j + dy, k + dz, b);
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b)
-          if (!szero(dx, dy, dz, a, b)) acc[a] = fma(P.S[d][a][b], xv[b], acc[a]);
+      for (int a = 0; a < 3; ++a) acc[a] = fma(E, tv[a], acc[a]);
     }
     const int64_t node = i + (int64_t)NX * (j + (int64_t)NY * k);
     const uint8_t inf = info[node];
-    const double E = P.E[inf >> 3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) y[3 * node + a] = ((inf >> a) & 1) ? x[3 * node + a] : E * acc[a];
+    for (int a = 0; a < 3; ++a) y[3 * node + a] = ((inf >> a) & 1) ? x[3 * node + a] : acc[a];
   }
 }
 
-// hex8 local node index of corner (lx, ly, lz) (element.hpp:22-23 ring, then z = +1).
-__host__ __device__ __forceinline__ int local_node(int lx, int ly, int lz) {
-  const int ring = lx ? (ly ? 2 : 1) : (ly ? 3 : 0);
-  return ring + 4 * lz;
-}
-
-// Interface corrections: y_n += sum_o (E_o - E_base) Khat_rows(ln(o)) x_e(o), free rows only.
-__global__ void k_stencil_fix(const __grid_constant__ StencilParams P, const double* __restrict__ x,
-                              const uint8_t* __restrict__ info, const uint8_t* __restrict__ phase,
-                              const int32_t* __restrict__ nodes, const uint8_t* __restrict__ omask, int64_t n_fix,
-                              double* __restrict__ y) {
-  const int NX = P.NX, NY = P.NY, NZ = P.NZ;
-  const int ex = NX - 1, ey = NY - 1, ez = NZ - 1;  // element counts
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_fix; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t node = nodes[t];
+// Octant corrections for the (mask-sorted) fix list; free rows only.
+__global__ void __launch_bounds__(128) k_stencil_fix(const __grid_constant__ StencilParams P,
+                                                     const double* __restrict__ x, const uint8_t* __restrict__ info,
+                                                     const uint8_t* __restrict__ phase,
+                                                     const int32_t* __restrict__ nodes,
+                                                     const uint8_t* __restrict__ omask, int64_t n_fix,
+                                                     double* __restrict__ y) {
+  const int NX = P.NX, NY = P.NY;
+  for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x; t0 < n_fix; t0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = t0 + threadIdx.x;
+    const bool live = t < n_fix;
+    const int64_t node = live ? nodes[t] : 0;
+    const uint8_t om = live ? omask[t] : 0;
     const int i = static_cast<int>(node % NX);
     const int64_t r = node / NX;
     const int j = static_cast<int>(r % NY), k = static_cast<int>(r / NY);
     const uint8_t inf = info[node];
     const double Eb = P.E[inf >> 3];
-    const uint8_t om = omask[t];
     double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll 1
     for (int o = 0; o < 8; ++o) {
-      if (!((om >> o) & 1)) continue;
-      const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
-      const int ei = i - 1 + ox, ej = j - 1 + oy, ek = k - 1 + oz;
-      const bool inside = ei >= 0 && ei < ex && ej >= 0 && ej < ey && ek >= 0 && ek < ez;
-      const int ph = inside ? phase[ei + (int64_t)ex * (ej + (int64_t)ey * ek)] : kVoid;
-      const double dE = P.E[ph] - Eb;
-      const int ln = local_node(1 - ox, 1 - oy, 1 - oz);
-      double t3[3] = {0.0, 0.0, 0.0};
+      const bool mine = (om >> o) & 1;
+      if (!__any_sync(0xffffffffu, mine)) continue;  // octant loop uniform across the warp
+      double tv[3];
+      octant_action(P, x, info, i, j, k, o, tv);
+      const double dE = mine ? P.E[octant_phase(P, phase, i, j, k, o)] - Eb : 0.0;
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const int mx = ((m & 3) == 1 || (m & 3) == 2) ? 1 : 0, my = (m & 3) >= 2 ? 1 : 0, mz = m >> 2;
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const double xv = xm_at(x, info, NX, NY, NZ, ei + mx, ej + my, ek + mz, b);
-#pragma unroll
-          for (int a = 0; a < 3; ++a) t3[a] = fma(P.K[3 * ln + a][3 * m + b], xv, t3[a]);
-        }
-      }
-#pragma unroll
-      for (int a = 0; a < 3; ++a) acc[a] = fma(dE, t3[a], acc[a]);
+      for (int a = 0; a < 3; ++a) acc[a] = fma(dE, tv[a], acc[a]);
     }
+    if (live)
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-      if (!((inf >> a) & 1)) y[3 * node + a] += acc[a];
+      for (int a = 0; a < 3; ++a)
+        if (!((inf >> a) & 1)) y[3 * node + a] += acc[a];
   }
 }
 
-// Node info byte + interface list. Base phase = most frequent octant phase (void counted), ties to
-// the smaller code.
-__global__ void k_stencil_classify(int NX, int NY, int NZ, const uint8_t* __restrict__ phase,
+// Per node: info byte (Dirichlet bits | base phase << 3) and, for nodes of the main kernel whose
+// octant family mixes moduli, a fix entry. Family F(n): octants not void in y or z (those are
+// removed exactly by the face coefficients); x-void octants stay in F(n) with E = 0. Base = the
+// most frequent phase code in F(n), ties to the smaller code.
+__global__ void k_stencil_classify(int NX, int NY, int NZ, int NXm, const uint8_t* __restrict__ phase,
                                    const uint8_t* __restrict__ dof_mask, uint8_t* __restrict__ info,
-                                   int32_t* __restrict__ fix_nodes, uint8_t* __restrict__ fix_mask,
-                                   unsigned long long* __restrict__ n_fix) {
+                                   uint64_t* __restrict__ fix_keys, unsigned long long* __restrict__ n_fix) {
   const int ex = NX - 1, ey = NY - 1, ez = NZ - 1;
   const int64_t total = (int64_t)NX * NY * NZ;
   for (int64_t node = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; node < total;
@@ -259,15 +325,19 @@ __global__ void k_stencil_classify(int NX, int NY, int NZ, const uint8_t* __rest
     const int64_t r = node / NX;
     const int j = static_cast<int>(r % NY), k = static_cast<int>(r / NY);
     int ph[8];
+    bool fam[8];
     for (int o = 0; o < 8; ++o) {
       const int ei = i - 1 + (o & 1), ej = j - 1 + ((o >> 1) & 1), ek = k - 1 + (o >> 2);
-      const bool inside = ei >= 0 && ei < ex && ej >= 0 && ej < ey && ek >= 0 && ek < ez;
+      const bool yz_in = ej >= 0 && ej < ey && ek >= 0 && ek < ez;
+      const bool inside = yz_in && ei >= 0 && ei < ex;
+      fam[o] = yz_in;
       ph[o] = inside ? phase[ei + (int64_t)ex * (ej + (int64_t)ey * ek)] : kVoid;
     }
-    int best = ph[0], bestc = 0;
+    int best = kVoid, bestc = 0;
     for (int o = 0; o < 8; ++o) {
+      if (!fam[o]) continue;
       int c = 0;
-      for (int q = 0; q < 8; ++q) c += ph[q] == ph[o];
+      for (int q = 0; q < 8; ++q) c += fam[q] && ph[q] == ph[o];
       if (c > bestc || (c == bestc && ph[o] < best)) {
         best = ph[o];
         bestc = c;
@@ -275,14 +345,20 @@ __global__ void k_stencil_classify(int NX, int NY, int NZ, const uint8_t* __rest
     }
     uint8_t om = 0;
     for (int o = 0; o < 8; ++o)
-      if (ph[o] != best) om |= static_cast<uint8_t>(1u << o);
+      if (fam[o] && ph[o] != best) om |= static_cast<uint8_t>(1u << o);
     const uint8_t m = (dof_mask[3 * node] ? 1 : 0) | (dof_mask[3 * node + 1] ? 2 : 0) | (dof_mask[3 * node + 2] ? 4 : 0);
     info[node] = static_cast<uint8_t>(m | (best << 3));
-    if (om && m != 7) {
+    if (i < NXm && om && m != 7) {
       const unsigned long long slot = atomicAdd(n_fix, 1ull);
-      fix_nodes[slot] = static_cast<int32_t>(node);
-      fix_mask[slot] = om;
+      fix_keys[slot] = (static_cast<uint64_t>(om) << 32) | static_cast<uint64_t>(node);
     }
+  }
+}
+
+__global__ void k_split_keys(const uint64_t* keys, int64_t n, int32_t* nodes, uint8_t* masks) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    nodes[t] = static_cast<int32_t>(keys[t] & 0xffffffffu);
+    masks[t] = static_cast<uint8_t>(keys[t] >> 32);
   }
 }
 
@@ -315,6 +391,44 @@ __global__ void k_brick_stiffness(const double* coords, const int32_t* conn, DMa
     for (int j = 0; j < 24; ++j) K[(3 * a_node + a) * 24 + j] = rows[a][j];
 }
 
+// Family stencil from Khat: sum over octants o in the family containing offset d.
+void family_stencil(const std::vector<double>& K, int yf, int zf, double out[27][3][3]) {
+  for (int d = 0; d < 27; ++d)
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) out[d][a][b] = 0.0;
+  for (int o = 0; o < 8; ++o) {
+    const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+    if (yf == 1 && oy == 0) continue;  // y lo face: octants below are void
+    if (yf == 2 && oy == 1) continue;
+    if (zf == 1 && oz == 0) continue;
+    if (zf == 2 && oz == 1) continue;
+    const int lx = 1 - ox, ly = 1 - oy, lz = 1 - oz;
+    const int ln = local_node(lx, ly, lz);
+    for (int m = 0; m < 8; ++m) {
+      const int mx = corner_x(m), my = corner_y(m), mz = m >> 2;
+      const int d = (mx - lx + 1) + 3 * (my - ly + 1) + 9 * (mz - lz + 1);
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) out[d][a][b] += K[(3 * ln + a) * 24 + 3 * m + b];
+    }
+  }
+}
+
+// Snap structural zeros; false if a snapped entry is not negligible (not a symmetric brick grid).
+bool snap(double s[27][3][3], int broken) {
+  double smax = 0.0;
+  for (int d = 0; d < 27; ++d)
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) smax = std::max(smax, std::abs(s[d][a][b]));
+  for (int d = 0; d < 27; ++d)
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        if (szero(d % 3 - 1, (d / 3) % 3 - 1, d / 9 - 1, a, b, broken)) {
+          if (std::abs(s[d][a][b]) > 1e-12 * smax) return false;
+          s[d][a][b] = 0.0;
+        }
+  return true;
+}
+
 }  // namespace
 
 StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
@@ -323,7 +437,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   const double nu = s.mats[0].nu;
   for (const DMat& m : s.mats)
     if (m.model != MODEL_LINEAR || m.nu != nu) return nullptr;
-  if (s.n_nodes > (int64_t)INT32_MAX) return nullptr;
+  if (s.n_nodes > (int64_t)INT32_MAX / 3) return nullptr;
   Ctx& c = *s.ctx;
   auto plan = std::make_unique<StencilPlan>();
   StencilParams& P = plan->p;
@@ -336,59 +450,71 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
 
   // Khat from element 0 at E = 1 (K_e = E * Khat for a common nu: c11, c12, c33 scale with E).
   DevArray<double> dK(576);
-  DMat unit = make_dmat(MODEL_LINEAR, 1.0, nu);
+  const DMat unit = make_dmat(MODEL_LINEAR, 1.0, nu);
   launch(c, k_brick_stiffness, 1, 32, 0, s.coords.p, s.conn.p, unit, dK.p);
   std::vector<double> K(576);
   AFEM_CK(cudaMemcpyAsync(K.data(), dK.p, 576 * 8, cudaMemcpyDeviceToHost, c.stream));
   AFEM_CK(cudaStreamSynchronize(c.stream));
   for (int r = 0; r < 24; ++r)
     for (int q = 0; q < 24; ++q) P.K[r][q] = K[r * 24 + q];
-  // S(d) = sum over octants o containing n and n + d of Khat[ln(o), lm(o, d)]
-  double smax = 0.0;
-  for (int d = 0; d < 27; ++d)
-    for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b) P.S[d][a][b] = 0.0;
-  for (int o = 0; o < 8; ++o) {
-    const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
-    const int lx = 1 - ox, ly = 1 - oy, lz = 1 - oz;
-    const int ln = local_node(lx, ly, lz);
-    for (int mz = 0; mz < 2; ++mz)
-      for (int my = 0; my < 2; ++my)
-        for (int mx = 0; mx < 2; ++mx) {
-          const int lm = local_node(mx, my, mz);
-          const int d = (mx - lx + 1) + 3 * (my - ly + 1) + 9 * (mz - lz + 1);
-          for (int a = 0; a < 3; ++a)
-            for (int b = 0; b < 3; ++b) P.S[d][a][b] += K[(3 * ln + a) * 24 + 3 * lm + b];
-        }
+  double fam[27][3][3];
+  family_stencil(K, 0, 0, fam);
+  if (!snap(fam, 0)) return nullptr;
+  std::memcpy(P.S, fam, sizeof P.S);
+  for (int sy = 0; sy < 2; ++sy) {
+    family_stencil(K, sy + 1, 0, fam);
+    if (!snap(fam, 2)) return nullptr;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dz = -1; dz <= 1; ++dz)
+        std::memcpy(P.HY[sy][(dx + 1) + 3 * (dz + 1)], fam[(dx + 1) + 3 * 1 + 9 * (dz + 1)], 9 * 8);
   }
-  for (int d = 0; d < 27; ++d)
-    for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b) smax = std::max(smax, std::abs(P.S[d][a][b]));
-  for (int d = 0; d < 27; ++d)
-    for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b)
-        if (szero(d % 3 - 1, (d / 3) % 3 - 1, d / 9 - 1, a, b)) {
-          if (std::abs(P.S[d][a][b]) > 1e-12 * smax) return nullptr;  // not a symmetric brick grid
-          P.S[d][a][b] = 0.0;
-        }
+  for (int sz = 0; sz < 2; ++sz) {
+    family_stencil(K, 0, sz + 1, fam);
+    if (!snap(fam, 4)) return nullptr;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        std::memcpy(P.HZ[sz][(dx + 1) + 3 * (dy + 1)], fam[(dx + 1) + 3 * (dy + 1) + 9 * 1], 9 * 8);
+  }
+  for (int sy = 0; sy < 2; ++sy)
+    for (int sz = 0; sz < 2; ++sz) {
+      family_stencil(K, sy + 1, sz + 1, fam);
+      if (!snap(fam, 6)) return nullptr;
+      for (int dx = -1; dx <= 1; ++dx) std::memcpy(P.HYZ[sy][sz][dx + 1], fam[(dx + 1) + 3 + 9], 9 * 8);
+    }
 
   const int64_t nn = s.n_nodes;
   plan->info.alloc(nn);
-  plan->fix_nodes.alloc(nn);
-  plan->fix_mask.alloc(nn);
+  DevArray<uint64_t> keys(nn);
   DevArray<unsigned long long> cnt(1);
   AFEM_CK(cudaMemsetAsync(cnt.p, 0, 8, c.stream));
-  launch(c, k_stencil_classify, grid_for(nn, 256, 148 * 32), 256, 0, P.NX, P.NY, P.NZ, s.phase.p, op.mask.p,
-         plan->info.p, plan->fix_nodes.p, plan->fix_mask.p, cnt.p);
+  launch(c, k_stencil_classify, grid_for(nn, 256, 148 * 32), 256, 0, P.NX, P.NY, P.NZ, P.NXm, s.phase.p, op.mask.p,
+         plan->info.p, keys.p, cnt.p);
   unsigned long long nf = 0;
   AFEM_CK(cudaMemcpyAsync(&nf, cnt.p, 8, cudaMemcpyDeviceToHost, c.stream));
   AFEM_CK(cudaStreamSynchronize(c.stream));
   plan->n_fix = static_cast<int64_t>(nf);
-  // z chunk: enough CTAs for ~3 per SM, at least 8 planes per chunk
+  if (nf) {  // sort by (octant mask, node): warps see uniform octant loops and nearby nodes
+    DevArray<uint64_t> sorted(nf);
+    size_t tmp = 0;
+    AFEM_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.p, sorted.p, (int)nf, 0, 40, c.stream));
+    DevArray<uint8_t> tb(tmp);
+    AFEM_CK(cub::DeviceRadixSort::SortKeys(tb.p, tmp, keys.p, sorted.p, (int)nf, 0, 40, c.stream));
+    c.launches += 1;
+    plan->fix_nodes.alloc(nf);
+    plan->fix_mask.alloc(nf);
+    launch(c, k_split_keys, grid_for(nf, 256, 148 * 16), 256, 0, sorted.p, (int64_t)nf, plan->fix_nodes.p,
+           plan->fix_mask.p);
+    AFEM_CK(cudaStreamSynchronize(c.stream));
+  }
+  // z chunks: one full wave of resident CTAs when the tile count allows it
+  int occ = 1;
+  AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main, NT, 0));
+  const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
   const int64_t tiles = (int64_t)(P.NXm / TX) * ((P.NY + TY - 1) / TY);
-  int chunks = tiles > 0 ? static_cast<int>((3 * c.num_sms + tiles - 1) / tiles) : 1;
-  chunks = std::max(1, std::min(chunks, (P.NZ + 7) / 8));
+  int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
+  chunks = std::min(chunks, std::max(1, P.NZ / 8));
   plan->kchunk = (P.NZ + chunks - 1) / chunks;
+  plan->nchunks = (P.NZ + plan->kchunk - 1) / plan->kchunk;
   return plan.release();
 }
 
@@ -396,11 +522,11 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y) 
   Ctx& c = *op.sys->ctx;
   const StencilParams& P = pl.p;
   if (P.NXm > 0) {
-    dim3 grid(P.NXm / TX, (P.NY + TY - 1) / TY, (P.NZ + pl.kchunk - 1) / pl.kchunk);
+    dim3 grid(P.NXm / TX, (P.NY + TY - 1) / TY, pl.nchunks);
     launch(c, k_stencil_main, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk);
   }
   const int64_t edge = (int64_t)(P.NX - P.NXm) * P.NY * P.NZ;
-  if (edge > 0) launch(c, k_stencil_edge, grid_for(edge, 128, 148 * 16), 128, 0, P, x, pl.info.p, y);
+  if (edge > 0) launch(c, k_stencil_edge, grid_for(edge, 128, 148 * 16), 128, 0, P, x, pl.info.p, op.sys->phase.p, y);
   if (pl.n_fix > 0)
     launch(c, k_stencil_fix, grid_for(pl.n_fix, 128, 148 * 32), 128, 0, P, x, pl.info.p, op.sys->phase.p,
            pl.fix_nodes.p, pl.fix_mask.p, pl.n_fix, y);
