@@ -38,10 +38,14 @@ struct StencilParams {
   double HY[2][9][3][3];       // y face lo/hi, entries with dy = 0: index (dx+1) + 3(dz+1)
   double HZ[2][9][3][3];       // z face lo/hi, entries with dz = 0: index (dx+1) + 3(dy+1)
   double HYZ[2][2][3][3][3];   // y and z faces, entries with dy = dz = 0: index dx+1
+  // Interior family by symmetry: S(d)_aa = Dg[a][|dx|][|dy|][|dz|];
+  // S(d)_ab = sgn(d_a) sgn(d_b) Og[pair(a,b)][|d_c|] (a != b, c the third axis; zero if d_a d_b = 0).
+  double Dg[3][2][2][2];
+  double Og[3][2];             // pairs xy, xz, yz
   double K[24][24];            // uniform-brick element stiffness at E = 1
   double E[32];                // modulus per phase code (E[kVoid] = 0)
   int NX, NY, NZ;              // node counts per axis
-  int NXm;                     // columns covered by 32-wide tiles
+  int NXm;                     // columns covered by 64-wide tiles
 };
 
 struct StencilPlan {
@@ -56,10 +60,12 @@ struct StencilPlan {
 
 namespace {
 
-constexpr int TX = 32, TY = 8, NT = TX * TY;
-constexpr int RW = 3 * (TX + 2);          // doubles per staged row (x-interleaved dofs)
-constexpr int ITEMS = (TY + 2) * RW;      // doubles per staged plane
-constexpr int PER = (ITEMS + NT - 1) / NT;
+// Main-kernel tile: 8 warps, one node row per warp, each lane owns 2 adjacent x nodes (64 per row).
+constexpr int TX = 32, TXN = 2 * TX, TY = 8, NT = TX * TY;
+constexpr int SC = TXN + 4;                 // shared row: pad, halo, 64 nodes, halo, pad (16 B aligned)
+constexpr int RW = 3 * (TXN + 2);           // staged doubles per row (x-interleaved dofs of 66 nodes)
+constexpr int ITEMS = (TY + 2) * RW;        // staged doubles per plane
+constexpr int PER = (ITEMS + NT - 1) / NT;  // per-thread staging items
 
 // Structural zero of a family's entry (a, b) at offset d: the brick's reflection symmetry about
 // an axis c that the family keeps intact makes every off-diagonal entry involving c vanish when
@@ -75,103 +81,148 @@ __host__ __device__ constexpr bool szero(int dx, int dy, int dz, int a, int b, i
   return false;
 }
 
-// Coefficient family of entry (d, a, b) for a node on y face YF / z face ZF (0 none, 1 lo, 2 hi).
-template <int DX, int DY, int DZ, int YF, int ZF>
-struct Fam {
-  static constexpr bool yb = YF != 0 && DY == 0;
-  static constexpr bool zb = ZF != 0 && DZ == 0;
-  static constexpr int broken = (yb ? 2 : 0) | (zb ? 4 : 0);
-  static __device__ __forceinline__ double c(const StencilParams& P, int a, int b) {
-    if constexpr (yb && zb) return P.HYZ[YF - 1][ZF - 1][DX + 1][a][b];
-    else if constexpr (yb) return P.HY[YF - 1][(DX + 1) + 3 * (DZ + 1)][a][b];
-    else if constexpr (zb) return P.HZ[ZF - 1][(DX + 1) + 3 * (DY + 1)][a][b];
-    else return P.S[(DX + 1) + 3 * (DY + 1) + 9 * (DZ + 1)][a][b];
-  }
-};
+template <int DX, int DY, int DZ, int A>
+constexpr int dcomp() { return A == 0 ? DX : (A == 1 ? DY : DZ); }
 
-template <int DX, int DY, int DZ, int YF, int ZF>
-__device__ __forceinline__ void sblock(const StencilParams& P, const double (&xv)[3], double (&acc)[3]) {
-  using F = Fam<DX, DY, DZ, YF, ZF>;
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-      if (!szero(DX, DY, DZ, a, b, F::broken)) acc[a] = fma(F::c(P, a, b), xv[b], acc[a]);
+// Coefficient of entry (d, a, b) for a node on y face YF / z face ZF (0 none, 1 lo, 2 hi). Interior
+// entries come from the 30 symmetry-unique values (they stay resident in uniform registers).
+template <int DX, int DY, int DZ, int YF, int ZF, int A, int B>
+__device__ __forceinline__ double coef(const StencilParams& P) {
+  constexpr bool yb = YF != 0 && DY == 0;
+  constexpr bool zb = ZF != 0 && DZ == 0;
+  if constexpr (yb && zb) return P.HYZ[YF - 1][ZF - 1][DX + 1][A][B];
+  else if constexpr (yb) return P.HY[YF - 1][(DX + 1) + 3 * (DZ + 1)][A][B];
+  else if constexpr (zb) return P.HZ[ZF - 1][(DX + 1) + 3 * (DY + 1)][A][B];
+  else if constexpr (A == B) return P.Dg[A][DX != 0][DY != 0][DZ != 0];
+  else {
+    constexpr int C = 3 - A - B;
+    constexpr int pair = (A + B == 1) ? 0 : (A + B == 2 ? 1 : 2);
+    constexpr int sg = dcomp<DX, DY, DZ, A>() * dcomp<DX, DY, DZ, B>();
+    const double v = P.Og[pair][dcomp<DX, DY, DZ, C>() != 0];
+    return sg > 0 ? v : -v;
+  }
 }
 
-// All contributions of the staged plane to the thread's three column nodes.
+template <int DX, int DY, int DZ, int YF, int ZF>
+constexpr int broken_of() {
+  return ((YF != 0 && DY == 0) ? 2 : 0) | ((ZF != 0 && DZ == 0) ? 4 : 0);
+}
+
+// acc[n][r][a]: node n (0, 1) of the lane, role r (0: node below the plane sees dz = +1, 1: node on
+// the plane dz = 0, 2: node above dz = -1), component a. One neighbour column (DI, DJ), one input
+// component B, the two nodes' inputs x0, x1.
+template <int DI, int DJ, int YF, int ZF, int B>
+__device__ __forceinline__ void nb(const StencilParams& P, double x0, double x1, double (&acc)[2][3][3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if constexpr (true) {
+      if (!szero(DI, DJ, 1, a, B, broken_of<DI, DJ, 1, YF, 0>())) {
+        const double c = a == 0 ? coef<DI, DJ, 1, YF, 0, 0, B>(P) : (a == 1 ? coef<DI, DJ, 1, YF, 0, 1, B>(P)
+                                                                              : coef<DI, DJ, 1, YF, 0, 2, B>(P));
+        acc[0][0][a] = fma(c, x0, acc[0][0][a]);
+        acc[1][0][a] = fma(c, x1, acc[1][0][a]);
+      }
+      if (!szero(DI, DJ, 0, a, B, broken_of<DI, DJ, 0, YF, ZF>())) {
+        const double c = a == 0 ? coef<DI, DJ, 0, YF, ZF, 0, B>(P) : (a == 1 ? coef<DI, DJ, 0, YF, ZF, 1, B>(P)
+                                                                               : coef<DI, DJ, 0, YF, ZF, 2, B>(P));
+        acc[0][1][a] = fma(c, x0, acc[0][1][a]);
+        acc[1][1][a] = fma(c, x1, acc[1][1][a]);
+      }
+      if (!szero(DI, DJ, -1, a, B, broken_of<DI, DJ, -1, YF, 0>())) {
+        const double c = a == 0 ? coef<DI, DJ, -1, YF, 0, 0, B>(P) : (a == 1 ? coef<DI, DJ, -1, YF, 0, 1, B>(P)
+                                                                               : coef<DI, DJ, -1, YF, 0, 2, B>(P));
+        acc[0][2][a] = fma(c, x0, acc[0][2][a]);
+        acc[1][2][a] = fma(c, x1, acc[1][2][a]);
+      }
+    }
+  }
+}
+
+// One staged row DJ, one component B: 3 x LDS.128 give the 6 values around the lane's node pair.
+template <int DJ, int YF, int ZF, int B>
+__device__ __forceinline__ void row_comp(const StencilParams& P, const double* __restrict__ srow, int tx,
+                                         double (&acc)[2][3][3]) {
+  const double2* r2 = reinterpret_cast<const double2*>(srow) + tx;
+  const double2 L = r2[0], M = r2[1], R = r2[2];  // columns 2tx .. 2tx+5; the nodes are 2tx+2, 2tx+3
+  nb<-1, DJ, YF, ZF, B>(P, L.y, M.x, acc);
+  nb<0, DJ, YF, ZF, B>(P, M.x, M.y, acc);
+  nb<1, DJ, YF, ZF, B>(P, M.y, R.x, acc);
+}
+
+template <int YF, int ZF>
+__device__ __forceinline__ void plane_step(const StencilParams& P, const double* __restrict__ s, int tx, int ty,
+                                           double (&acc)[2][3][3]) {
+  // s: [3][TY+2][SC] for one buffer
+  const double* c0 = s + 0 * (TY + 2) * SC;
+  const double* c1 = s + 1 * (TY + 2) * SC;
+  const double* c2 = s + 2 * (TY + 2) * SC;
+  row_comp<-1, YF, ZF, 0>(P, c0 + (ty + 0) * SC, tx, acc);
+  row_comp<-1, YF, ZF, 1>(P, c1 + (ty + 0) * SC, tx, acc);
+  row_comp<-1, YF, ZF, 2>(P, c2 + (ty + 0) * SC, tx, acc);
+  row_comp<0, YF, ZF, 0>(P, c0 + (ty + 1) * SC, tx, acc);
+  row_comp<0, YF, ZF, 1>(P, c1 + (ty + 1) * SC, tx, acc);
+  row_comp<0, YF, ZF, 2>(P, c2 + (ty + 1) * SC, tx, acc);
+  row_comp<1, YF, ZF, 0>(P, c0 + (ty + 2) * SC, tx, acc);
+  row_comp<1, YF, ZF, 1>(P, c1 + (ty + 2) * SC, tx, acc);
+  row_comp<1, YF, ZF, 2>(P, c2 + (ty + 2) * SC, tx, acc);
+}
+
 template <int YF>
-__device__ __forceinline__ void plane_step(const StencilParams& P, const double (*sm)[TY + 2][TX + 2], int tx, int ty,
-                                           bool dprev, bool dcur, bool dnext, int zcur, double (&ap)[3],
-                                           double (&ac)[3], double (&an)[3]) {
-#define AFEM_NB(DI, DJ)                                                                                      \
-  {                                                                                                          \
-    const double xv[3] = {sm[0][ty + 1 + DJ][tx + 1 + DI], sm[1][ty + 1 + DJ][tx + 1 + DI],                  \
-                          sm[2][ty + 1 + DJ][tx + 1 + DI]};                                                  \
-    if (dnext) sblock<DI, DJ, -1, YF, 0>(P, xv, an);                                                         \
-    if (dcur) {                                                                                              \
-      if (zcur == 0) sblock<DI, DJ, 0, YF, 0>(P, xv, ac);                                                    \
-      else if (zcur == 1) sblock<DI, DJ, 0, YF, 1>(P, xv, ac);                                               \
-      else sblock<DI, DJ, 0, YF, 2>(P, xv, ac);                                                              \
-    }                                                                                                        \
-    if (dprev) sblock<DI, DJ, 1, YF, 0>(P, xv, ap);                                                          \
-  }
-  AFEM_NB(-1, -1) AFEM_NB(0, -1) AFEM_NB(1, -1)
-  AFEM_NB(-1, 0) AFEM_NB(0, 0) AFEM_NB(1, 0)
-  AFEM_NB(-1, 1) AFEM_NB(0, 1) AFEM_NB(1, 1)
-#undef AFEM_NB
+__device__ __forceinline__ void plane_dispatch(const StencilParams& P, const double* s, int tx, int ty, int zc,
+                                               double (&acc)[2][3][3]) {
+  if (zc == 0) plane_step<YF, 0>(P, s, tx, ty, acc);
+  else if (zc == 1) plane_step<YF, 1>(P, s, tx, ty, acc);
+  else plane_step<YF, 2>(P, s, tx, ty, acc);
 }
 
-__global__ void __launch_bounds__(NT, 3) k_stencil_main(const __grid_constant__ StencilParams P,
+__global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ StencilParams P,
                                                         const double* __restrict__ x,
                                                         const uint8_t* __restrict__ info, double* __restrict__ y,
                                                         int kchunk) {
-  __shared__ double sm[2][3][TY + 2][TX + 2];
+  __shared__ __align__(16) double sm[2][3][TY + 2][SC];
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int NX = P.NX, NY = P.NY, NZ = P.NZ;
-  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+  const int i0 = blockIdx.x * TXN, j0 = blockIdx.y * TY;
   const int k0 = blockIdx.z * kchunk, k1 = min(k0 + kchunk, NZ);
-  const int i = i0 + tx, j = j0 + ty;
+  const int i = i0 + 2 * tx, j = j0 + ty;
   const bool active = j < NY;
   const int yf = j == 0 ? 1 : (j == NY - 1 ? 2 : 0);
   const int64_t plane = (int64_t)NX * NY;
 
-  // Per-item staging geometry (independent of the plane): global dof offset within a plane,
-  // node offset for the info byte, component, shared-memory slot, validity.
-  int goff[PER], noff[PER], slot[PER];
-  uint8_t comp[PER];
-  bool valid[PER];
-#pragma unroll
-  for (int it = 0; it < PER; ++it) {
-    const int idx = threadIdx.x + it * NT;
-    const int r = idx / RW, c = idx - r * RW;
-    const int ii = i0 - 1 + c / 3, jj = j0 - 1 + r;
-    valid[it] = idx < ITEMS && ii >= 0 && ii < NX && jj >= 0 && jj < NY;
-    noff[it] = valid[it] ? ii + NX * jj : 0;
-    goff[it] = 3 * noff[it] + c % 3;
-    comp[it] = static_cast<uint8_t>(c % 3);
-    slot[it] = idx < ITEMS ? (c % 3) * (TY + 2) * (TX + 2) + r * (TX + 2) + c / 3 : -1;
-  }
   double pv[PER];
   uint8_t pm[PER];
-  auto fetch = [&](int p) {
+  auto fetch = [&](int p) {  // unconditional, independent loads; masking at store
     const bool inplane = p >= 0 && p < NZ;
     const int64_t pb = plane * (inplane ? p : 0);
 #pragma unroll
-    for (int it = 0; it < PER; ++it) {  // unconditional, independent loads; masking at store
-      pv[it] = __ldg(&x[3 * pb + goff[it]]);
-      pm[it] = __ldg(&info[pb + noff[it]]);
-      if (!(inplane && valid[it])) pm[it] = 0xff;
+    for (int it = 0; it < PER; ++it) {
+      const int idx = threadIdx.x + it * NT;
+      const int r = idx / RW, c = idx - r * RW;
+      const int ii = i0 - 1 + c / 3, jj = j0 - 1 + r;
+      const bool ok = inplane && idx < ITEMS && ii >= 0 && ii < NX && jj >= 0 && jj < NY;
+      const int64_t node = ok ? pb + ii + (int64_t)NX * jj : 0;
+      pv[it] = __ldg(&x[3 * node + c % 3]);
+      pm[it] = ok ? __ldg(&info[node]) : 0xff;
     }
   };
   auto store = [&](int buf) {
-    double* s = &sm[buf][0][0][0];
 #pragma unroll
-    for (int it = 0; it < PER; ++it)
-      if (slot[it] >= 0) s[slot[it]] = ((pm[it] >> comp[it]) & 1) ? 0.0 : pv[it];
+    for (int it = 0; it < PER; ++it) {
+      const int idx = threadIdx.x + it * NT;
+      if (idx < ITEMS) {
+        const int r = idx / RW, c = idx - r * RW, comp = c % 3;
+        sm[buf][comp][r][1 + c / 3] = ((pm[it] >> comp) & 1) ? 0.0 : pv[it];
+      }
+    }
   };
 
-  double ap[3] = {0.0, 0.0, 0.0}, ac[3] = {0.0, 0.0, 0.0}, an[3] = {0.0, 0.0, 0.0};
+  double acc[2][3][3];
+#pragma unroll
+  for (int n = 0; n < 2; ++n)
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) acc[n][r][a] = 0.0;
   fetch(k0 - 1);
   store(0);
   __syncthreads();
@@ -179,25 +230,31 @@ __global__ void __launch_bounds__(NT, 3) k_stencil_main(const __grid_constant__ 
     const int buf = (p - (k0 - 1)) & 1;
     if (p < k1) fetch(p + 1);
     const int64_t onode = i + (int64_t)NX * (active ? j : 0) + plane * max(p - 1, 0);
-    const uint8_t oinf = __ldg(&info[onode]);
+    const uint8_t oi0 = __ldg(&info[onode]), oi1 = __ldg(&info[onode + 1]);
     if (active && p >= 0 && p < NZ) {
-      const bool dprev = p - 1 >= k0, dcur = p >= k0 && p < k1, dnext = p + 1 < k1;
-      const int zcur = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
-      if (yf == 0) plane_step<0>(P, sm[buf], tx, ty, dprev, dcur, dnext, zcur, ap, ac, an);
-      else if (yf == 1) plane_step<1>(P, sm[buf], tx, ty, dprev, dcur, dnext, zcur, ap, ac, an);
-      else plane_step<2>(P, sm[buf], tx, ty, dprev, dcur, dnext, zcur, ap, ac, an);
+      const int zc = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
+      const double* s = &sm[buf][0][0][0];
+      if (yf == 0) plane_dispatch<0>(P, s, tx, ty, zc, acc);
+      else if (yf == 1) plane_dispatch<1>(P, s, tx, ty, zc, acc);
+      else plane_dispatch<2>(P, s, tx, ty, zc, acc);
     }
-    if (active && p - 1 >= k0) {  // node (i, j, p-1) is complete
-      const double E = P.E[oinf >> 3];
+    if (active && p - 1 >= k0) {  // nodes (i, j, p-1) and (i+1, j, p-1) are complete
+      const double E0 = P.E[oi0 >> 3], E1 = P.E[oi1 >> 3];
+      double* yo = y + 3 * onode;
 #pragma unroll
-      for (int a = 0; a < 3; ++a) y[3 * onode + a] = ((oinf >> a) & 1) ? __ldg(&x[3 * onode + a]) : E * ap[a];
+      for (int a = 0; a < 3; ++a) {
+        yo[a] = ((oi0 >> a) & 1) ? __ldg(&x[3 * onode + a]) : E0 * acc[0][0][a];
+        yo[3 + a] = ((oi1 >> a) & 1) ? __ldg(&x[3 * onode + 3 + a]) : E1 * acc[1][0][a];
+      }
     }
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      ap[a] = ac[a];
-      ac[a] = an[a];
-      an[a] = 0.0;
-    }
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        acc[n][0][a] = acc[n][1][a];
+        acc[n][1][a] = acc[n][2][a];
+        acc[n][2][a] = 0.0;
+      }
     if (p < k1) store(buf ^ 1);
     __syncthreads();
   }
@@ -444,7 +501,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   P.NX = s.nx + 1;
   P.NY = s.ny + 1;
   P.NZ = s.nz + 1;
-  P.NXm = (P.NX / TX) * TX;
+  P.NXm = (P.NX / TXN) * TXN;
   for (int k = 0; k < 32; ++k) P.E[k] = 0.0;
   for (size_t k = 0; k < s.mats.size(); ++k) P.E[k] = s.mats[k].E;
 
@@ -461,6 +518,40 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   family_stencil(K, 0, 0, fam);
   if (!snap(fam, 0)) return nullptr;
   std::memcpy(P.S, fam, sizeof P.S);
+  // Symmetry-unique interior values; every entry must agree with its representative.
+  double smax = 0.0;
+  for (int d = 0; d < 27; ++d)
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) smax = std::max(smax, std::abs(fam[d][a][b]));
+  for (int a = 0; a < 3; ++a)
+    for (int ax = 0; ax < 2; ++ax)
+      for (int ay = 0; ay < 2; ++ay)
+        for (int az = 0; az < 2; ++az) P.Dg[a][ax][ay][az] = fam[(ax + 1) + 3 * (ay + 1) + 9 * (az + 1)][a][a];
+  const int pa[3] = {0, 0, 1}, pb[3] = {1, 2, 2};
+  for (int q = 0; q < 3; ++q)
+    for (int acz = 0; acz < 2; ++acz) {
+      int dd[3] = {0, 0, 0};
+      dd[pa[q]] = 1;
+      dd[pb[q]] = 1;
+      dd[3 - pa[q] - pb[q]] = acz;
+      P.Og[q][acz] = fam[(dd[0] + 1) + 3 * (dd[1] + 1) + 9 * (dd[2] + 1)][pa[q]][pb[q]];
+    }
+  for (int d = 0; d < 27; ++d) {
+    const int dv[3] = {d % 3 - 1, (d / 3) % 3 - 1, d / 9 - 1};
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double rep;
+        if (a == b) {
+          rep = P.Dg[a][dv[0] != 0][dv[1] != 0][dv[2] != 0];
+        } else if (dv[a] == 0 || dv[b] == 0) {
+          rep = 0.0;
+        } else {
+          const int q = (a + b == 1) ? 0 : (a + b == 2 ? 1 : 2);
+          rep = (dv[a] * dv[b] > 0 ? 1.0 : -1.0) * P.Og[q][dv[3 - a - b] != 0];
+        }
+        if (std::abs(rep - fam[d][a][b]) > 1e-12 * smax) return nullptr;  // not a symmetric brick
+      }
+  }
   for (int sy = 0; sy < 2; ++sy) {
     family_stencil(K, sy + 1, 0, fam);
     if (!snap(fam, 2)) return nullptr;
@@ -510,7 +601,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   int occ = 1;
   AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main, NT, 0));
   const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
-  const int64_t tiles = (int64_t)(P.NXm / TX) * ((P.NY + TY - 1) / TY);
+  const int64_t tiles = (int64_t)(P.NXm / TXN) * ((P.NY + TY - 1) / TY);
   int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
   chunks = std::min(chunks, std::max(1, P.NZ / 8));
   plan->kchunk = (P.NZ + chunks - 1) / chunks;
@@ -522,7 +613,7 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y) 
   Ctx& c = *op.sys->ctx;
   const StencilParams& P = pl.p;
   if (P.NXm > 0) {
-    dim3 grid(P.NXm / TX, (P.NY + TY - 1) / TY, pl.nchunks);
+    dim3 grid(P.NXm / TXN, (P.NY + TY - 1) / TY, pl.nchunks);
     launch(c, k_stencil_main, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk);
   }
   const int64_t edge = (int64_t)(P.NX - P.NXm) * P.NY * P.NZ;
