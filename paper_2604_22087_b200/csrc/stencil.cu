@@ -25,6 +25,8 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "afem_impl.hpp"
@@ -56,16 +58,16 @@ struct StencilPlan {
   int64_t n_fix = 0;
   int kchunk = 16;
   int nchunks = 1;
+  int occ_variant = 3;
 };
 
 namespace {
 
 // Main-kernel tile: 8 warps, one node row per warp, each lane owns 2 adjacent x nodes (64 per row).
 constexpr int TX = 32, TXN = 2 * TX, TY = 8, NT = TX * TY;
-constexpr int SC = TXN + 4;                 // shared row: pad, halo, 64 nodes, halo, pad (16 B aligned)
-constexpr int RW = 3 * (TXN + 2);           // staged doubles per row (x-interleaved dofs of 66 nodes)
-constexpr int ITEMS = (TY + 2) * RW;        // staged doubles per plane
-constexpr int PER = (ITEMS + NT - 1) / NT;  // per-thread staging items
+constexpr int RS = 3 * (TXN + 2);            // shared row: interleaved dofs of 66 nodes (198 doubles, 16 B multiple)
+constexpr int NODES = (TY + 2) * (TXN + 2);  // staged nodes per plane (tile + one-node halo)
+constexpr int PER = (NODES + NT - 1) / NT;   // staged nodes per thread
 
 // Structural zero of a family's entry (a, b) at offset d: the brick's reflection symmetry about
 // an axis c that the family keeps intact makes every off-diagonal entry involving c vanish when
@@ -138,33 +140,30 @@ __device__ __forceinline__ void nb(const StencilParams& P, double x0, double x1,
   }
 }
 
-// One staged row DJ, one component B: 3 x LDS.128 give the 6 values around the lane's node pair.
-template <int DJ, int YF, int ZF, int B>
-__device__ __forceinline__ void row_comp(const StencilParams& P, const double* __restrict__ srow, int tx,
+// One staged row DJ: 6 LDS.128 (conflict-free, 48 B lane stride) give the 12 interleaved dofs of
+// the lane's window: left neighbour, node 0, node 1, right neighbour.
+template <int DJ, int YF, int ZF>
+__device__ __forceinline__ void row_step(const StencilParams& P, const double* __restrict__ srow, int tx,
                                          double (&acc)[2][3][3]) {
-  const double2* r2 = reinterpret_cast<const double2*>(srow) + tx;
-  const double2 L = r2[0], M = r2[1], R = r2[2];  // columns 2tx .. 2tx+5; the nodes are 2tx+2, 2tx+3
-  nb<-1, DJ, YF, ZF, B>(P, L.y, M.x, acc);
-  nb<0, DJ, YF, ZF, B>(P, M.x, M.y, acc);
-  nb<1, DJ, YF, ZF, B>(P, M.y, R.x, acc);
+  const double2* r2 = reinterpret_cast<const double2*>(srow + 6 * tx);
+  const double2 w0 = r2[0], w1 = r2[1], w2 = r2[2], w3 = r2[3], w4 = r2[4], w5 = r2[5];
+  nb<-1, DJ, YF, ZF, 0>(P, w0.x, w1.y, acc);
+  nb<-1, DJ, YF, ZF, 1>(P, w0.y, w2.x, acc);
+  nb<-1, DJ, YF, ZF, 2>(P, w1.x, w2.y, acc);
+  nb<0, DJ, YF, ZF, 0>(P, w1.y, w3.x, acc);
+  nb<0, DJ, YF, ZF, 1>(P, w2.x, w3.y, acc);
+  nb<0, DJ, YF, ZF, 2>(P, w2.y, w4.x, acc);
+  nb<1, DJ, YF, ZF, 0>(P, w3.x, w4.y, acc);
+  nb<1, DJ, YF, ZF, 1>(P, w3.y, w5.x, acc);
+  nb<1, DJ, YF, ZF, 2>(P, w4.x, w5.y, acc);
 }
 
 template <int YF, int ZF>
 __device__ __forceinline__ void plane_step(const StencilParams& P, const double* __restrict__ s, int tx, int ty,
                                            double (&acc)[2][3][3]) {
-  // s: [3][TY+2][SC] for one buffer
-  const double* c0 = s + 0 * (TY + 2) * SC;
-  const double* c1 = s + 1 * (TY + 2) * SC;
-  const double* c2 = s + 2 * (TY + 2) * SC;
-  row_comp<-1, YF, ZF, 0>(P, c0 + (ty + 0) * SC, tx, acc);
-  row_comp<-1, YF, ZF, 1>(P, c1 + (ty + 0) * SC, tx, acc);
-  row_comp<-1, YF, ZF, 2>(P, c2 + (ty + 0) * SC, tx, acc);
-  row_comp<0, YF, ZF, 0>(P, c0 + (ty + 1) * SC, tx, acc);
-  row_comp<0, YF, ZF, 1>(P, c1 + (ty + 1) * SC, tx, acc);
-  row_comp<0, YF, ZF, 2>(P, c2 + (ty + 1) * SC, tx, acc);
-  row_comp<1, YF, ZF, 0>(P, c0 + (ty + 2) * SC, tx, acc);
-  row_comp<1, YF, ZF, 1>(P, c1 + (ty + 2) * SC, tx, acc);
-  row_comp<1, YF, ZF, 2>(P, c2 + (ty + 2) * SC, tx, acc);
+  row_step<-1, YF, ZF>(P, s + (ty + 0) * RS, tx, acc);
+  row_step<0, YF, ZF>(P, s + (ty + 1) * RS, tx, acc);
+  row_step<1, YF, ZF>(P, s + (ty + 2) * RS, tx, acc);
 }
 
 template <int YF>
@@ -175,11 +174,13 @@ __device__ __forceinline__ void plane_dispatch(const StencilParams& P, const dou
   else plane_step<YF, 2>(P, s, tx, ty, acc);
 }
 
-__global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ StencilParams P,
+// OCC: resident CTAs per SM the register budget is sized for (2: 128 regs, 3: 80 regs).
+template <int OCC>
+__global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant__ StencilParams P,
                                                         const double* __restrict__ x,
                                                         const uint8_t* __restrict__ info, double* __restrict__ y,
                                                         int kchunk) {
-  __shared__ __align__(16) double sm[2][3][TY + 2][SC];
+  __shared__ __align__(16) double sm[2][TY + 2][RS];
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int NX = P.NX, NY = P.NY, NZ = P.NZ;
   const int i0 = blockIdx.x * TXN, j0 = blockIdx.y * TY;
@@ -189,31 +190,50 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
   const int yf = j == 0 ? 1 : (j == NY - 1 ? 2 : 0);
   const int64_t plane = (int64_t)NX * NY;
 
-  double pv[PER];
+  // Node-granular staging geometry, independent of the plane: node offset within a plane (-1 if
+  // outside the domain) and shared offset (-1 for unused slots).
+  int gnode[PER], soff[PER];
+#pragma unroll
+  for (int it = 0; it < PER; ++it) {
+    const int m = threadIdx.x + it * NT;
+    const int r = m / (TXN + 2), col = m - r * (TXN + 2);
+    const int ii = i0 - 1 + col, jj = j0 - 1 + r;
+    gnode[it] = (m < NODES && ii >= 0 && ii < NX && jj >= 0 && jj < NY) ? ii + NX * jj : -1;
+    soff[it] = m < NODES ? r * RS + 3 * col : -1;
+  }
+  // Plane staging with cp.async (LDGSTS): no registers held across the compute; out-of-domain
+  // nodes are zero-filled (src-size 0); Dirichlet masks are applied to the thread's own items
+  // after the wait, before the block barrier.
   uint8_t pm[PER];
-  auto fetch = [&](int p) {  // unconditional, independent loads; masking at store
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(&sm[0][0][0]));
+  auto fetch = [&](int p, int buf) {
     const bool inplane = p >= 0 && p < NZ;
     const int64_t pb = plane * (inplane ? p : 0);
 #pragma unroll
     for (int it = 0; it < PER; ++it) {
-      const int idx = threadIdx.x + it * NT;
-      const int r = idx / RW, c = idx - r * RW;
-      const int ii = i0 - 1 + c / 3, jj = j0 - 1 + r;
-      const bool ok = inplane && idx < ITEMS && ii >= 0 && ii < NX && jj >= 0 && jj < NY;
-      const int64_t node = ok ? pb + ii + (int64_t)NX * jj : 0;
-      pv[it] = __ldg(&x[3 * node + c % 3]);
-      pm[it] = ok ? __ldg(&info[node]) : 0xff;
-    }
-  };
-  auto store = [&](int buf) {
+      if (soff[it] < 0) continue;
+      const bool ok = inplane && gnode[it] >= 0;
+      const int64_t node = pb + (ok ? gnode[it] : 0);
+      const uint32_t dst = sbase + 8u * static_cast<uint32_t>(buf * (TY + 2) * RS + soff[it]);
+      const double* src = x + 3 * node;
+      const int sz = ok ? 8 : 0;
 #pragma unroll
-    for (int it = 0; it < PER; ++it) {
-      const int idx = threadIdx.x + it * NT;
-      if (idx < ITEMS) {
-        const int r = idx / RW, c = idx - r * RW, comp = c % 3;
-        sm[buf][comp][r][1 + c / 3] = ((pm[it] >> comp) & 1) ? 0.0 : pv[it];
-      }
+      for (int c = 0; c < 3; ++c)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst + 8u * c), "l"(src + c), "r"(sz)
+                     : "memory");
+      pm[it] = ok ? __ldg(&info[node]) : 0;
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  auto land = [&](int buf) {  // wait for own copies, apply own masks
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    double* s = &sm[buf][0][0];
+#pragma unroll
+    for (int it = 0; it < PER; ++it)
+      if (soff[it] >= 0 && (pm[it] & 7))
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if ((pm[it] >> c) & 1) s[soff[it] + c] = 0.0;
   };
 
   double acc[2][3][3];
@@ -223,17 +243,17 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int a = 0; a < 3; ++a) acc[n][r][a] = 0.0;
-  fetch(k0 - 1);
-  store(0);
+  fetch(k0 - 1, 0);
+  land(0);
   __syncthreads();
   for (int p = k0 - 1; p <= k1; ++p) {
     const int buf = (p - (k0 - 1)) & 1;
-    if (p < k1) fetch(p + 1);
+    if (p < k1) fetch(p + 1, buf ^ 1);
     const int64_t onode = i + (int64_t)NX * (active ? j : 0) + plane * max(p - 1, 0);
     const uint8_t oi0 = __ldg(&info[onode]), oi1 = __ldg(&info[onode + 1]);
     if (active && p >= 0 && p < NZ) {
       const int zc = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
-      const double* s = &sm[buf][0][0][0];
+      const double* s = &sm[buf][0][0];
       if (yf == 0) plane_dispatch<0>(P, s, tx, ty, zc, acc);
       else if (yf == 1) plane_dispatch<1>(P, s, tx, ty, zc, acc);
       else plane_dispatch<2>(P, s, tx, ty, zc, acc);
@@ -255,10 +275,11 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
         acc[n][1][a] = acc[n][2][a];
         acc[n][2][a] = 0.0;
       }
-    if (p < k1) store(buf ^ 1);
+    if (p < k1) land(buf ^ 1);
     __syncthreads();
   }
 }
+
 
 __host__ __device__ __forceinline__ int local_node(int lx, int ly, int lz) {
   const int ring = lx ? (ly ? 2 : 1) : (ly ? 3 : 0);  // element.hpp:22-23 ring, then z = +1
@@ -597,9 +618,14 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
            plan->fix_mask.p);
     AFEM_CK(cudaStreamSynchronize(c.stream));
   }
-  // z chunks: one full wave of resident CTAs when the tile count allows it
+  // variant (register budget) and z chunks: one full wave of resident CTAs when tiles allow it
+  const char* env = std::getenv("AFEM_STENCIL_OCC");
+  plan->occ_variant = (env && std::atoi(env) == 2) ? 2 : 3;
   int occ = 1;
-  AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main, NT, 0));
+  if (plan->occ_variant == 2)
+    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<2>, NT, 0));
+  else
+    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<3>, NT, 0));
   const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
   const int64_t tiles = (int64_t)(P.NXm / TXN) * ((P.NY + TY - 1) / TY);
   int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
@@ -614,7 +640,8 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y) 
   const StencilParams& P = pl.p;
   if (P.NXm > 0) {
     dim3 grid(P.NXm / TXN, (P.NY + TY - 1) / TY, pl.nchunks);
-    launch(c, k_stencil_main, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk);
+    if (pl.occ_variant == 2) launch(c, k_stencil_main<2>, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk);
+    else launch(c, k_stencil_main<3>, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk);
   }
   const int64_t edge = (int64_t)(P.NX - P.NXm) * P.NY * P.NZ;
   if (edge > 0) launch(c, k_stencil_edge, grid_for(edge, 128, 148 * 16), 128, 0, P, x, pl.info.p, op.sys->phase.p, y);
