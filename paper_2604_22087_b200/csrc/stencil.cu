@@ -9,21 +9,22 @@
 // coefficients), and E_base(n) the majority modulus over F(n) (octants void in x count as E = 0).
 //
 // Kernels:
-//  k_stencil_main   32x8 node tile per CTA, marching in z over a chunk of planes (one wave); each
-//                   x-plane (one-node halo, Dirichlet-masked) is staged once in shared memory
-//                   (double-buffered, register prefetch, one barrier per plane) and each thread
-//                   keeps the partial sums of the three column nodes the plane touches. 153 DFMA
-//                   per interior node (the 243-entry stencil minus the 90 symmetry zeros), all
-//                   coefficients in the kernel-parameter constant bank; y/z faces switch to the
-//                   half/quarter coefficient families (warp- or CTA-uniform). No atomics; every y
-//                   entry is written exactly once by this kernel.
-//  k_stencil_edge   the x columns a 32-wide tile cannot cover (NX mod 32): exact octant form.
-//  k_stencil_fix    nodes whose family F(n) mixes moduli (fibre interfaces, the x = 0 face): adds
-//                   the octant corrections; the list is sorted by octant mask so each warp's
-//                   octant loop is uniform (Khat rows stay uniform constant-bank operands).
+//  k_stencil_main   64x8 node tile per CTA (8 warps, one row per warp, 2 nodes per lane), marching
+//                   in z over a chunk of planes (one wave); each x-plane (one-node halo) is staged
+//                   once in shared memory in the interleaved dof layout with cp.async (zero-fill out
+//                   of the domain, Dirichlet masks applied after landing; double-buffered, one
+//                   barrier per plane) and each lane keeps the partial sums of the six column nodes
+//                   the plane touches. 153 DFMA per interior node (the 243-entry stencil minus the
+//                   90 symmetry zeros) over 30 symmetry-unique coefficients held in (uniform)
+//                   registers; y/z faces switch to the half/quarter families (warp- or CTA-uniform).
+//                   No atomics; every y entry of the covered columns is written exactly once.
+//  k_stencil_items  one thread per (node, octant) correction: mixed-family nodes (fibre
+//                   interfaces, the x = 0 face) add dE Khat_rows x_e; the NX mod 64 edge columns are
+//                   written in exact octant form. Segmented, fixed-order shuffle sums per node.
 // Algorithmic traffic of the main kernel: x (8 B/dof) + y (8 B/dof) + one info byte per node.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -53,9 +54,12 @@ struct StencilParams {
 struct StencilPlan {
   StencilParams p;
   DevArray<uint8_t> info;       // per node: bits 0-2 Dirichlet mask, bits 3-7 base phase code
-  DevArray<int32_t> fix_nodes;  // nodes needing octant corrections, sorted by mask
-  DevArray<uint8_t> fix_mask;   // their octant masks
-  int64_t n_fix = 0;
+  // correction items (k_stencil_items): mixed-family nodes and the edge columns
+  DevArray<int32_t> it_node;
+  DevArray<uint8_t> it_oct, it_seg, it_mode;
+  DevArray<double> it_dE;
+  int64_t n_items = 0;   // padded to a multiple of 32
+  int64_t n_fix_nodes = 0, n_edge_nodes = 0;
   int kchunk = 16;
   int nchunks = 1;
   int occ_variant = 3;
@@ -190,50 +194,63 @@ __global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant_
   const int yf = j == 0 ? 1 : (j == NY - 1 ? 2 : 0);
   const int64_t plane = (int64_t)NX * NY;
 
-  // Node-granular staging geometry, independent of the plane: node offset within a plane (-1 if
-  // outside the domain) and shared offset (-1 for unused slots).
-  int gnode[PER], soff[PER];
-#pragma unroll
-  for (int it = 0; it < PER; ++it) {
-    const int m = threadIdx.x + it * NT;
-    const int r = m / (TXN + 2), col = m - r * (TXN + 2);
-    const int ii = i0 - 1 + col, jj = j0 - 1 + r;
-    gnode[it] = (m < NODES && ii >= 0 && ii < NX && jj >= 0 && jj < NY) ? ii + NX * jj : -1;
-    soff[it] = m < NODES ? r * RS + 3 * col : -1;
-  }
   // Plane staging with cp.async (LDGSTS): no registers held across the compute; out-of-domain
-  // nodes are zero-filled (src-size 0); Dirichlet masks are applied to the thread's own items
-  // after the wait, before the block barrier.
-  uint8_t pm[PER];
+  // nodes are zero-filled (src-size 0); Dirichlet masks are applied to the thread's own slots after
+  // the wait, before the block barrier. Slots (warp-row mapping, geometry recomputed, no division
+  // except the 132-node extra rows): s0/s1/s2 = row ty, columns lane, lane+32, lane+64 (< 66);
+  // s3 = rows 8-9 spread over the block.
+  const int lane = tx;
+  const int q3 = ty * 32 + lane;
+  const int r3 = TY + q3 / (TXN + 2), c3 = q3 % (TXN + 2);
+  auto slot = [&](int s, int& r, int& col) -> bool {
+    if (s < 3) {
+      r = ty;
+      col = lane + 32 * s;
+      return col < TXN + 2;
+    }
+    r = r3;
+    col = c3;
+    return q3 < 2 * (TXN + 2);
+  };
+  uint32_t pm = 0;
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(&sm[0][0][0]));
   auto fetch = [&](int p, int buf) {
     const bool inplane = p >= 0 && p < NZ;
     const int64_t pb = plane * (inplane ? p : 0);
+    pm = 0;
 #pragma unroll
-    for (int it = 0; it < PER; ++it) {
-      if (soff[it] < 0) continue;
-      const bool ok = inplane && gnode[it] >= 0;
-      const int64_t node = pb + (ok ? gnode[it] : 0);
-      const uint32_t dst = sbase + 8u * static_cast<uint32_t>(buf * (TY + 2) * RS + soff[it]);
+    for (int s = 0; s < 4; ++s) {
+      int r, col;
+      if (!slot(s, r, col)) continue;
+      const int ii = i0 - 1 + col, jj = j0 - 1 + r;
+      const bool ok = inplane && ii >= 0 && ii < NX && jj >= 0 && jj < NY;
+      const int64_t node = ok ? pb + ii + (int64_t)NX * jj : 0;
+      const uint32_t dst = sbase + 8u * static_cast<uint32_t>(buf * (TY + 2) * RS + r * RS + 3 * col);
       const double* src = x + 3 * node;
       const int sz = ok ? 8 : 0;
 #pragma unroll
       for (int c = 0; c < 3; ++c)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst + 8u * c), "l"(src + c), "r"(sz)
                      : "memory");
-      pm[it] = ok ? __ldg(&info[node]) : 0;
+      if (ok) pm |= static_cast<uint32_t>(__ldg(&info[node]) & 7) << (8 * s);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
   auto land = [&](int buf) {  // wait for own copies, apply own masks
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    double* s = &sm[buf][0][0];
+    if (pm) {
+      double* sb = &sm[buf][0][0];
 #pragma unroll
-    for (int it = 0; it < PER; ++it)
-      if (soff[it] >= 0 && (pm[it] & 7))
+      for (int s = 0; s < 4; ++s) {
+        const uint32_t m = (pm >> (8 * s)) & 7;
+        if (!m) continue;
+        int r, col;
+        slot(s, r, col);
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-          if ((pm[it] >> c) & 1) s[soff[it] + c] = 0.0;
+          if ((m >> c) & 1) sb[r * RS + 3 * col + c] = 0.0;
+      }
+    }
   };
 
   double acc[2][3][3];
@@ -288,103 +305,96 @@ __host__ __device__ __forceinline__ int local_node(int lx, int ly, int lz) {
 __host__ __device__ __forceinline__ int corner_x(int m) { return ((m & 3) == 1 || (m & 3) == 2) ? 1 : 0; }
 __host__ __device__ __forceinline__ int corner_y(int m) { return (m & 3) >= 2 ? 1 : 0; }
 
-// Khat_rows(o) x_e(o) for octant o of node (i, j, k): masked x, zero outside the domain.
-__device__ __forceinline__ void octant_action(const StencilParams& P, const double* __restrict__ x,
-                                              const uint8_t* __restrict__ info, int i, int j, int k, int o,
-                                              double (&t)[3]) {
+// Correction items: one thread per (node, octant) pair. y_n receives dE * Khat_rows(o) x_e(o) with
+// dE = E_o - E_base(n) for mixed-family nodes of the main kernel, and dE = E_o (written, not added)
+// for the edge columns the main kernel does not cover. Items of a node are contiguous, in octant
+// order, and never straddle a warp (the plan pads); the segment head sums them with shuffles in a
+// fixed order and updates y — deterministic, no atomics. Khat is staged in shared memory as
+// Ks[q][a][ln] so lanes of different octants read adjacent words (conflict-free).
+constexpr int kItemThreads = 256;
+
+struct Items {
+  const int32_t* node;   // -1: padding
+  const uint8_t* oct;    // octant
+  const uint8_t* seg;    // head: number of items of the node (1..8); 0: not a head
+  const uint8_t* mode;   // head: 1 = edge node (write), 0 = add
+  const double* dE;
+  int64_t n;             // padded count (multiple of 32)
+};
+
+__global__ void __launch_bounds__(kItemThreads) k_stencil_items(const __grid_constant__ StencilParams P,
+                                                                 const double* __restrict__ x,
+                                                                 const uint8_t* __restrict__ info, Items it,
+                                                                 double* __restrict__ y) {
+  __shared__ double Ks[24][3][8];
+  for (int t = threadIdx.x; t < 576; t += blockDim.x) {
+    const int q = t / 24, r = t % 24;  // Ks[q][a][ln] = Khat[3 ln + a][q]
+    Ks[q][r % 3][r / 3] = P.K[r][q];
+  }
+  __syncthreads();
   const int NX = P.NX, NY = P.NY, NZ = P.NZ;
-  const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
-  const int ei = i - 1 + ox, ej = j - 1 + oy, ek = k - 1 + oz;
-  const int ln = local_node(1 - ox, 1 - oy, 1 - oz);
-  double xv[24];
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < it.n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = base + threadIdx.x;
+    const int32_t node = t < it.n ? it.node[t] : -1;
+    double r[3] = {0.0, 0.0, 0.0};
+    int i = 0, j = 0, k = 0;
+    if (node >= 0) {
+      i = node % NX;
+      const int rr = node / NX;
+      j = rr % NY;
+      k = rr / NY;
+      const int o = it.oct[t];
+      const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+      const int ei = i - 1 + ox, ej = j - 1 + oy, ek = k - 1 + oz;
+      const int ln = local_node(1 - ox, 1 - oy, 1 - oz);
+      double xv[24];
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const int ii = ei + corner_x(m), jj = ej + corner_y(m), kk = ek + (m >> 2);
-    const bool in = ii >= 0 && ii < NX && jj >= 0 && jj < NY && kk >= 0 && kk < NZ;
-    const int64_t node = in ? ii + (int64_t)NX * (jj + (int64_t)NY * kk) : 0;
-    const uint8_t inf = in ? __ldg(&info[node]) : 0x7;
+      for (int m = 0; m < 8; ++m) {  // 24 independent loads in flight
+        const int ii = ei + corner_x(m), jj = ej + corner_y(m), kk = ek + (m >> 2);
+        const bool in = ii >= 0 && ii < NX && jj >= 0 && jj < NY && kk >= 0 && kk < NZ;
+        const int64_t nd = in ? ii + (int64_t)NX * (jj + (int64_t)NY * kk) : 0;
+        const uint8_t inf = in ? __ldg(&info[nd]) : 0x7;
 #pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      const double v = __ldg(&x[3 * node + b]);
-      xv[3 * m + b] = ((inf >> b) & 1) ? 0.0 : v;
+        for (int b = 0; b < 3; ++b) {
+          const double v = __ldg(&x[3 * nd + b]);
+          xv[3 * m + b] = ((inf >> b) & 1) ? 0.0 : v;
+        }
+      }
+      const double dE = it.dE[t];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 24; ++q) s = fma(Ks[q][a][ln], xv[q], s);
+        r[a] = dE * s;
+      }
     }
-  }
+    const int L = t < it.n ? it.seg[t] : 0;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < 24; ++q) s = fma(P.K[3 * ln + a][q], xv[q], s);
-    t[a] = s;
-  }
-}
-
-__device__ __forceinline__ int octant_phase(const StencilParams& P, const uint8_t* __restrict__ phase, int i, int j,
-                                            int k, int o) {
-  const int ex = P.NX - 1, ey = P.NY - 1, ez = P.NZ - 1;
-  const int ei = i - 1 + (o & 1), ej = j - 1 + ((o >> 1) & 1), ek = k - 1 + (o >> 2);
-  const bool inside = ei >= 0 && ei < ex && ej >= 0 && ej < ey && ek >= 0 && ek < ez;
-  return inside ? phase[ei + (int64_t)ex * (ej + (int64_t)ey * ek)] : kVoid;
-}
-
-// Columns i >= NXm: exact octant form y_n = sum_o E_o Khat_rows(o) x_e(o).
-__global__ void k_stencil_edge(const __grid_constant__ StencilParams P, const double* __restrict__ x,
-                               const uint8_t* __restrict__ info, const uint8_t* __restrict__ phase,
-                               double* __restrict__ y) {
-  const int NX = P.NX, NY = P.NY, NZ = P.NZ, W = NX - P.NXm;
-  const int64_t total = (int64_t)W * NY * NZ;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int i = P.NXm + static_cast<int>(t % W);
-    const int64_t r = t / W;
-    const int j = static_cast<int>(r % NY), k = static_cast<int>(r / NY);
-    double acc[3] = {0.0, 0.0, 0.0};
-    for (int o = 0; o < 8; ++o) {
-      const double E = P.E[octant_phase(P, phase, i, j, k, o)];
-      if (E == 0.0) continue;
-      double tv[3];
-      octant_action(P, x, info, i, j, k, o, tv);
-#pragma unroll
-      for (int a = 0; a < 3; ++a) acc[a] = fma(E, tv[a], acc[a]);
+    for (int d = 1; d < 8; ++d) {
+      const double v0 = __shfl_down_sync(0xffffffffu, r[0], d);
+      const double v1 = __shfl_down_sync(0xffffffffu, r[1], d);
+      const double v2 = __shfl_down_sync(0xffffffffu, r[2], d);
+      if (d < L) {  // segments never cross the warp, so lane + d < 32 here
+        r[0] += v0;
+        r[1] += v1;
+        r[2] += v2;
+      }
     }
-    const int64_t node = i + (int64_t)NX * (j + (int64_t)NY * k);
-    const uint8_t inf = info[node];
+    if (L > 0 && node >= 0) {
+      (void)lane;
+      const uint8_t inf = __ldg(&info[node]);
+      double* yo = y + 3 * (int64_t)node;
+      if (it.mode[t]) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) y[3 * node + a] = ((inf >> a) & 1) ? x[3 * node + a] : acc[a];
-  }
-}
-
-// Octant corrections for the (mask-sorted) fix list; free rows only.
-__global__ void __launch_bounds__(128) k_stencil_fix(const __grid_constant__ StencilParams P,
-                                                     const double* __restrict__ x, const uint8_t* __restrict__ info,
-                                                     const uint8_t* __restrict__ phase,
-                                                     const int32_t* __restrict__ nodes,
-                                                     const uint8_t* __restrict__ omask, int64_t n_fix,
-                                                     double* __restrict__ y) {
-  const int NX = P.NX, NY = P.NY;
-  for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x; t0 < n_fix; t0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = t0 + threadIdx.x;
-    const bool live = t < n_fix;
-    const int64_t node = live ? nodes[t] : 0;
-    const uint8_t om = live ? omask[t] : 0;
-    const int i = static_cast<int>(node % NX);
-    const int64_t r = node / NX;
-    const int j = static_cast<int>(r % NY), k = static_cast<int>(r / NY);
-    const uint8_t inf = info[node];
-    const double Eb = P.E[inf >> 3];
-    double acc[3] = {0.0, 0.0, 0.0};
-#pragma unroll 1
-    for (int o = 0; o < 8; ++o) {
-      const bool mine = (om >> o) & 1;
-      if (!__any_sync(0xffffffffu, mine)) continue;  // octant loop uniform across the warp
-      double tv[3];
-      octant_action(P, x, info, i, j, k, o, tv);
-      const double dE = mine ? P.E[octant_phase(P, phase, i, j, k, o)] - Eb : 0.0;
+        for (int a = 0; a < 3; ++a) yo[a] = ((inf >> a) & 1) ? x[3 * (int64_t)node + a] : r[a];
+      } else {
 #pragma unroll
-      for (int a = 0; a < 3; ++a) acc[a] = fma(dE, tv[a], acc[a]);
+        for (int a = 0; a < 3; ++a)
+          if (!((inf >> a) & 1)) yo[a] += r[a];
+      }
     }
-    if (live)
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-        if (!((inf >> a) & 1)) y[3 * node + a] += acc[a];
   }
 }
 
@@ -433,12 +443,6 @@ __global__ void k_stencil_classify(int NX, int NY, int NZ, int NXm, const uint8_
   }
 }
 
-__global__ void k_split_keys(const uint64_t* keys, int64_t n, int32_t* nodes, uint8_t* masks) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    nodes[t] = static_cast<int32_t>(keys[t] & 0xffffffffu);
-    masks[t] = static_cast<uint8_t>(keys[t] >> 32);
-  }
-}
 
 // Uniform-brick element stiffness at E = 1 (same device math as the general tangent kernel).
 __global__ void k_brick_stiffness(const double* coords, const int32_t* conn, DMat m, double* K) {
@@ -604,19 +608,80 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   unsigned long long nf = 0;
   AFEM_CK(cudaMemcpyAsync(&nf, cnt.p, 8, cudaMemcpyDeviceToHost, c.stream));
   AFEM_CK(cudaStreamSynchronize(c.stream));
-  plan->n_fix = static_cast<int64_t>(nf);
-  if (nf) {  // sort by (octant mask, node): warps see uniform octant loops and nearby nodes
-    DevArray<uint64_t> sorted(nf);
-    size_t tmp = 0;
-    AFEM_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.p, sorted.p, (int)nf, 0, 40, c.stream));
-    DevArray<uint8_t> tb(tmp);
-    AFEM_CK(cub::DeviceRadixSort::SortKeys(tb.p, tmp, keys.p, sorted.p, (int)nf, 0, 40, c.stream));
-    c.launches += 1;
-    plan->fix_nodes.alloc(nf);
-    plan->fix_mask.alloc(nf);
-    launch(c, k_split_keys, grid_for(nf, 256, 148 * 16), 256, 0, sorted.p, (int64_t)nf, plan->fix_nodes.p,
-           plan->fix_mask.p);
+  {
+    // Correction items, built on the host once per operator: (node, octant, dE) for every octant of
+    // a mixed-family node whose modulus differs from the node's base, and for every existing octant
+    // of the edge-column nodes (base 0, written). Node order; a node's items never cross a warp.
+    std::vector<uint64_t> hk(nf);
+    if (nf) AFEM_CK(cudaMemcpyAsync(hk.data(), keys.p, nf * 8, cudaMemcpyDeviceToHost, c.stream));
+    std::vector<uint8_t> hph(s.n_elem), hinfo(nn);
+    AFEM_CK(cudaMemcpyAsync(hph.data(), s.phase.p, s.n_elem, cudaMemcpyDeviceToHost, c.stream));
+    AFEM_CK(cudaMemcpyAsync(hinfo.data(), plan->info.p, nn, cudaMemcpyDeviceToHost, c.stream));
     AFEM_CK(cudaStreamSynchronize(c.stream));
+    struct NodeMask { int64_t node; uint8_t mask; bool edge; };
+    std::vector<NodeMask> list;
+    list.reserve(nf + (size_t)(P.NX - P.NXm) * P.NY * P.NZ);
+    for (uint64_t k : hk) list.push_back({static_cast<int64_t>(k & 0xffffffffu), static_cast<uint8_t>(k >> 32), false});
+    const int ex = P.NX - 1, ey = P.NY - 1, ez = P.NZ - 1;
+    auto oct_phase = [&](int64_t node, int o) -> int {
+      const int i = static_cast<int>(node % P.NX);
+      const int64_t r = node / P.NX;
+      const int j = static_cast<int>(r % P.NY), k = static_cast<int>(r / P.NY);
+      const int ei = i - 1 + (o & 1), ej = j - 1 + ((o >> 1) & 1), ek = k - 1 + (o >> 2);
+      const bool inside = ei >= 0 && ei < ex && ej >= 0 && ej < ey && ek >= 0 && ek < ez;
+      return inside ? hph[ei + (int64_t)ex * (ej + (int64_t)ey * ek)] : kVoid;
+    };
+    for (int k = 0; k < P.NZ; ++k)
+      for (int j = 0; j < P.NY; ++j)
+        for (int i = P.NXm; i < P.NX; ++i) {
+          const int64_t node = i + (int64_t)P.NX * (j + (int64_t)P.NY * k);
+          uint8_t m = 0;
+          for (int o = 0; o < 8; ++o)
+            if (oct_phase(node, o) != kVoid) m |= static_cast<uint8_t>(1u << o);
+          list.push_back({node, m, true});
+        }
+    std::sort(list.begin(), list.end(), [](const NodeMask& a, const NodeMask& b) { return a.node < b.node; });
+    std::vector<int32_t> inode;
+    std::vector<uint8_t> ioct, iseg, imode;
+    std::vector<double> idE;
+    for (const NodeMask& nm : list) {
+      const int L = __builtin_popcount(nm.mask);
+      if (L == 0) continue;
+      if ((inode.size() % 32) + L > 32)
+        while (inode.size() % 32) {  // pad to the warp boundary
+          inode.push_back(-1); ioct.push_back(0); iseg.push_back(0); imode.push_back(0); idE.push_back(0.0);
+        }
+      const double Eb = nm.edge ? 0.0 : P.E[hinfo[nm.node] >> 3];
+      bool head = true;
+      for (int o = 0; o < 8; ++o) {
+        if (!((nm.mask >> o) & 1)) continue;
+        inode.push_back(static_cast<int32_t>(nm.node));
+        ioct.push_back(static_cast<uint8_t>(o));
+        iseg.push_back(head ? static_cast<uint8_t>(L) : 0);
+        imode.push_back(nm.edge ? 1 : 0);
+        idE.push_back(P.E[oct_phase(nm.node, o)] - Eb);
+        head = false;
+      }
+      (nm.edge ? plan->n_edge_nodes : plan->n_fix_nodes) += 1;
+    }
+    while (inode.size() % 32) {
+      inode.push_back(-1); ioct.push_back(0); iseg.push_back(0); imode.push_back(0); idE.push_back(0.0);
+    }
+    const size_t n = inode.size();
+    plan->n_items = static_cast<int64_t>(n);
+    if (n) {
+      plan->it_node.alloc(n);
+      plan->it_oct.alloc(n);
+      plan->it_seg.alloc(n);
+      plan->it_mode.alloc(n);
+      plan->it_dE.alloc(n);
+      AFEM_CK(cudaMemcpyAsync(plan->it_node.p, inode.data(), n * 4, cudaMemcpyHostToDevice, c.stream));
+      AFEM_CK(cudaMemcpyAsync(plan->it_oct.p, ioct.data(), n, cudaMemcpyHostToDevice, c.stream));
+      AFEM_CK(cudaMemcpyAsync(plan->it_seg.p, iseg.data(), n, cudaMemcpyHostToDevice, c.stream));
+      AFEM_CK(cudaMemcpyAsync(plan->it_mode.p, imode.data(), n, cudaMemcpyHostToDevice, c.stream));
+      AFEM_CK(cudaMemcpyAsync(plan->it_dE.p, idE.data(), n * 8, cudaMemcpyHostToDevice, c.stream));
+      AFEM_CK(cudaStreamSynchronize(c.stream));
+    }
   }
   // variant (register budget) and z chunks: one full wave of resident CTAs when tiles allow it
   const char* env = std::getenv("AFEM_STENCIL_OCC");
@@ -643,11 +708,10 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y) 
     if (pl.occ_variant == 2) launch(c, k_stencil_main<2>, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk);
     else launch(c, k_stencil_main<3>, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk);
   }
-  const int64_t edge = (int64_t)(P.NX - P.NXm) * P.NY * P.NZ;
-  if (edge > 0) launch(c, k_stencil_edge, grid_for(edge, 128, 148 * 16), 128, 0, P, x, pl.info.p, op.sys->phase.p, y);
-  if (pl.n_fix > 0)
-    launch(c, k_stencil_fix, grid_for(pl.n_fix, 128, 148 * 32), 128, 0, P, x, pl.info.p, op.sys->phase.p,
-           pl.fix_nodes.p, pl.fix_mask.p, pl.n_fix, y);
+  if (pl.n_items > 0) {
+    const Items it{pl.it_node.p, pl.it_oct.p, pl.it_seg.p, pl.it_mode.p, pl.it_dE.p, pl.n_items};
+    launch(c, k_stencil_items, grid_for(pl.n_items, kItemThreads, 148 * 8), kItemThreads, 0, P, x, pl.info.p, it, y);
+  }
 }
 
 void destroy_stencil_plan(StencilPlan* p) { delete p; }
