@@ -58,6 +58,7 @@ struct StencilPlan {
   DevArray<int32_t> it_node;
   DevArray<uint8_t> it_oct, it_seg, it_mode;
   DevArray<double> it_dE;
+  DevArray<double> Kg;   // Khat (row-major 24 x 24) in global memory for the item kernel
   int64_t n_items = 0;   // padded to a multiple of 32
   int64_t n_fix_nodes = 0, n_edge_nodes = 0;
   int kchunk = 16;
@@ -322,17 +323,17 @@ struct Items {
   int64_t n;             // padded count (multiple of 32)
 };
 
-__global__ void __launch_bounds__(kItemThreads) k_stencil_items(const __grid_constant__ StencilParams P,
+__global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, int NZ,
+                                                                 const double* __restrict__ Kg,
                                                                  const double* __restrict__ x,
                                                                  const uint8_t* __restrict__ info, Items it,
                                                                  double* __restrict__ y) {
   __shared__ double Ks[24][3][8];
-  for (int t = threadIdx.x; t < 576; t += blockDim.x) {
-    const int q = t / 24, r = t % 24;  // Ks[q][a][ln] = Khat[3 ln + a][q]
-    Ks[q][r % 3][r / 3] = P.K[r][q];
+  for (int t = threadIdx.x; t < 576; t += blockDim.x) {  // coalesced global read of Khat (row-major)
+    const int r = t / 24, q = t % 24;                    // Ks[q][a][ln] = Khat[3 ln + a][q]
+    Ks[q][r % 3][r / 3] = __ldg(&Kg[t]);
   }
   __syncthreads();
-  const int NX = P.NX, NY = P.NY, NZ = P.NZ;
   const int lane = threadIdx.x & 31;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < it.n; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = base + threadIdx.x;
@@ -539,6 +540,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   AFEM_CK(cudaStreamSynchronize(c.stream));
   for (int r = 0; r < 24; ++r)
     for (int q = 0; q < 24; ++q) P.K[r][q] = K[r * 24 + q];
+  plan->Kg = std::move(dK);
   double fam[27][3][3];
   family_stencil(K, 0, 0, fam);
   if (!snap(fam, 0)) return nullptr;
@@ -710,7 +712,8 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y) 
   }
   if (pl.n_items > 0) {
     const Items it{pl.it_node.p, pl.it_oct.p, pl.it_seg.p, pl.it_mode.p, pl.it_dE.p, pl.n_items};
-    launch(c, k_stencil_items, grid_for(pl.n_items, kItemThreads, 148 * 8), kItemThreads, 0, P, x, pl.info.p, it, y);
+    launch(c, k_stencil_items, grid_for(pl.n_items, kItemThreads, 4 * c.num_sms), kItemThreads, 0, P.NX, P.NY, P.NZ,
+           pl.Kg.p, x, pl.info.p, it, y);
   }
 }
 
