@@ -99,6 +99,8 @@ struct Operator {
   int64_t n = 0;
   virtual void validate() const {}
   virtual void apply(const double* x, double* y) = 0;  // device pointers, ctx stream, async
+  // y = A x and dot_out[0] = x.y in one pass (deterministic); false if the operator cannot fuse.
+  virtual bool apply_dot(const double*, double*, double*) { return false; }
   virtual void diagonal(double* d) = 0;                 // device pointer
   virtual bool uses_stencil() const { return false; }
 };
@@ -117,6 +119,7 @@ struct MfOp : Operator {
   StencilPlan* stencil = nullptr;  // owned; released by destroy_stencil_plan
   ~MfOp() override;
   void apply(const double* x, double* y) override;
+  bool apply_dot(const double* x, double* y, double* dot_out) override;
   void diagonal(double* d) override;
   bool uses_stencil() const override { return stencil != nullptr; }
 };
@@ -172,7 +175,7 @@ void solve(Operator& op, const SolverCfg& cfg, const double* b, const double* x0
 
 // ---- stencil.cu
 StencilPlan* make_stencil_plan(System& s, const MfOp& op);  // nullptr when not applicable
-void stencil_apply(StencilPlan& p, const MfOp& op, const double* x, double* y);
+void stencil_apply(StencilPlan& p, const MfOp& op, const double* x, double* y, double* dot_out = nullptr);
 void destroy_stencil_plan(StencilPlan* p);
 
 }  // namespace afem

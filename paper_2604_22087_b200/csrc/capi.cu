@@ -45,6 +45,11 @@ void MfOp::apply(const double* x, double* y) {
   if (stencil) stencil_apply(*stencil, *this, x, y);
   else mf_apply_general(*sys, state.p, mask.p, x, y);
 }
+bool MfOp::apply_dot(const double* x, double* y, double* dot_out) {
+  if (!stencil) return false;
+  stencil_apply(*stencil, *this, x, y, dot_out);
+  return true;
+}
 void MfOp::diagonal(double* d) { copy(*sys->ctx, diag.p, d, n); }
 
 __global__ void k_unit_on_mask(const uint8_t* mask, double* d, int64_t n) {

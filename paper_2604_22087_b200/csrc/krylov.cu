@@ -40,13 +40,12 @@ __global__ void k_residual_vec(const double* b, const double* ax, double* r, int
     if (threadIdx.x == 0) out[0] = sqrt(v[0]);
 }
 
-// z = M r; p = z; rz = r.z
-__global__ void k_cg_start(const double* r, const double* inv, double* z, double* p, int64_t n, double* partials,
+// p = z = M r; rz = r.z
+__global__ void k_cg_start(const double* r, const double* inv, double* p, int64_t n, double* partials,
                            unsigned int* counter, CgDev* st) {
   double s = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double zi = inv ? r[i] * inv[i] : r[i];
-    z[i] = zi;
     p[i] = zi;
     s += r[i] * zi;
   }
@@ -66,28 +65,29 @@ __global__ void k_cg_pap(const double* p, const double* ap, int64_t n, double* p
     s += p[i] * ap[i];
   double v[1] = {s};
   if (grid_reduce<1>(v, partials, counter))
-    if (threadIdx.x == 0) {
-      st->pap = v[0];
-      if (!(v[0] > 0.0)) {
-        st->fail = 1;
-        st->done = 1;
-      } else {
-        st->alpha = st->rz / v[0];
-      }
-    }
+    if (threadIdx.x == 0) st->pap = v[0];
 }
 
-__global__ void k_cg_update(double* x, const double* p, double* r, const double* ap, const double* inv, double* z,
-                            int64_t n, double* partials, unsigned int* counter, CgDev* st, double* hist) {
+// x += alpha p; r -= alpha Ap; (r.r, r.z) with z = M r formed on the fly (never stored). alpha =
+// rz / pAp, where pAp was produced by k_cg_pap or fused into the operator apply.
+__global__ void k_cg_update(double* x, const double* p, double* r, const double* ap, const double* inv, int64_t n,
+                            double* partials, unsigned int* counter, CgDev* st, double* hist) {
   if (st->done) return;
-  const double a = st->alpha;
+  const double pap = st->pap;
+  if (!(pap > 0.0)) {  // krylov.hpp:377-381
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->fail = 1;
+      st->done = 1;
+    }
+    return;
+  }
+  const double a = st->rz / pap;
   double rr = 0.0, rz = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     x[i] += a * p[i];
     const double ri = r[i] - a * ap[i];
     r[i] = ri;
     const double zi = inv ? ri * inv[i] : ri;
-    z[i] = zi;
     rr += ri * ri;
     rz += ri * zi;
   }
@@ -109,11 +109,13 @@ __global__ void k_cg_update(double* x, const double* p, double* r, const double*
     }
 }
 
-__global__ void k_cg_p(const double* z, double* p, int64_t n, const CgDev* st) {
+// p = M r + beta p
+__global__ void k_cg_p(const double* __restrict__ r, const double* __restrict__ inv, double* __restrict__ p, int64_t n,
+                       const CgDev* st) {
   if (st->done) return;
   const double b = st->beta;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = z[i] + b * p[i];
+    p[i] = (inv ? r[i] * inv[i] : r[i]) + b * p[i];
 }
 
 __global__ void k_inv_diag(const double* d, double* inv, int64_t n, unsigned long long* first_zero) {
@@ -173,7 +175,7 @@ void jacobi_inverse(Operator& op, DevArray<double>& inv) {
 void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const double* inv, SolveReport& rep) {
   Ctx& c = *op.sys->ctx;
   const int64_t n = op.n;
-  DevArray<double> r(n), z(n), p(n), ap(n), scratch(n), hist(cfg.max_iter + 2);
+  DevArray<double> r(n), p(n), ap(n), scratch(n), hist(cfg.max_iter + 2);
   DevArray<CgDev> st(1);
   const double bnorm = std::sqrt(dot(c, b, b, n));
   const double denom = bnorm > 0.0 ? bnorm : 1.0;
@@ -188,15 +190,19 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
   const unsigned rg = red_grid(n), eg = grid_for(n, 256, 148 * 16);
   while (true) {
     if (rep.history.back() > cfg.rtol && rep.iterations < cfg.max_iter) {
-      launch(c, k_cg_start, rg, kRedThreads, 0, r.p, inv, z.p, p.p, n, c.red_partials.p, c.red_counter.p, st.p);
+      launch(c, k_cg_start, rg, kRedThreads, 0, r.p, inv, p.p, n, c.red_partials.p, c.red_counter.p, st.p);
       int chunk = 4;
       while (true) {
         for (int k = 0; k < chunk; ++k) {
-          op.apply(p.p, ap.p);
-          launch(c, k_cg_pap, rg, kRedThreads, 0, p.p, ap.p, n, c.red_partials.p, c.red_counter.p, st.p);
-          launch(c, k_cg_update, rg, kRedThreads, 0, x, p.p, r.p, ap.p, inv, z.p, n, c.red_partials.p,
-                 c.red_counter.p, st.p, hist.p);
-          launch(c, k_cg_p, eg, 256, 0, z.p, p.p, n, st.p);
+          // fused operators write p^T A p straight into st->pap; others get the reduction kernel
+          double* pap_dev = reinterpret_cast<double*>(reinterpret_cast<char*>(st.p) + offsetof(CgDev, pap));
+          if (!op.apply_dot(p.p, ap.p, pap_dev)) {
+            op.apply(p.p, ap.p);
+            launch(c, k_cg_pap, rg, kRedThreads, 0, p.p, ap.p, n, c.red_partials.p, c.red_counter.p, st.p);
+          }
+          launch(c, k_cg_update, rg, kRedThreads, 0, x, p.p, r.p, ap.p, inv, n, c.red_partials.p, c.red_counter.p,
+                 st.p, hist.p);
+          launch(c, k_cg_p, eg, 256, 0, r.p, inv, p.p, n, st.p);
         }
         hs = fetch(c, st.p);
         if (hs.done) break;

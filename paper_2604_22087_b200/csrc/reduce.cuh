@@ -57,4 +57,33 @@ __device__ __forceinline__ bool grid_reduce(double (&v)[NV], double* partials, u
   return true;
 }
 
+// Cross-kernel fixed-order reduction: every block of a kernel stores its block sum in
+// mine[bid]; the last block to finish (ticket) adds prior[0..nprior) then mine[0..nmine) in index
+// order and writes out[0]. Deterministic for fixed launch shapes.
+__device__ __forceinline__ void block_to_slot_and_finish(double v, double* mine, int bid, int nmine,
+                                                         const double* prior, int nprior, unsigned int* counter,
+                                                         double* out) {
+  __shared__ bool last;
+  double a[1] = {v};
+  block_reduce<1>(a);
+  if (threadIdx.x == 0) {
+    mine[bid] = a[0];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == static_cast<unsigned>(nmine - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double s = 0.0;
+  // fixed assignment of partials to threads, then a fixed-shape block reduction
+  for (int b = threadIdx.x; b < nprior; b += blockDim.x) s += __ldcg(&prior[b]);
+  for (int b = threadIdx.x; b < nmine; b += blockDim.x) s += __ldcg(&mine[b]);
+  a[0] = s;
+  block_reduce<1>(a);
+  if (threadIdx.x == 0) {
+    out[0] = a[0];
+    *counter = 0u;
+  }
+}
+
 }  // namespace afem

@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "afem_impl.hpp"
+#include "reduce.cuh"
 
 namespace afem {
 
@@ -57,6 +58,10 @@ struct StencilPlan {
   // correction items (k_stencil_items): mixed-family nodes and the edge columns
   DevArray<int32_t> it_node;
   DevArray<uint8_t> it_oct, it_seg, it_mode;
+  DevArray<uint32_t> it_zmask;
+  DevArray<double> part_main, part_items;  // fused p.Ap partials (main kernel, item kernel)
+  DevArray<unsigned int> counter;
+  int item_blocks = 1;
   DevArray<double> it_dE;
   DevArray<double> Kg;   // Khat (row-major 24 x 24) in global memory for the item kernel
   int64_t n_items = 0;   // padded to a multiple of 32
@@ -180,12 +185,25 @@ __device__ __forceinline__ void plane_dispatch(const StencilParams& P, const dou
 }
 
 // OCC: resident CTAs per SM the register budget is sized for (2: 128 regs, 3: 80 regs).
-template <int OCC>
+// DOT: also accumulate x.y (the CG p^T A p) into per-block partials; when `finish`, the last block
+// completes the fixed-order reduction into dot_out (otherwise k_stencil_items does).
+struct DotArgs {
+  double* part_main;
+  double* part_items;
+  unsigned int* counter;
+  double* out;
+  int finish;
+  int n_main;  // number of main-kernel partials (read by the items kernel's last block)
+};
+
+template <int OCC, bool DOT>
 __global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant__ StencilParams P,
                                                         const double* __restrict__ x,
                                                         const uint8_t* __restrict__ info, double* __restrict__ y,
-                                                        int kchunk) {
+                                                        int kchunk, DotArgs dot) {
+  double dsum = 0.0;
   __shared__ __align__(16) double sm[2][TY + 2][RS];
+  __shared__ uint32_t sinfo[2][NT][4];
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int NX = P.NX, NY = P.NY, NZ = P.NZ;
   const int i0 = blockIdx.x * TXN, j0 = blockIdx.y * TY;
@@ -213,44 +231,54 @@ __global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant_
     col = c3;
     return q3 < 2 * (TXN + 2);
   };
-  uint32_t pm = 0;
+  // The info byte of each slot's node travels the same way: the 4-byte word holding it is copied
+  // into this thread's private shared words (sinfo), so no load result is consumed before the
+  // wait; the byte's position is kept in a 2-bit field per slot (sel), 0xff marks "no node".
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(&sm[0][0][0]));
+  const uint32_t ibase = static_cast<uint32_t>(__cvta_generic_to_shared(&sinfo[0][threadIdx.x][0]));
+  uint32_t sel = 0;
   auto fetch = [&](int p, int buf) {
     const bool inplane = p >= 0 && p < NZ;
     const int64_t pb = plane * (inplane ? p : 0);
-    pm = 0;
+    sel = 0;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       int r, col;
-      if (!slot(s, r, col)) continue;
+      const bool used = slot(s, r, col);
       const int ii = i0 - 1 + col, jj = j0 - 1 + r;
-      const bool ok = inplane && ii >= 0 && ii < NX && jj >= 0 && jj < NY;
+      const bool ok = used && inplane && ii >= 0 && ii < NX && jj >= 0 && jj < NY;
       const int64_t node = ok ? pb + ii + (int64_t)NX * jj : 0;
-      const uint32_t dst = sbase + 8u * static_cast<uint32_t>(buf * (TY + 2) * RS + r * RS + 3 * col);
-      const double* src = x + 3 * node;
-      const int sz = ok ? 8 : 0;
+      if (used) {
+        const uint32_t dst = sbase + 8u * static_cast<uint32_t>(buf * (TY + 2) * RS + r * RS + 3 * col);
+        const double* src = x + 3 * node;
+        const int sz = ok ? 8 : 0;
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst + 8u * c), "l"(src + c), "r"(sz)
-                     : "memory");
-      if (ok) pm |= static_cast<uint32_t>(__ldg(&info[node]) & 7) << (8 * s);
+        for (int c = 0; c < 3; ++c)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst + 8u * c), "l"(src + c), "r"(sz)
+                       : "memory");
+      }
+      const uint32_t idst = ibase + 4u * static_cast<uint32_t>(buf * NT * 4 + s);
+      const uint8_t* isrc = info + (node & ~int64_t(3));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(idst), "l"(isrc), "r"(ok ? 4 : 0)
+                   : "memory");
+      sel |= (ok ? static_cast<uint32_t>(node & 3) : 4u) << (4 * s);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
   auto land = [&](int buf) {  // wait for own copies, apply own masks
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    if (pm) {
-      double* sb = &sm[buf][0][0];
+    double* sb = &sm[buf][0][0];
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const uint32_t m = (pm >> (8 * s)) & 7;
-        if (!m) continue;
-        int r, col;
-        slot(s, r, col);
+    for (int s = 0; s < 4; ++s) {
+      const uint32_t b = (sel >> (4 * s)) & 7;
+      if (b >= 4) continue;
+      const uint32_t m = (sinfo[buf][threadIdx.x][s] >> (8 * b)) & 7;
+      if (!m) continue;
+      int r, col;
+      slot(s, r, col);
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if ((m >> c) & 1) sb[r * RS + 3 * col + c] = 0.0;
-      }
+      for (int c = 0; c < 3; ++c)
+        if ((m >> c) & 1) sb[r * RS + 3 * col + c] = 0.0;
     }
   };
 
@@ -269,6 +297,11 @@ __global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant_
     if (p < k1) fetch(p + 1, buf ^ 1);
     const int64_t onode = i + (int64_t)NX * (active ? j : 0) + plane * max(p - 1, 0);
     const uint8_t oi0 = __ldg(&info[onode]), oi1 = __ldg(&info[onode + 1]);
+    double xo[6];  // the finishing nodes' raw inputs (Dirichlet rows; the fused dot), issued early
+    if constexpr (DOT) {
+#pragma unroll
+      for (int a = 0; a < 6; ++a) xo[a] = __ldg(&x[3 * onode + a]);
+    }
     if (active && p >= 0 && p < NZ) {
       const int zc = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
       const double* s = &sm[buf][0][0];
@@ -281,8 +314,17 @@ __global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant_
       double* yo = y + 3 * onode;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        yo[a] = ((oi0 >> a) & 1) ? __ldg(&x[3 * onode + a]) : E0 * acc[0][0][a];
-        yo[3 + a] = ((oi1 >> a) & 1) ? __ldg(&x[3 * onode + 3 + a]) : E1 * acc[1][0][a];
+        if constexpr (DOT) {
+          const double y0 = ((oi0 >> a) & 1) ? xo[a] : E0 * acc[0][0][a];
+          const double y1 = ((oi1 >> a) & 1) ? xo[3 + a] : E1 * acc[1][0][a];
+          yo[a] = y0;
+          yo[3 + a] = y1;
+          dsum = fma(xo[a], y0, dsum);
+          dsum = fma(xo[3 + a], y1, dsum);
+        } else {
+          yo[a] = ((oi0 >> a) & 1) ? __ldg(&x[3 * onode + a]) : E0 * acc[0][0][a];
+          yo[3 + a] = ((oi1 >> a) & 1) ? __ldg(&x[3 * onode + 3 + a]) : E1 * acc[1][0][a];
+        }
       }
     }
 #pragma unroll
@@ -295,6 +337,17 @@ __global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant_
       }
     if (p < k1) land(buf ^ 1);
     __syncthreads();
+  }
+  if constexpr (DOT) {
+    const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int nb = gridDim.x * gridDim.y * gridDim.z;
+    if (dot.finish) {
+      block_to_slot_and_finish(dsum, dot.part_main, bid, nb, nullptr, 0, dot.counter, dot.out);
+    } else {
+      double a[1] = {dsum};
+      block_reduce<1>(a);
+      if (threadIdx.x == 0) dot.part_main[bid] = a[0];
+    }
   }
 }
 
@@ -319,15 +372,18 @@ struct Items {
   const uint8_t* oct;    // octant
   const uint8_t* seg;    // head: number of items of the node (1..8); 0: not a head
   const uint8_t* mode;   // head: 1 = edge node (write), 0 = add
+  const uint32_t* zmask; // bit 3m+b: input b of element node m is zero (Dirichlet or outside)
   const double* dE;
   int64_t n;             // padded count (multiple of 32)
 };
 
+template <bool DOT>
 __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, int NZ,
                                                                  const double* __restrict__ Kg,
                                                                  const double* __restrict__ x,
                                                                  const uint8_t* __restrict__ info, Items it,
-                                                                 double* __restrict__ y) {
+                                                                 double* __restrict__ y, DotArgs dot) {
+  double dsum = 0.0;
   __shared__ double Ks[24][3][8];
   for (int t = threadIdx.x; t < 576; t += blockDim.x) {  // coalesced global read of Khat (row-major)
     const int r = t / 24, q = t % 24;                    // Ks[q][a][ln] = Khat[3 ln + a][q]
@@ -349,17 +405,17 @@ __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, 
       const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
       const int ei = i - 1 + ox, ej = j - 1 + oy, ek = k - 1 + oz;
       const int ln = local_node(1 - ox, 1 - oy, 1 - oz);
+      const uint32_t zm = it.zmask[t];
       double xv[24];
 #pragma unroll
       for (int m = 0; m < 8; ++m) {  // 24 independent loads in flight
         const int ii = ei + corner_x(m), jj = ej + corner_y(m), kk = ek + (m >> 2);
         const bool in = ii >= 0 && ii < NX && jj >= 0 && jj < NY && kk >= 0 && kk < NZ;
         const int64_t nd = in ? ii + (int64_t)NX * (jj + (int64_t)NY * kk) : 0;
-        const uint8_t inf = in ? __ldg(&info[nd]) : 0x7;
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
           const double v = __ldg(&x[3 * nd + b]);
-          xv[3 * m + b] = ((inf >> b) & 1) ? 0.0 : v;
+          xv[3 * m + b] = ((zm >> (3 * m + b)) & 1) ? 0.0 : v;
         }
       }
       const double dE = it.dE[t];
@@ -387,16 +443,28 @@ __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, 
       (void)lane;
       const uint8_t inf = __ldg(&info[node]);
       double* yo = y + 3 * (int64_t)node;
+      const double* xn = x + 3 * (int64_t)node;
       if (it.mode[t]) {
 #pragma unroll
-        for (int a = 0; a < 3; ++a) yo[a] = ((inf >> a) & 1) ? x[3 * (int64_t)node + a] : r[a];
+        for (int a = 0; a < 3; ++a) {
+          const double xa = xn[a];
+          const double ya = ((inf >> a) & 1) ? xa : r[a];
+          yo[a] = ya;
+          if constexpr (DOT) dsum = fma(xa, ya, dsum);
+        }
       } else {
 #pragma unroll
         for (int a = 0; a < 3; ++a)
-          if (!((inf >> a) & 1)) yo[a] += r[a];
+          if (!((inf >> a) & 1)) {
+            yo[a] += r[a];
+            if constexpr (DOT) dsum = fma(xn[a], r[a], dsum);
+          }
       }
     }
   }
+  if constexpr (DOT)
+    block_to_slot_and_finish(dsum, dot.part_items, blockIdx.x, gridDim.x, dot.part_main, dot.n_main, dot.counter,
+                             dot.out);
 }
 
 // Per node: info byte (Dirichlet bits | base phase << 3) and, for nodes of the main kernel whose
@@ -601,7 +669,8 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
     }
 
   const int64_t nn = s.n_nodes;
-  plan->info.alloc(nn);
+  plan->info.alloc(nn + 4);  // +4: the main kernel copies the aligned 4-byte word holding a node's byte
+  AFEM_CK(cudaMemsetAsync(plan->info.p, 0, nn + 4, c.stream));
   DevArray<uint64_t> keys(nn);
   DevArray<unsigned long long> cnt(1);
   AFEM_CK(cudaMemsetAsync(cnt.p, 0, 8, c.stream));
@@ -645,30 +714,44 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
     std::sort(list.begin(), list.end(), [](const NodeMask& a, const NodeMask& b) { return a.node < b.node; });
     std::vector<int32_t> inode;
     std::vector<uint8_t> ioct, iseg, imode;
+    std::vector<uint32_t> izm;
     std::vector<double> idE;
+    auto pad = [&] {
+      inode.push_back(-1); ioct.push_back(0); iseg.push_back(0); imode.push_back(0); izm.push_back(0);
+      idE.push_back(0.0);
+    };
     for (const NodeMask& nm : list) {
       const int L = __builtin_popcount(nm.mask);
       if (L == 0) continue;
       if ((inode.size() % 32) + L > 32)
-        while (inode.size() % 32) {  // pad to the warp boundary
-          inode.push_back(-1); ioct.push_back(0); iseg.push_back(0); imode.push_back(0); idE.push_back(0.0);
-        }
+        while (inode.size() % 32) pad();  // a node's items never cross a warp
       const double Eb = nm.edge ? 0.0 : P.E[hinfo[nm.node] >> 3];
+      const int ni = static_cast<int>(nm.node % P.NX);
+      const int64_t nr = nm.node / P.NX;
+      const int nj = static_cast<int>(nr % P.NY), nk = static_cast<int>(nr / P.NY);
       bool head = true;
       for (int o = 0; o < 8; ++o) {
         if (!((nm.mask >> o) & 1)) continue;
+        // zero-input mask of the octant element's 8 nodes (outside the domain, or Dirichlet)
+        uint32_t zm = 0;
+        const int ei = ni - 1 + (o & 1), ej = nj - 1 + ((o >> 1) & 1), ek = nk - 1 + (o >> 2);
+        for (int m = 0; m < 8; ++m) {
+          const int ii = ei + corner_x(m), jj = ej + corner_y(m), kk = ek + (m >> 2);
+          const bool in = ii >= 0 && ii < P.NX && jj >= 0 && jj < P.NY && kk >= 0 && kk < P.NZ;
+          const uint32_t bits = in ? (hinfo[ii + (int64_t)P.NX * (jj + (int64_t)P.NY * kk)] & 7u) : 7u;
+          zm |= bits << (3 * m);
+        }
         inode.push_back(static_cast<int32_t>(nm.node));
         ioct.push_back(static_cast<uint8_t>(o));
         iseg.push_back(head ? static_cast<uint8_t>(L) : 0);
         imode.push_back(nm.edge ? 1 : 0);
+        izm.push_back(zm);
         idE.push_back(P.E[oct_phase(nm.node, o)] - Eb);
         head = false;
       }
       (nm.edge ? plan->n_edge_nodes : plan->n_fix_nodes) += 1;
     }
-    while (inode.size() % 32) {
-      inode.push_back(-1); ioct.push_back(0); iseg.push_back(0); imode.push_back(0); idE.push_back(0.0);
-    }
+    while (inode.size() % 32) pad();
     const size_t n = inode.size();
     plan->n_items = static_cast<int64_t>(n);
     if (n) {
@@ -676,44 +759,64 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
       plan->it_oct.alloc(n);
       plan->it_seg.alloc(n);
       plan->it_mode.alloc(n);
+      plan->it_zmask.alloc(n);
       plan->it_dE.alloc(n);
       AFEM_CK(cudaMemcpyAsync(plan->it_node.p, inode.data(), n * 4, cudaMemcpyHostToDevice, c.stream));
       AFEM_CK(cudaMemcpyAsync(plan->it_oct.p, ioct.data(), n, cudaMemcpyHostToDevice, c.stream));
       AFEM_CK(cudaMemcpyAsync(plan->it_seg.p, iseg.data(), n, cudaMemcpyHostToDevice, c.stream));
       AFEM_CK(cudaMemcpyAsync(plan->it_mode.p, imode.data(), n, cudaMemcpyHostToDevice, c.stream));
+      AFEM_CK(cudaMemcpyAsync(plan->it_zmask.p, izm.data(), n * 4, cudaMemcpyHostToDevice, c.stream));
       AFEM_CK(cudaMemcpyAsync(plan->it_dE.p, idE.data(), n * 8, cudaMemcpyHostToDevice, c.stream));
       AFEM_CK(cudaStreamSynchronize(c.stream));
     }
   }
   // variant (register budget) and z chunks: one full wave of resident CTAs when tiles allow it
   const char* env = std::getenv("AFEM_STENCIL_OCC");
-  plan->occ_variant = (env && std::atoi(env) == 2) ? 2 : 3;
+  plan->occ_variant = (env && std::atoi(env) == 3) ? 3 : 2;
   int occ = 1;
   if (plan->occ_variant == 2)
-    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<2>, NT, 0));
+    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<2, true>, NT, 0));
   else
-    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<3>, NT, 0));
+    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<3, true>, NT, 0));
   const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
   const int64_t tiles = (int64_t)(P.NXm / TXN) * ((P.NY + TY - 1) / TY);
   int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
   chunks = std::min(chunks, std::max(1, P.NZ / 8));
   plan->kchunk = (P.NZ + chunks - 1) / chunks;
   plan->nchunks = (P.NZ + plan->kchunk - 1) / plan->kchunk;
+  plan->item_blocks = static_cast<int>(grid_for(std::max<int64_t>(plan->n_items, 1), kItemThreads, 4 * c.num_sms));
+  const int64_t nb_main = (int64_t)(P.NXm / TXN) * ((P.NY + TY - 1) / TY) * plan->nchunks;
+  plan->part_main.alloc(std::max<int64_t>(nb_main, 1));
+  plan->part_items.alloc(plan->item_blocks);
+  plan->counter.alloc(1);
+  AFEM_CK(cudaMemsetAsync(plan->counter.p, 0, sizeof(unsigned), c.stream));
+  AFEM_CK(cudaStreamSynchronize(c.stream));
   return plan.release();
 }
 
-void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y) {
+void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, double* dot_out) {
   Ctx& c = *op.sys->ctx;
   const StencilParams& P = pl.p;
+  const dim3 grid(P.NXm / TXN, (P.NY + TY - 1) / TY, pl.nchunks);
+  const int nb_main = P.NXm > 0 ? static_cast<int>(grid.x * grid.y * grid.z) : 0;
+  const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main};
   if (P.NXm > 0) {
-    dim3 grid(P.NXm / TXN, (P.NY + TY - 1) / TY, pl.nchunks);
-    if (pl.occ_variant == 2) launch(c, k_stencil_main<2>, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk);
-    else launch(c, k_stencil_main<3>, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk);
+    if (dot_out) {
+      if (pl.occ_variant == 2) launch(c, k_stencil_main<2, true>, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk, dot);
+      else launch(c, k_stencil_main<3, true>, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk, dot);
+    } else {
+      if (pl.occ_variant == 2) launch(c, k_stencil_main<2, false>, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk, dot);
+      else launch(c, k_stencil_main<3, false>, grid, NT, 0, P, x, pl.info.p, y, pl.kchunk, dot);
+    }
   }
   if (pl.n_items > 0) {
-    const Items it{pl.it_node.p, pl.it_oct.p, pl.it_seg.p, pl.it_mode.p, pl.it_dE.p, pl.n_items};
-    launch(c, k_stencil_items, grid_for(pl.n_items, kItemThreads, 4 * c.num_sms), kItemThreads, 0, P.NX, P.NY, P.NZ,
-           pl.Kg.p, x, pl.info.p, it, y);
+    const Items it{pl.it_node.p, pl.it_oct.p, pl.it_seg.p, pl.it_mode.p, pl.it_zmask.p, pl.it_dE.p, pl.n_items};
+    if (dot_out)
+      launch(c, k_stencil_items<true>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, P.NZ, pl.Kg.p, x, pl.info.p, it,
+             y, dot);
+    else
+      launch(c, k_stencil_items<false>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, P.NZ, pl.Kg.p, x, pl.info.p,
+             it, y, dot);
   }
 }
 
