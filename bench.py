@@ -77,15 +77,16 @@ class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,utilization.gpu")
 
-    def __init__(self, device):
+    def __init__(self, device, period_ms=100):
         self.device = device
+        self.period_ms = period_ms
         self.proc = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", str(self.period_ms)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
 
@@ -235,22 +236,33 @@ def ours(args, rank, world, local_rank):
     t_apply = T / args.steps * 1e-3  # s per apply (max over ranks)
     value = world * n_dof * args.steps / (T * 1e-3)
 
-    # CG solve time (device-resident, Jacobi-PCG, rtol 1e-8): K du = -R(u0)
+    clk = clocks.stop()
+
+    # CG solve time (device-resident, Jacobi-PCG, rtol 1e-8): K du = -R(u0). Timed outside the
+    # nvidia-smi polling window (the poller contends for the driver lock the CG loop's per-chunk
+    # synchronisations need); clocks are sampled again at a 1 s period around it.
     cg = None
     if not args.no_cg:
         r0 = torch.from_numpy(sys_.constrain_residual(sys_.residual(u0), u0)).cuda()
         b = -r0
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        du, rep = afem.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        solve_s = e0.elapsed_time(e1) * 1e-3
+        cg_clk = ClockSampler(local_rank, period_ms=1000)
+        cg_clk.start()
+        best = None
+        for _ in range(2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            du, rep = afem.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            solve_s = e0.elapsed_time(e1) * 1e-3
+            if best is None or solve_s < best[0]:
+                best = (solve_s, rep)
+        solve_s, rep = best
         cg = {"solve_s": solve_s, "iterations": rep["iterations"], "converged": rep["converged"],
               "true_rel_residual": float(rep["residual_history"][-1]), "rtol": 1e-8, "precond": "jacobi",
-              "ms_per_iteration": 1e3 * solve_s / max(rep["iterations"], 1)}
-    clk = clocks.stop()
+              "ms_per_iteration": 1e3 * solve_s / max(rep["iterations"], 1), "best_of": 2,
+              "clocks": cg_clk.stop()}
 
     # end to end through the C ABI with pinned host buffers
     xh = x.cpu().pin_memory()

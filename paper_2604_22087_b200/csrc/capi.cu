@@ -46,7 +46,8 @@ void MfOp::apply(const double* x, double* y) {
   else mf_apply_general(*sys, state.p, mask.p, x, y);
 }
 bool MfOp::apply_dot(const double* x, double* y, double* dot_out) {
-  if (!stencil) return false;
+  static const bool disabled = std::getenv("AFEM_NO_FUSED_DOT") != nullptr;
+  if (!stencil || disabled) return false;
   stencil_apply(*stencil, *this, x, y, dot_out);
   return true;
 }

@@ -48,7 +48,10 @@ def test_stencil_matches_oracle(afem, ctx, n):
     assert rel_err(op.diagonal(), o.mf_diagonal(u)) <= TOL
 
 
-@pytest.mark.parametrize("shape", [(33, 17, 20), (40, 9, 31), (64, 64, 7), (31, 31, 31)])
+# NX = nx+1 nodes: >= 65 runs the 64-wide main kernel; NX mod 64 == 1 fuses the edge column into it,
+# other remainders exercise the separate edge-item kernel; NX < 65 is edge-only.
+@pytest.mark.parametrize("shape", [(64, 17, 20), (70, 9, 31), (64, 64, 7), (127, 12, 10), (128, 9, 17),
+                                   (33, 17, 20), (31, 31, 31)])
 def test_stencil_matches_general_kernel(afem, ctx, shape):
     nx, ny, nz = shape
     s = grid(afem, ctx, nx, ny=ny, nz=nz, n_fibres=10, radius=0.1, seed=7)
@@ -70,13 +73,35 @@ def test_stencil_matches_general_kernel(afem, ctx, shape):
         assert rel_err(ops.apply(x), opg.apply(x)) <= TOL
 
 
+def test_stencil_cg_matches_general_kernel_cg(afem, ctx):
+    """The fused p^T A p path (stencil operator) against the unfused general operator, same mesh."""
+    s = grid(afem, ctx, 64, ny=14, nz=12, n_fibres=8, radius=0.15, seed=5)
+    s.set_benchmark_dirichlet(0.01)
+    coords, conn, phase = s.mesh()
+    g = afem.System(ctx, 3, coords, conn, phase, LINEAR)
+    node, comp, val = Oracle("restate").bcs(3, 64, 14, 12, 1.0, 0.01)
+    g.set_dirichlet(node, comp, val)
+    u = s.impose_dirichlet(np.zeros(s.n))
+    b = -s.constrain_residual(s.residual(u), u)
+    ops, opg = afem.matrix_free_operator(s, u), afem.matrix_free_operator(g, u)
+    assert ops.uses_stencil and not opg.uses_stencil
+    xs, rs = afem.run_solver(ops, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
+    xg, rg = afem.run_solver(opg, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
+    assert rs["converged"] and rg["converged"]
+    assert abs(rs["iterations"] - rg["iterations"]) <= 2
+    assert rel_err(xs, xg) <= 1e-8
+    # repeated solves are bitwise identical (deterministic fused reductions)
+    xs2, _ = afem.run_solver(ops, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
+    assert xs.tobytes() == xs2.tobytes()
+
+
 def test_stencil_high_contrast_and_multiphase(afem, ctx):
     mats = [(afem.LINEAR, 1.0, 0.25), (afem.LINEAR, 1000.0, 0.25)]
-    s = grid(afem, ctx, 20, mats=mats, n_fibres=12, radius=0.15, seed=99)
+    s = grid(afem, ctx, 64, ny=20, nz=20, mats=mats, n_fibres=12, radius=0.15, seed=99)
     s.set_benchmark_dirichlet(0.01)
     coords, conn, phase = s.mesh()
     g = afem.System(ctx, 3, coords, conn, phase, mats)
-    g.set_dirichlet(*Oracle("restate").bcs(3, 20, 20, 20, 1.0, 0.01))
+    g.set_dirichlet(*Oracle("restate").bcs(3, 64, 20, 20, 1.0, 0.01))
     u = np.zeros(s.n)
     ops = afem.matrix_free_operator(s, u)
     opg = afem.matrix_free_operator(g, u)
