@@ -609,7 +609,7 @@ __global__ void k_stencil_classify(int NX, int NY, int NZ, int NXm, const uint8_
     }
     int best = kVoid, bestc = 0;
     for (int o = 0; o < 8; ++o) {
-      if (!fam[o]) continue;
+      if (!fam[o] || ph[o] == kVoid) continue;  // base: most frequent existing phase (E_base > 0)
       int c = 0;
       for (int q = 0; q < 8; ++q) c += fam[q] && ph[q] == ph[o];
       if (c > bestc || (c == bestc && ph[o] < best)) {
