@@ -331,10 +331,35 @@ __global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant_
   fetch(k0 - 1, 0);
   land(0);
   __syncthreads();
+  // Item metadata of the layer processed at step p is prefetched one step earlier (bounds and the
+  // first batch's word/coef), so its load latency hides behind a plane of stencil work.
+  const int lo_p = max(k0, 1), hi_p = min(k1, NZ - 1);
+  auto item_prefetch = [&](int p, int& b0, int& b1, uint32_t& w, double& cf) {
+    b0 = b1 = 0;
+    w = 3u << 11;
+    cf = 0.0;
+    if (active && p >= lo_p && p <= hi_p) {
+      const int lid = (blockIdx.x * NY + j) * (NZ - 1) + (p - 1);
+      b0 = __ldg(&cr.ptr[lid]);
+      b1 = __ldg(&cr.ptr[lid + 1]);
+      if (b0 + lane < b1) {
+        w = __ldg(&cr.word[b0 + lane]);
+        cf = __ldg(&cr.coef[b0 + lane]);
+      }
+    }
+  };
+  int nb0, nb1;
+  uint32_t nw;
+  double ncf;
+  item_prefetch(k0 - 1, nb0, nb1, nw, ncf);
   int cur = 0;  // ring slot of plane p
   for (int p = k0 - 1; p <= k1; ++p) {
     const int nxt = cur == RING - 1 ? 0 : cur + 1, prv = cur == 0 ? RING - 1 : cur - 1;
     if (p < k1) fetch(p + 1, nxt);
+    const int b0 = nb0, b1 = nb1;
+    const uint32_t w0 = nw;
+    const double cf0 = ncf;
+    item_prefetch(p + 1, nb0, nb1, nw, ncf);
     const int64_t onode = i + (int64_t)NX * (active ? j : 0) + plane * max(p - 1, 0);
     const uint8_t oi0 = __ldg(&info[onode]), oi1 = __ldg(&info[onode + 1]);
     double xo[6];  // the finishing nodes' raw inputs (Dirichlet rows; the fused dot), issued early
@@ -350,15 +375,14 @@ __global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant_
       else plane_dispatch<2>(P, s, tx, ty, zc, acc);
     }
     // ---- correction items of the element layer (p-1, p): both planes are resident
-    if (active && p >= max(k0, 1) && p <= min(k1, NZ - 1)) {
-      const int lid = (blockIdx.x * NY + j) * (NZ - 1) + (p - 1);
-      const int b0 = __ldg(&cr.ptr[lid]), b1 = __ldg(&cr.ptr[lid + 1]);
+    if (active && p >= lo_p && p <= hi_p) {
       if (b1 > b0) {  // warp-uniform
         const double* slo = &sm[prv][0][0];
         const double* shi = &sm[cur][0][0];
         for (int base = b0; base < b1; base += 32) {
           const int t = base + lane;
-          const uint32_t w = t < b1 ? __ldg(&cr.word[t]) : (3u << 11);
+          const bool first = base == b0;
+          const uint32_t w = first ? w0 : (t < b1 ? __ldg(&cr.word[t]) : (3u << 11));
           const int tcol = w & 127, flag = (w >> 7) & 1, o = (w >> 8) & 7, mode = (w >> 11) & 3, L = w >> 13;
           // chunk ends: lower-plane targets below k0 and upper-plane targets at k1 belong to neighbours
           const bool skip = mode == 3 || (flag == 0 && p - 1 < k0) || (flag == 1 && p >= k1);
@@ -377,7 +401,7 @@ __global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant_
                 r2 = fma(Ks[3 * m + b][2][ln], xv, r2);
               }
             }
-            const double cf = __ldg(&cr.coef[t]);
+            const double cf = first ? cf0 : __ldg(&cr.coef[t]);
             r0 *= cf;
             r1 *= cf;
             r2 *= cf;
