@@ -65,6 +65,7 @@ struct StencilPlan {
   DevArray<double> c_coef;
   int64_t n_citems = 0;
   int edge_fused = 0;
+  int fuse_items = 0;
   DevArray<double> part_main, part_items;  // fused p.Ap partials (main kernel, item kernel)
   DevArray<unsigned int> counter;
   int item_blocks = 1;
@@ -74,7 +75,6 @@ struct StencilPlan {
   int64_t n_fix_nodes = 0, n_edge_nodes = 0;
   int kchunk = 16;
   int nchunks = 1;
-  int occ_variant = 3;
 };
 
 namespace {
@@ -227,8 +227,9 @@ constexpr size_t kMainSmem = sizeof(double) * (RING * (TY + 2) * RS + TY * 2 * T
                              sizeof(uint32_t) * RING * NT * 4;
 
 // OCC: resident CTAs per SM the register budget is sized for (2: 128 regs, 3: 80 regs).
-template <int OCC, bool DOT>
-__global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant__ StencilParams P,
+// CORR: the in-tile correction phase (opt-in, AFEM_STENCIL_FUSE_ITEMS=1).
+template <bool DOT, bool CORR>
+__global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ StencilParams P,
                                                         const double* __restrict__ x,
                                                         const uint8_t* __restrict__ info, double* __restrict__ y,
                                                         int kchunk, DotArgs dot, CorrArgs cr) {
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant_
     b0 = b1 = 0;
     w = 3u << 11;
     cf = 0.0;
-    if (active && p >= lo_p && p <= hi_p) {
+    if (CORR && active && p >= lo_p && p <= hi_p) {
       const int lid = (blockIdx.x * NY + j) * (NZ - 1) + (p - 1);
       b0 = __ldg(&cr.ptr[lid]);
       b1 = __ldg(&cr.ptr[lid + 1]);
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(NT, OCC) k_stencil_main(const __grid_constant_
       else plane_dispatch<2>(P, s, tx, ty, zc, acc);
     }
     // ---- correction items of the element layer (p-1, p): both planes are resident
-    if (active && p >= lo_p && p <= hi_p) {
+    if (CORR && active && p >= lo_p && p <= hi_p) {
       if (b1 > b0) {  // warp-uniform
         const double* slo = &sm[prv][0][0];
         const double* shi = &sm[cur][0][0];
@@ -858,13 +859,18 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
     // is the single column i = NXm, the last tile's right halo) every octant of the edge nodes.
     // One segment per (target, element layer); CSR over (x tile, row, layer); padded so no segment
     // crosses a 32-item batch of its list.
-    plan->edge_fused = (P.NX - P.NXm == 1 && P.NXm > 0) ? 1 : 0;
+    // Default: corrections run in k_stencil_items (measured faster: ~7 items per warp-step leave
+    // the in-tile batches mostly idle). AFEM_STENCIL_FUSE_ITEMS=1 selects the in-tile variant.
+    const char* fenv = std::getenv("AFEM_STENCIL_FUSE_ITEMS");
+    plan->fuse_items = (fenv && fenv[0] == '1') ? 1 : 0;
+    plan->edge_fused = (plan->fuse_items && P.NX - P.NXm == 1 && P.NXm > 0) ? 1 : 0;
     const int ntx = P.NXm / TXN;
     const int64_t nlist = (int64_t)std::max(ntx, 1) * P.NY * std::max(P.NZ - 1, 1);
     struct CItem { int64_t lid; uint32_t key; uint32_t word; double coef; };  // key orders (flag, tcol, o)
     std::vector<CItem> ci;
     bool base_ok = true;
     for (const NodeMask& nm : list) {
+      if (!plan->fuse_items) break;
       if (nm.edge && !plan->edge_fused) continue;
       const int ni = static_cast<int>(nm.node % P.NX);
       const int64_t nr = nm.node / P.NX;
@@ -937,7 +943,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
       idE.push_back(0.0);
     };
     for (const NodeMask& nm : list) {
-      if (!nm.edge || plan->edge_fused) continue;
+      if (plan->fuse_items ? (!nm.edge || plan->edge_fused) : false) continue;
       const int L = __builtin_popcount(nm.mask);
       if (L == 0) continue;
       if ((inode.size() % 32) + L > 32)
@@ -986,22 +992,17 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
       AFEM_CK(cudaStreamSynchronize(c.stream));
     }
   }
-  // variant (register budget) and z chunks: one full wave of resident CTAs when tiles allow it
-  const char* env = std::getenv("AFEM_STENCIL_OCC");
-  plan->occ_variant = (env && std::atoi(env) == 3) ? 3 : 2;
+  // z chunks: one full wave of resident CTAs when tiles allow it
   static bool attrs = false;
   if (!attrs) {
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
     attrs = true;
   }
   int occ = 1;
-  if (plan->occ_variant == 2)
-    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<2, true>, NT, kMainSmem));
-  else
-    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<3, true>, NT, kMainSmem));
+  AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<true, false>, NT, kMainSmem));
   const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
   const int64_t tiles = (int64_t)(P.NXm / TXN) * ((P.NY + TY - 1) / TY);
   int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
@@ -1026,16 +1027,12 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, 
   const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main};
   const CorrArgs cr{pl.c_ptr.p, pl.c_word.p, pl.c_coef.p, pl.Kg.p, pl.edge_fused};
   if (P.NXm > 0) {
-    if (dot_out) {
-      if (pl.occ_variant == 2)
-        launch(c, k_stencil_main<2, true>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
-      else
-        launch(c, k_stencil_main<3, true>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
+    if (pl.fuse_items) {
+      if (dot_out) launch(c, k_stencil_main<true, true>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
+      else launch(c, k_stencil_main<false, true>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
     } else {
-      if (pl.occ_variant == 2)
-        launch(c, k_stencil_main<2, false>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
-      else
-        launch(c, k_stencil_main<3, false>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
+      if (dot_out) launch(c, k_stencil_main<true, false>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
+      else launch(c, k_stencil_main<false, false>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
     }
   }
   if (pl.n_items > 0) {

@@ -73,6 +73,21 @@ def test_stencil_matches_general_kernel(afem, ctx, shape):
         assert rel_err(ops.apply(x), opg.apply(x)) <= TOL
 
 
+@pytest.mark.parametrize("shape", [(64, 17, 20), (70, 9, 31)])
+def test_stencil_fused_corrections_variant(afem, ctx, shape, monkeypatch):
+    """The opt-in in-tile correction path (AFEM_STENCIL_FUSE_ITEMS=1) equals the default path."""
+    nx, ny, nz = shape
+    s = grid(afem, ctx, nx, ny=ny, nz=nz, n_fibres=10, radius=0.1, seed=7)
+    s.set_benchmark_dirichlet(0.02)
+    u = s.impose_dirichlet(np.zeros(s.n))
+    x = random_vector(s.n, 1.0, 77)
+    y_default = afem.matrix_free_operator(s, u).apply(x)
+    monkeypatch.setenv("AFEM_STENCIL_FUSE_ITEMS", "1")
+    op = afem.matrix_free_operator(s, u)
+    assert op.uses_stencil
+    assert rel_err(op.apply(x), y_default) <= TOL
+
+
 def test_stencil_cg_matches_general_kernel_cg(afem, ctx):
     """The fused p^T A p path (stencil operator) against the unfused general operator, same mesh."""
     s = grid(afem, ctx, 64, ny=14, nz=12, n_fibres=8, radius=0.15, seed=5)
