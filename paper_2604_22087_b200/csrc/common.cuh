@@ -87,7 +87,7 @@ struct Ctx {
   }
 };
 
-constexpr int kRedBlocks = 592;  // 4 x 148 SMs: partial-sum slots for the deterministic reductions
+constexpr int kRedBlocks = 1184;  // 8 x 148 SMs: partial-sum slots for the deterministic reductions
 constexpr int kRedThreads = 256;
 
 // Counted launch on the context stream. Every kernel the library issues goes through here so

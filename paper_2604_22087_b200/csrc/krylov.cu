@@ -83,7 +83,33 @@ __global__ void k_cg_update(double* x, const double* p, double* r, const double*
   }
   const double a = st->rz / pap;
   double rr = 0.0, rz = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  // 16-byte vector body (device allocations are 256-byte aligned) + scalar tail
+  const int64_t n2 = n / 2;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  const double2* ap2 = reinterpret_cast<const double2*>(ap);
+  const double2* inv2 = reinterpret_cast<const double2*>(inv);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 pv = __ldcs(&p2[i]), av = __ldcs(&ap2[i]);
+    double2 xv = __ldcs(&x2[i]), rv = __ldcs(&r2[i]);
+    xv.x += a * pv.x;
+    xv.y += a * pv.y;
+    rv.x -= a * av.x;
+    rv.y -= a * av.y;
+    __stcs(&x2[i], xv);
+    __stcs(&r2[i], rv);
+    double zx = rv.x, zy = rv.y;
+    if (inv) {
+      const double2 iv = __ldg(&inv2[i]);
+      zx *= iv.x;
+      zy *= iv.y;
+    }
+    rr += rv.x * rv.x + rv.y * rv.y;
+    rz += rv.x * zx + rv.y * zy;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
+    const int64_t i = n - 1;
     x[i] += a * p[i];
     const double ri = r[i] - a * ap[i];
     r[i] = ri;
@@ -114,8 +140,26 @@ __global__ void k_cg_p(const double* __restrict__ r, const double* __restrict__ 
                        const CgDev* st) {
   if (st->done) return;
   const double b = st->beta;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+  const int64_t n2 = n / 2;
+  const double2* r2 = reinterpret_cast<const double2*>(r);
+  const double2* inv2 = reinterpret_cast<const double2*>(inv);
+  double2* p2 = reinterpret_cast<double2*>(p);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 z = __ldg(&r2[i]);
+    if (inv) {
+      const double2 iv = __ldg(&inv2[i]);
+      z.x *= iv.x;
+      z.y *= iv.y;
+    }
+    double2 pv = p2[i];
+    pv.x = z.x + b * pv.x;
+    pv.y = z.y + b * pv.y;
+    p2[i] = pv;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
+    const int64_t i = n - 1;
     p[i] = (inv ? r[i] * inv[i] : r[i]) + b * p[i];
+  }
 }
 
 __global__ void k_inv_diag(const double* d, double* inv, int64_t n, unsigned long long* first_zero) {
@@ -345,10 +389,18 @@ void solve(Operator& op, const SolverCfg& cfg, const double* b, const double* x0
   Ctx& c = *op.sys->ctx;
   DevArray<double> inv;
   if (cfg.precond == 1) jacobi_inverse(op, inv);
-  if (x0) copy(c, x0, x, op.n);
-  else fill(c, 0.0, x, op.n);
-  if (cfg.method == 0) cg(op, cfg, b, x, inv.p, rep);
-  else gmres(op, cfg, b, x, inv.p, rep);
+  // the vector kernels use 16-byte accesses: iterate in an aligned buffer if the caller's is not
+  DevArray<double> xa;
+  double* xw = x;
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0) {
+    xa.alloc(op.n);
+    xw = xa.p;
+  }
+  if (x0) copy(c, x0, xw, op.n);
+  else fill(c, 0.0, xw, op.n);
+  if (cfg.method == 0) cg(op, cfg, b, xw, inv.p, rep);
+  else gmres(op, cfg, b, xw, inv.p, rep);
+  if (xw != x) copy(c, xw, x, op.n);
   AFEM_CK(cudaStreamSynchronize(c.stream));
   rep.wall_time = timer.seconds();
 }
