@@ -246,6 +246,36 @@ afem_status afem_load_stepping(afem_system sys, double total_strain, int32_t n_s
                                const afem_newton_cfg* cfg, double* u, int32_t* failed_step,
                                int32_t* converged, int32_t* step_iterations);
 
+/* ------------------------------------------------------------------ multi-GPU slab decomposition
+ * (the reference has no distribution — the paper distributes only the PETSc solve,
+ * PAPER.md:296-302). One process per GPU, each owning a contiguous z-slab of element layers; the
+ * node plane between slabs is shared and owned by the lower rank. The only data-path collectives
+ * are a one-plane exchange with each neighbour per operator apply and scalar allreduces for the
+ * Krylov dot products (NCCL over NVLink). A threads backend runs the same algorithm with several
+ * subdomains on one device (tests). */
+typedef struct afem_dist_s* afem_dist;
+typedef struct afem_thread_group_s* afem_thread_group;
+
+/* Element layers [z0, z1) of rank `rank` when nz layers are split over `size` ranks. Host only. */
+afem_status afem_slab_range(int32_t nz, int32_t size, int32_t rank, int32_t* z0, int32_t* z1);
+/* 128-byte NCCL unique id (rank 0 creates it, the host broadcasts it). */
+afem_status afem_nccl_unique_id(void* out128);
+afem_status afem_dist_create_nccl(afem_ctx ctx, const void* uid128, int32_t rank, int32_t size, afem_dist* out);
+afem_status afem_thread_group_create(int32_t size, afem_thread_group* out);
+afem_status afem_thread_group_destroy(afem_thread_group g);
+afem_status afem_dist_create_threads(afem_ctx ctx, afem_thread_group g, int32_t rank, afem_dist* out);
+afem_status afem_dist_destroy(afem_dist d);
+/* benchmark_bcs of the global grid restricted to this rank's slab system (the slab's local grid
+ * system from afem_system_create_grid with nz = z1 - z0 and lz scaled accordingly). */
+afem_status afem_dist_set_benchmark_dirichlet(afem_dist d, afem_system slab, double strain, double lx_global);
+/* matrix_free_operator over the distributed system (local operator + plane halo). */
+afem_status afem_dist_op_create_mf(afem_dist d, afem_system slab, const double* u, afem_op* out);
+/* run_solver, CG (+ Jacobi), every rank calling collectively; reports are identical on all ranks. */
+afem_status afem_dist_solve(afem_dist d, afem_op op, const afem_solver_cfg* cfg, const double* b, const double* x0,
+                            double* x, afem_solve_report* rep, double* history, int32_t hist_cap);
+/* Global dot over owned dofs (collective). */
+afem_status afem_dist_dot(afem_dist d, afem_op op, const double* a, const double* b, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -157,6 +157,17 @@ def load():
         "afem_solve": ([vp, vp, vp, vp, vp, vp, vp, i32], i32),
         "afem_solve_bvp": ([vp, vp, vp, vp, vp, vp, i32], i32),
         "afem_load_stepping": ([vp, f64, i32, vp, vp, vp, vp, vp], i32),
+        "afem_slab_range": ([i32, i32, i32, vp, vp], i32),
+        "afem_nccl_unique_id": ([vp], i32),
+        "afem_dist_create_nccl": ([vp, vp, i32, i32, vp], i32),
+        "afem_thread_group_create": ([i32, vp], i32),
+        "afem_thread_group_destroy": ([vp], i32),
+        "afem_dist_create_threads": ([vp, vp, i32, vp], i32),
+        "afem_dist_destroy": ([vp], i32),
+        "afem_dist_set_benchmark_dirichlet": ([vp, vp, f64, f64], i32),
+        "afem_dist_op_create_mf": ([vp, vp, vp, vp], i32),
+        "afem_dist_solve": ([vp, vp, vp, vp, vp, vp, vp, vp, i32], i32),
+        "afem_dist_dot": ([vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sigs.items():
         f = getattr(L, name)
@@ -554,3 +565,91 @@ def run_solver(op: LinearOperator, b, method=CG, precond=NONE, rtol=1e-13, max_i
     return x, dict(converged=bool(rep.converged), iterations=rep.iterations,
                    residual_history=hist[:min(rep.n_history, cap)].copy(), wall_time=rep.wall_time,
                    failure=rep.failure.decode())
+
+
+# ---------------------------------------------------------------------------- multi-GPU (slab)
+
+def slab_range(nz: int, size: int, rank: int):
+    """Element layers [z0, z1) of `rank` when nz layers are split over `size` ranks (host only)."""
+    L = load()
+    z0, z1 = C.c_int32(), C.c_int32()
+    _check(L.afem_slab_range(nz, size, rank, C.byref(z0), C.byref(z1)))
+    return z0.value, z1.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(load().afem_nccl_unique_id(buf))
+    return buf.raw
+
+
+class ThreadGroup:
+    """Several subdomains of one process on one device (the threads backend of the slab solver)."""
+
+    def __init__(self, size: int):
+        h = C.c_void_p()
+        _check(load().afem_thread_group_create(size, C.byref(h)))
+        self.h = h
+        self.size = size
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.afem_thread_group_destroy(self.h)
+            self.h = None
+
+
+class Dist:
+    """One rank of the z-slab decomposition: backend 'nccl' (one process per GPU; `uid` from
+    nccl_unique_id() on rank 0, broadcast by the host) or 'threads' (a ThreadGroup)."""
+
+    def __init__(self, ctx: Context, rank: int, size: int, backend: str = "nccl", uid: bytes = None,
+                 group: ThreadGroup = None):
+        L = load()
+        h = C.c_void_p()
+        if backend == "nccl":
+            buf = C.create_string_buffer(uid, 128)
+            _check(L.afem_dist_create_nccl(ctx.h, buf, rank, size, C.byref(h)))
+        else:
+            _check(L.afem_dist_create_threads(ctx.h, group.h, rank, C.byref(h)))
+        self.h, self.ctx, self.rank, self.size = h, ctx, rank, size
+        self._group = group
+
+    def set_benchmark_dirichlet(self, sys: System, strain: float, lx_global: float = 1.0):
+        _check(_lib.afem_dist_set_benchmark_dirichlet(self.h, sys.h, strain, lx_global))
+
+    def matrix_free_operator(self, sys: System, u) -> LinearOperator:
+        h = C.c_void_p()
+        _check(_lib.afem_dist_op_create_mf(self.h, sys.h, _ptr(_f64(u)), C.byref(h)))
+        return LinearOperator(h, sys, keep=self)
+
+    def run_solver(self, op: LinearOperator, b, method=CG, precond=JACOBI, rtol=1e-13, max_iter=10000, x0=None):
+        cfg = afem_solver_cfg(method, precond, rtol, max_iter, 30)
+        rep = afem_solve_report()
+        cap = max_iter + 2
+        hist = np.zeros(cap)
+        x = b.new_zeros(op.n) if hasattr(b, "data_ptr") else np.zeros(op.n)
+        x0 = None if x0 is None else _f64(x0)
+        _check(_lib.afem_dist_solve(self.h, op.h, C.byref(cfg), _ptr(_f64(b)), _ptr(x0), _ptr(x), C.byref(rep),
+                                    _ptr(hist), cap))
+        return x, dict(converged=bool(rep.converged), iterations=rep.iterations,
+                       residual_history=hist[:min(rep.n_history, cap)].copy(), wall_time=rep.wall_time,
+                       failure=rep.failure.decode())
+
+    def dot(self, op: LinearOperator, a, b) -> float:
+        out = C.c_double()
+        _check(_lib.afem_dist_dot(self.h, op.h, _ptr(_f64(a)), _ptr(_f64(b)), C.byref(out)))
+        return out.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.afem_dist_destroy(self.h)
+            self.h = None
+
+
+def slab_system(ctx: Context, nx: int, ny: int, nz_global: int, rank: int, size: int, lx=1.0, ly=1.0, lz=1.0,
+                inclusions=(), radius=0.0, materials=((LINEAR, 1.0, 0.3), (LINEAR, 10.0, 0.3))):
+    """The local grid system of one z-slab (fibres are parallel to z, so the slab's phase pattern is
+    the global one; the operator is translation invariant, so local z starts at 0)."""
+    z0, z1 = slab_range(nz_global, size, rank)
+    return System.grid(ctx, 3, nx, ny, z1 - z0, lx, ly, lz * (z1 - z0) / nz_global, inclusions, radius,
+                       materials), (z0, z1)

@@ -11,6 +11,7 @@
 
 #include "../../include/afem.h"
 #include "afem_impl.hpp"
+#include "dist.hpp"
 
 struct afem_ctx_s {
   afem::Ctx c;
@@ -26,6 +27,13 @@ struct afem_buffer_s {
 };
 struct afem_op_s {
   std::unique_ptr<afem::Operator> op;
+};
+struct afem_dist_s {
+  afem::Ctx* ctx = nullptr;
+  std::unique_ptr<afem::Comm> comm;
+};
+struct afem_thread_group_s {
+  afem::ThreadGroup* g = nullptr;
 };
 
 namespace afem {
@@ -136,6 +144,7 @@ afem_status guarded(F&& f) {
   } catch (const FactorizationError& e) { g_err = e.what(); return AFEM_E_FACTORIZATION;
   } catch (const InvertedElementError& e) { g_err = e.what(); return AFEM_E_INVERTED_ELEMENT;
   } catch (const CudaError& e) { g_err = e.what(); return AFEM_E_CUDA;
+  } catch (const NcclError& e) { g_err = e.what(); return AFEM_E_NCCL;
   } catch (const NomemError& e) { g_err = e.what(); return AFEM_E_NOMEM;
   } catch (const std::invalid_argument& e) { g_err = e.what(); return AFEM_E_INVALID_ARGUMENT;
   } catch (const std::out_of_range& e) { g_err = e.what(); return AFEM_E_OUT_OF_RANGE;
@@ -943,6 +952,122 @@ afem_status afem_load_stepping(afem_system sys, double total_strain, int32_t n_s
     }
     if (converged) *converged = 1;
     du.finish();
+  });
+}
+
+// ---- multi-GPU slab decomposition
+afem_status afem_slab_range(int32_t nz, int32_t size, int32_t rank, int32_t* z0, int32_t* z1) {
+  return guarded([&] {
+    need(z0, "z0");
+    need(z1, "z1");
+    slab_range(nz, size, rank, z0, z1);
+  });
+}
+
+afem_status afem_nccl_unique_id(void* out) {
+  return guarded([&] {
+    need(out, "out");
+    nccl_unique_id(out);
+  });
+}
+
+afem_status afem_dist_create_nccl(afem_ctx ctx, const void* uid, int32_t rank, int32_t size, afem_dist* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(uid, "uid");
+    need(out, "out");
+    begin(ctx->c);
+    auto d = std::make_unique<afem_dist_s>();
+    d->ctx = &ctx->c;
+    d->comm.reset(comm_create_nccl(uid, rank, size));
+    *out = d.release();
+  });
+}
+
+afem_status afem_thread_group_create(int32_t size, afem_thread_group* out) {
+  return guarded([&] {
+    need(out, "out");
+    auto g = std::make_unique<afem_thread_group_s>();
+    g->g = thread_group_create(size);
+    *out = g.release();
+  });
+}
+
+afem_status afem_thread_group_destroy(afem_thread_group g) {
+  return guarded([&] {
+    if (!g) return;
+    thread_group_destroy(g->g);
+    delete g;
+  });
+}
+
+afem_status afem_dist_create_threads(afem_ctx ctx, afem_thread_group g, int32_t rank, afem_dist* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(g, "group");
+    need(out, "out");
+    auto d = std::make_unique<afem_dist_s>();
+    d->ctx = &ctx->c;
+    d->comm.reset(comm_create_threads(g->g, rank));
+    *out = d.release();
+  });
+}
+
+afem_status afem_dist_destroy(afem_dist d) {
+  return guarded([&] { delete d; });
+}
+
+afem_status afem_dist_set_benchmark_dirichlet(afem_dist d, afem_system slab, double strain, double lx_global) {
+  return guarded([&] {
+    need(d, "dist");
+    System& s = SYS(slab);
+    set_dirichlet(s, slab_benchmark_bcs(s, d->comm->rank, d->comm->size, strain, lx_global));
+  });
+}
+
+afem_status afem_dist_op_create_mf(afem_dist d, afem_system slab, const double* u, afem_op* out) {
+  return guarded([&] {
+    need(d, "dist");
+    need(u, "u");
+    need(out, "out");
+    System& s = SYS(slab);
+    In<double> du(*s.ctx, u, s.n_dof);
+    auto h = std::make_unique<afem_op_s>();
+    h->op = make_dist_mf_op(s, d->comm.get(), make_mf_op(s, du.d));
+    *out = h.release();
+  });
+}
+
+afem_status afem_dist_solve(afem_dist d, afem_op op, const afem_solver_cfg* cfg, const double* b, const double* x0,
+                            double* x, afem_solve_report* rep, double* history, int32_t hist_cap) {
+  return guarded([&] {
+    need(d, "dist");
+    need(op, "op");
+    need(cfg, "cfg");
+    need(b, "b");
+    need(x, "x");
+    auto* dop = dynamic_cast<DistMfOp*>(op->op.get());
+    if (!dop) throw std::invalid_argument("afem_dist_solve: operator is not distributed");
+    Ctx& c = begin(*dop->sys->ctx);
+    In<double> db(c, b, dop->n), dx0(c, x0, dop->n);
+    Out<double> dx(c, x, dop->n, false);
+    SolveReport r;
+    dist_solve(*dop, to_cfg(cfg), db.d, dx0.d, dx.d, r);
+    dx.finish();
+    fill_report(r, rep, history, hist_cap);
+  });
+}
+
+afem_status afem_dist_dot(afem_dist d, afem_op op, const double* a, const double* b, double* out) {
+  return guarded([&] {
+    need(d, "dist");
+    need(op, "op");
+    need(out, "out");
+    auto* dop = dynamic_cast<DistMfOp*>(op->op.get());
+    if (!dop) throw std::invalid_argument("afem_dist_dot: operator is not distributed");
+    Ctx& c = begin(*dop->sys->ctx);
+    In<double> da(c, a, dop->n), dbb(c, b, dop->n);
+    *out = dist_dot(*dop, da.d, dbb.d);
   });
 }
 

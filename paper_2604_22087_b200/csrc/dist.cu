@@ -1,0 +1,514 @@
+// Multi-GPU slab decomposition: one process per GPU, each owning a contiguous z-slab of
+// element layers. The node plane between two slabs is held by both ranks and owned by the lower
+// one. The matrix-free operator applies the local stencil (the slab's own elements only, so the
+// shared planes receive partial sums — the z-face families of stencil.cu are exactly the one-sided
+// sums), then adds the neighbour's partial plane (one plane exchanged with each neighbour) and
+// re-imposes the unit Dirichlet rows. Dot products run over owned dofs and are summed across
+// ranks. The collectives are the only data-path communication: a plane exchange per apply and
+// scalar allreduces in the Krylov loop, over NCCL (NVLink/NVSwitch) — or, for single-GPU tests
+// of the same algorithm, over a threads backend (several subdomains on one device).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "afem_impl.hpp"
+#include "dist.hpp"
+#include "reduce.cuh"
+
+namespace afem {
+
+unsigned red_grid(int64_t n);
+
+// ------------------------------------------------------------------ NCCL (dlopen: reuse the copy
+// the process already loaded, e.g. torch's, else the system one)
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static bool loaded = false;
+  if (loaded) return api;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) throw std::runtime_error(std::string("NCCL unavailable: ") + dlerror());
+  auto sym = [&](const char* n) {
+    void* f = dlsym(h, n);
+    if (!f) throw std::runtime_error(std::string("NCCL symbol missing: ") + n);
+    return f;
+  };
+  api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(sym("ncclGetUniqueId"));
+  api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(sym("ncclCommInitRank"));
+  api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(sym("ncclCommDestroy"));
+  api.allReduce = reinterpret_cast<decltype(api.allReduce)>(sym("ncclAllReduce"));
+  api.send = reinterpret_cast<decltype(api.send)>(sym("ncclSend"));
+  api.recv = reinterpret_cast<decltype(api.recv)>(sym("ncclRecv"));
+  api.groupStart = reinterpret_cast<decltype(api.groupStart)>(sym("ncclGroupStart"));
+  api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(sym("ncclGroupEnd"));
+  api.errorString = reinterpret_cast<decltype(api.errorString)>(sym("ncclGetErrorString"));
+  loaded = true;
+  return api;
+}
+
+#define AFEM_NCCL(x)                                                                           \
+  do {                                                                                         \
+    ncclResult_t r_ = (x);                                                                     \
+    if (r_ != ncclSuccess) throw NcclError(std::string("NCCL: ") + nccl().errorString(r_));   \
+  } while (0)
+
+void nccl_unique_id(void* out) {
+  ncclUniqueId id;
+  AFEM_NCCL(nccl().getUniqueId(&id));
+  std::memcpy(out, &id, sizeof id);
+}
+
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  NcclComm(const void* uid, int r, int n) {
+    rank = r;
+    size = n;
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof id);
+    AFEM_NCCL(nccl().commInitRank(&comm, n, id, r));
+  }
+  ~NcclComm() override {
+    if (comm) nccl().commDestroy(comm);
+  }
+  void allreduce_sum(double* d, int n, cudaStream_t s) override {
+    AFEM_NCCL(nccl().allReduce(d, d, n, ncclFloat64, ncclSum, comm, s));
+  }
+  void exchange(const double* send_lo, double* recv_lo, const double* send_hi, double* recv_hi, size_t n,
+                cudaStream_t s) override {
+    AFEM_NCCL(nccl().groupStart());
+    if (send_lo) {
+      AFEM_NCCL(nccl().send(send_lo, n, ncclFloat64, rank - 1, comm, s));
+      AFEM_NCCL(nccl().recv(recv_lo, n, ncclFloat64, rank - 1, comm, s));
+    }
+    if (send_hi) {
+      AFEM_NCCL(nccl().send(send_hi, n, ncclFloat64, rank + 1, comm, s));
+      AFEM_NCCL(nccl().recv(recv_hi, n, ncclFloat64, rank + 1, comm, s));
+    }
+    AFEM_NCCL(nccl().groupEnd());
+  }
+};
+
+// ------------------------------------------------------------------ threads backend
+struct ThreadGroup {
+  int n = 1;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<double> vals;
+  std::vector<const double*> lo, hi;
+  explicit ThreadGroup(int size) : n(size), lo(size, nullptr), hi(size, nullptr) {}
+  void barrier() {
+    std::unique_lock<std::mutex> l(m);
+    const uint64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(l, [&] { return gen != g; });
+    }
+  }
+};
+
+struct ThreadComm : Comm {
+  ThreadGroup* g;
+  ThreadComm(ThreadGroup* grp, int r) : g(grp) {
+    rank = r;
+    size = grp->n;
+  }
+  void allreduce_sum(double* d, int n, cudaStream_t s) override {
+    std::vector<double> h(n);
+    AFEM_CK(cudaMemcpyAsync(h.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    AFEM_CK(cudaStreamSynchronize(s));
+    {
+      std::lock_guard<std::mutex> l(g->m);
+      if (g->vals.size() < static_cast<size_t>(g->n * n)) g->vals.resize(g->n * n);
+      std::memcpy(&g->vals[rank * n], h.data(), n * sizeof(double));
+    }
+    g->barrier();
+    for (int k = 0; k < n; ++k) {  // fixed rank order: identical on every rank
+      double t = 0.0;
+      for (int r = 0; r < g->n; ++r) t += g->vals[r * n + k];
+      h[k] = t;
+    }
+    g->barrier();
+    AFEM_CK(cudaMemcpyAsync(d, h.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+    AFEM_CK(cudaStreamSynchronize(s));
+  }
+  void exchange(const double* send_lo, double* recv_lo, const double* send_hi, double* recv_hi, size_t n,
+                cudaStream_t s) override {
+    AFEM_CK(cudaStreamSynchronize(s));
+    g->lo[rank] = send_lo;
+    g->hi[rank] = send_hi;
+    g->barrier();
+    if (recv_lo) AFEM_CK(cudaMemcpyAsync(recv_lo, g->hi[rank - 1], n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (recv_hi) AFEM_CK(cudaMemcpyAsync(recv_hi, g->lo[rank + 1], n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    AFEM_CK(cudaStreamSynchronize(s));
+    g->barrier();
+  }
+};
+
+ThreadGroup* thread_group_create(int n) {
+  if (n < 1) throw std::invalid_argument("thread group: size must be >= 1");
+  return new ThreadGroup(n);
+}
+void thread_group_destroy(ThreadGroup* g) { delete g; }
+Comm* comm_create_nccl(const void* uid, int rank, int size) {
+  if (size < 1 || rank < 0 || rank >= size) throw std::invalid_argument("dist: bad rank/size");
+  return new NcclComm(uid, rank, size);
+}
+Comm* comm_create_threads(ThreadGroup* g, int rank) {
+  if (!g || rank < 0 || rank >= g->n) throw std::invalid_argument("dist: bad rank for thread group");
+  return new ThreadComm(g, rank);
+}
+
+// ------------------------------------------------------------------ slab partition
+void slab_range(int nz, int size, int rank, int* z0, int* z1) {
+  if (size < 1 || rank < 0 || rank >= size) throw std::invalid_argument("slab: bad rank/size");
+  if (nz < size) throw std::invalid_argument("slab: fewer element layers than ranks");
+  const int base = nz / size, extra = nz % size;  // the first `extra` ranks take one more layer
+  *z0 = rank * base + std::min(rank, extra);
+  *z1 = *z0 + base + (rank < extra ? 1 : 0);
+}
+
+// benchmark_bcs of the global grid restricted to a slab (3D twin of mesh.hpp:89-101).
+std::vector<Constraint> slab_benchmark_bcs(const System& s, int rank, int size, double strain, double lx_global) {
+  if (!s.grid || s.dim != 3) throw std::invalid_argument("slab bcs: 3D grid system required");
+  std::vector<Constraint> c;
+  const int nx = s.nx, ny = s.ny, nz = s.nz;
+  auto node = [&](int i, int j, int k) { return i + (nx + 1) * (j + (ny + 1) * k); };
+  for (int k = 0; k <= nz; ++k)
+    for (int j = 0; j <= ny; ++j) c.push_back({node(0, j, k), 0, 0.0});
+  if (rank == 0) {
+    c.push_back({node(0, 0, 0), 1, 0.0});
+    c.push_back({node(0, 0, 0), 2, 0.0});
+  }
+  if (rank == size - 1) c.push_back({node(0, 0, nz), 1, 0.0});
+  const double u_right = strain * lx_global;
+  for (int k = 0; k <= nz; ++k)
+    for (int j = 0; j <= ny; ++j) c.push_back({node(nx, j, k), 0, u_right});
+  return c;
+}
+
+// ------------------------------------------------------------------ distributed operator
+namespace {
+
+__global__ void k_add(double* __restrict__ v, const double* __restrict__ w, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] += w[i];
+}
+
+__global__ void k_reset_masked(double* __restrict__ v, const double* __restrict__ x, const uint8_t* __restrict__ mask,
+                               double one_or_x, int use_x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (mask[i]) v[i] = use_x ? x[i] : one_or_x;
+}
+
+}  // namespace
+
+DistMfOp::~DistMfOp() = default;
+
+void DistMfOp::halo_add(double* v, const double* x_for_mask, bool diag_mode) {
+  Ctx& c = *sys->ctx;
+  if (comm->size == 1) return;
+  const int64_t np = plane;
+  const bool lo = comm->rank > 0, hi = comm->rank < comm->size - 1;
+  double* top = v + (n - np);
+  if (lo) copy(c, v, send_lo.p, np);
+  if (hi) copy(c, top, send_hi.p, np);
+  comm->exchange(lo ? send_lo.p : nullptr, lo ? recv_lo.p : nullptr, hi ? send_hi.p : nullptr,
+                 hi ? recv_hi.p : nullptr, static_cast<size_t>(np), c.stream);
+  const unsigned g = grid_for(np, 256, 148 * 4);
+  if (lo) {
+    launch(c, k_add, g, 256, 0, v, recv_lo.p, np);
+    launch(c, k_reset_masked, g, 256, 0, v, x_for_mask, local->mask.p, 1.0, diag_mode ? 0 : 1, np);
+  }
+  if (hi) {
+    launch(c, k_add, g, 256, 0, top, recv_hi.p, np);
+    launch(c, k_reset_masked, g, 256, 0, top, x_for_mask ? x_for_mask + (n - np) : nullptr,
+           local->mask.p + (n - np), 1.0, diag_mode ? 0 : 1, np);
+  }
+}
+
+void DistMfOp::apply(const double* x, double* y) {
+  local->apply(x, y);
+  halo_add(y, x, false);
+}
+
+void DistMfOp::diagonal(double* d) { copy(*sys->ctx, diag.p, d, n); }
+
+std::unique_ptr<DistMfOp> make_dist_mf_op(System& s, Comm* comm, std::unique_ptr<MfOp> local) {
+  if (!s.grid || s.dim != 3) throw std::invalid_argument("dist operator: 3D grid (slab) system required");
+  auto op = std::make_unique<DistMfOp>();
+  op->sys = &s;
+  op->kind = 1;
+  op->n = s.n_dof;
+  op->comm = comm;
+  op->plane = static_cast<int64_t>(s.nx + 1) * (s.ny + 1) * 3;
+  op->owned_offset = comm->rank > 0 ? op->plane : 0;
+  op->send_lo.alloc(op->plane);
+  op->recv_lo.alloc(op->plane);
+  op->send_hi.alloc(op->plane);
+  op->recv_hi.alloc(op->plane);
+  op->local = std::move(local);
+  op->diag.alloc(s.n_dof);
+  op->local->diagonal(op->diag.p);
+  op->halo_add(op->diag.p, nullptr, true);  // Jacobi diagonal of the global operator, unit on constraints
+  AFEM_CK(cudaStreamSynchronize(s.ctx->stream));
+  return op;
+}
+
+// ------------------------------------------------------------------ distributed CG (krylov.hpp:350-408)
+namespace {
+
+struct DcgDev {
+  double rz, pap, beta, denom, rtol, loc[2];
+  int it, max_iter, done, fail, conv;
+};
+
+__global__ void k_owned_dot(const double* a, const double* b, int64_t n, double* partials, unsigned* counter,
+                            double* out) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s += a[i] * b[i];
+  double v[1] = {s};
+  if (grid_reduce<1>(v, partials, counter))
+    if (threadIdx.x == 0) out[0] = v[0];
+}
+
+// r = b - Ax (all dofs); out = owned sum of r^2
+__global__ void k_dres(const double* b, const double* ax, double* r, int64_t n, int64_t off, double* partials,
+                       unsigned* counter, double* out) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = b[i] - ax[i];
+    if (r) r[i] = d;
+    if (i >= off) s += d * d;
+  }
+  double v[1] = {s};
+  if (grid_reduce<1>(v, partials, counter))
+    if (threadIdx.x == 0) out[0] = v[0];
+}
+
+// p = z = M r; loc[0] = owned r.z
+__global__ void k_dcg_start(const double* r, const double* inv, double* p, int64_t n, int64_t off, double* partials,
+                            unsigned* counter, DcgDev* st) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double z = inv ? r[i] * inv[i] : r[i];
+    p[i] = z;
+    if (i >= off) s += r[i] * z;
+  }
+  double v[1] = {s};
+  if (grid_reduce<1>(v, partials, counter))
+    if (threadIdx.x == 0) st->loc[0] = v[0];
+}
+
+__global__ void k_dcg_start_finish(DcgDev* st) {
+  st->rz = st->loc[0];
+  st->done = 0;
+}
+
+__global__ void k_dcg_pap(const double* p, const double* ap, int64_t n, int64_t off, double* partials,
+                          unsigned* counter, DcgDev* st) {
+  if (st->done) return;
+  double s = 0.0;
+  for (int64_t i = off + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s += p[i] * ap[i];
+  double v[1] = {s};
+  if (grid_reduce<1>(v, partials, counter))
+    if (threadIdx.x == 0) st->pap = v[0];
+}
+
+__global__ void k_dcg_update(double* x, const double* p, double* r, const double* ap, const double* inv, int64_t n,
+                             int64_t off, double* partials, unsigned* counter, DcgDev* st) {
+  if (st->done || !(st->pap > 0.0)) return;
+  const double a = st->rz / st->pap;
+  double rr = 0.0, rz = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += a * p[i];
+    const double ri = r[i] - a * ap[i];
+    r[i] = ri;
+    if (i >= off) {
+      rr += ri * ri;
+      rz += ri * (inv ? ri * inv[i] : ri);
+    }
+  }
+  double v[2] = {rr, rz};
+  if (grid_reduce<2>(v, partials, counter))
+    if (threadIdx.x == 0) {
+      st->loc[0] = v[0];
+      st->loc[1] = v[1];
+    }
+}
+
+__global__ void k_dcg_finish(DcgDev* st, double* hist) {
+  if (st->done) return;
+  if (!(st->pap > 0.0)) {  // krylov.hpp:377-381
+    st->fail = 1;
+    st->done = 1;
+    return;
+  }
+  const int it = st->it + 1;
+  st->it = it;
+  const double h = sqrt(st->loc[0]) / st->denom;
+  hist[it] = h;
+  if (h <= st->rtol) {
+    st->done = 1;
+    st->conv = 1;
+  } else {
+    st->beta = st->loc[1] / st->rz;
+    st->rz = st->loc[1];
+    if (it >= st->max_iter) st->done = 1;
+  }
+}
+
+__global__ void k_dcg_p(const double* r, const double* inv, double* p, int64_t n, const DcgDev* st) {
+  if (st->done) return;
+  const double b = st->beta;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (inv ? r[i] * inv[i] : r[i]) + b * p[i];
+}
+
+__global__ void k_inv(const double* d, double* inv, int64_t n, unsigned long long* first_zero) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (d[i] == 0.0) atomicMin(first_zero, static_cast<unsigned long long>(i));
+    inv[i] = 1.0 / d[i];
+  }
+}
+
+template <class T>
+T fetch_dev(Ctx& c, const T* d) {
+  T h{};
+  AFEM_CK(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+  AFEM_CK(cudaStreamSynchronize(c.stream));
+  return h;
+}
+
+}  // namespace
+
+// Global ||b - A x|| over owned dofs (keeps r when given).
+static double dist_residual_norm(DistMfOp& op, const double* b, const double* x, double* scratch, double* r,
+                                 double* scal) {
+  Ctx& c = *op.sys->ctx;
+  op.apply(x, scratch);
+  launch(c, k_dres, red_grid(op.n), kRedThreads, 0, b, scratch, r, op.n, op.owned_offset, c.red_partials.p,
+         c.red_counter.p, scal);
+  op.comm->allreduce_sum(scal, 1, c.stream);
+  return std::sqrt(fetch_dev(c, scal));
+}
+
+void dist_solve(DistMfOp& op, const SolverCfg& cfg, const double* b, const double* x0, double* x, SolveReport& rep) {
+  validate_cfg(cfg);
+  if (cfg.method != 0) throw CapabilityError("distributed run_solver: CG only");
+  if (cfg.precond != 0 && cfg.precond != 1) throw CapabilityError("distributed run_solver: NONE or JACOBI");
+  const auto t0 = std::chrono::steady_clock::now();
+  Ctx& c = *op.sys->ctx;
+  const int64_t n = op.n, off = op.owned_offset;
+  const unsigned rg = red_grid(n), eg = grid_for(n, 256, 148 * 16);
+  DevArray<double> inv, r(n), p(n), ap(n), scratch(n), hist(cfg.max_iter + 2), scal(4);
+  if (cfg.precond == 1) {
+    inv.alloc(n);
+    DevArray<unsigned long long> fz(1);
+    const unsigned long long init = ~0ull;
+    AFEM_CK(cudaMemcpyAsync(fz.p, &init, 8, cudaMemcpyHostToDevice, c.stream));
+    launch(c, k_inv, eg, 256, 0, op.diag.p, inv.p, n, fz.p);
+    const unsigned long long z = fetch_dev(c, fz.p);
+    if (z != ~0ull) throw FactorizationError("jacobi: zero diagonal at local row " + std::to_string(z));
+  }
+  if (x0) copy(c, x0, x, n);
+  else fill(c, 0.0, x, n);
+  // ||b|| over owned dofs, summed across ranks
+  launch(c, k_owned_dot, rg, kRedThreads, 0, b + off, b + off, n - off, c.red_partials.p, c.red_counter.p, scal.p);
+  op.comm->allreduce_sum(scal.p, 1, c.stream);
+  const double bnorm = std::sqrt(fetch_dev(c, scal.p));
+  const double denom = bnorm > 0.0 ? bnorm : 1.0;
+  rep.history.assign(1, dist_residual_norm(op, b, x, ap.p, r.p, scal.p) / denom);
+  DevArray<DcgDev> st(1);
+  DcgDev hs{};
+  hs.denom = denom;
+  hs.rtol = cfg.rtol;
+  hs.max_iter = cfg.max_iter;
+  hs.done = 1;
+  AFEM_CK(cudaMemcpyAsync(st.p, &hs, sizeof hs, cudaMemcpyHostToDevice, c.stream));
+  double* loc = reinterpret_cast<double*>(reinterpret_cast<char*>(st.p) + offsetof(DcgDev, loc));
+  double* pap = reinterpret_cast<double*>(reinterpret_cast<char*>(st.p) + offsetof(DcgDev, pap));
+  while (true) {
+    if (rep.history.back() > cfg.rtol && rep.iterations < cfg.max_iter) {
+      launch(c, k_dcg_start, rg, kRedThreads, 0, r.p, inv.p, p.p, n, off, c.red_partials.p, c.red_counter.p, st.p);
+      op.comm->allreduce_sum(loc, 1, c.stream);
+      launch(c, k_dcg_start_finish, 1, 1, 0, st.p);
+      int chunk = 4;
+      while (true) {
+        for (int k = 0; k < chunk; ++k) {
+          op.apply(p.p, ap.p);
+          launch(c, k_dcg_pap, rg, kRedThreads, 0, p.p, ap.p, n, off, c.red_partials.p, c.red_counter.p, st.p);
+          op.comm->allreduce_sum(pap, 1, c.stream);
+          launch(c, k_dcg_update, rg, kRedThreads, 0, x, p.p, r.p, ap.p, inv.p, n, off, c.red_partials.p,
+                 c.red_counter.p, st.p);
+          op.comm->allreduce_sum(loc, 2, c.stream);
+          launch(c, k_dcg_finish, 1, 1, 0, st.p, hist.p);
+          launch(c, k_dcg_p, eg, 256, 0, r.p, inv.p, p.p, n, st.p);
+        }
+        hs = fetch_dev(c, st.p);
+        if (hs.done) break;
+        chunk = std::min(chunk * 2, 64);
+      }
+      const int it0 = rep.iterations;
+      rep.iterations = hs.it;
+      if (hs.it > it0) {
+        rep.history.resize(hs.it + 1);
+        AFEM_CK(cudaMemcpyAsync(rep.history.data() + it0 + 1, hist.p + it0 + 1, (hs.it - it0) * sizeof(double),
+                                cudaMemcpyDeviceToHost, c.stream));
+        AFEM_CK(cudaStreamSynchronize(c.stream));
+      }
+      if (hs.fail)
+        rep.failure = "cg: operator not positive definite (p^T A p <= 0 at iteration " +
+                      std::to_string(rep.iterations + 1) + ")";
+    }
+    const double true_rres = dist_residual_norm(op, b, x, scratch.p, nullptr, scal.p) / denom;
+    rep.history.back() = true_rres;
+    if (true_rres <= cfg.rtol) {
+      rep.converged = rep.failure.empty();
+      break;
+    }
+    if (!rep.failure.empty() || rep.iterations >= cfg.max_iter) break;
+    dist_residual_norm(op, b, x, ap.p, r.p, scal.p);
+  }
+  AFEM_CK(cudaStreamSynchronize(c.stream));
+  rep.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Global owned dot (tests / drivers).
+double dist_dot(DistMfOp& op, const double* a, const double* b) {
+  Ctx& c = *op.sys->ctx;
+  DevArray<double> s(1);
+  const int64_t off = op.owned_offset;
+  launch(c, k_owned_dot, red_grid(op.n - off), kRedThreads, 0, a + off, b + off, op.n - off, c.red_partials.p,
+         c.red_counter.p, s.p);
+  op.comm->allreduce_sum(s.p, 1, c.stream);
+  return fetch_dev(c, s.p);
+}
+
+}  // namespace afem

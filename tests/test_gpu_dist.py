@@ -1,0 +1,101 @@
+"""GPU tests of the slab-decomposed operator and CG (dist.cu) on one B200: the threads backend runs
+2-3 subdomains (one host thread + stream each) through the same code path the NCCL backend runs
+across GPUs; the NCCL backend itself is exercised at world size 1.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from tests.helpers import LINEAR, rel_err
+
+pytestmark = pytest.mark.gpu
+
+NX, NY, NZ = 64, 10, 24
+STRAIN = 0.01
+
+
+@pytest.fixture(scope="module")
+def afem():
+    import paper_2604_22087_b200 as m
+    m.load()
+    return m
+
+
+def _global(afem):
+    ctx = afem.Context(0)
+    fib = afem.fibres(12345, 6)
+    s = afem.System.grid(ctx, 3, NX, NY, NZ, inclusions=fib, radius=0.15, materials=LINEAR)
+    s.set_benchmark_dirichlet(STRAIN)
+    u = s.impose_dirichlet(np.zeros(s.n))
+    x = np.random.default_rng(1).uniform(-1, 1, s.n)
+    op = afem.matrix_free_operator(s, u)
+    b = -s.constrain_residual(s.residual(u), u)
+    return ctx, fib, s, u, x, op, b
+
+
+def _run_threads(afem, size, fib, x, b, results):
+    group = afem.ThreadGroup(size)
+    plane = 3 * (NX + 1) * (NY + 1)
+
+    def work(rank):
+        try:
+            ctx = afem.Context(0)
+            sys_, (z0, z1) = afem.slab_system(ctx, NX, NY, NZ, rank, size, inclusions=fib, radius=0.15,
+                                              materials=LINEAR)
+            d = afem.Dist(ctx, rank, size, backend="threads", group=group)
+            d.set_benchmark_dirichlet(sys_, STRAIN)
+            sl = slice(plane * z0, plane * (z1 + 1))
+            u = sys_.impose_dirichlet(np.zeros(sys_.n))
+            op = d.matrix_free_operator(sys_, u)
+            y = op.apply(x[sl])
+            dot = d.dot(op, x[sl], y)
+            xs, rep = d.run_solver(op, b[sl], method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
+            results[rank] = dict(z=(z0, z1), y=y, dot=dot, x=xs, rep=rep, stencil=op.uses_stencil)
+        except Exception as e:  # surfaced by the caller
+            results[rank] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(size)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    return plane
+
+
+@pytest.mark.parametrize("size", [2, 3])
+def test_threads_backend_matches_single_domain(afem, size):
+    ctx, fib, s, u, x, op, b = _global(afem)
+    y_global = op.apply(x)
+    xg, rg = afem.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
+    results = {}
+    plane = _run_threads(afem, size, fib, x, b, results)
+    for r in range(size):
+        assert not isinstance(results[r], Exception), results[r]
+    for r in range(size):
+        res = results[r]
+        z0, z1 = res["z"]
+        sl = slice(plane * z0, plane * (z1 + 1))
+        assert res["stencil"]
+        assert rel_err(res["y"], y_global[sl]) <= 1e-12
+        assert abs(res["dot"] - float(x @ y_global)) <= 1e-12 * abs(float(x @ y_global))
+        assert res["rep"]["converged"]
+        assert abs(res["rep"]["iterations"] - rg["iterations"]) <= 2
+        assert rel_err(res["x"], xg[sl]) <= 1e-8
+    # every rank reports the same history (identical global scalars)
+    h0 = results[0]["rep"]["residual_history"]
+    for r in range(1, size):
+        assert np.array_equal(results[r]["rep"]["residual_history"], h0)
+
+
+def test_nccl_backend_single_rank(afem):
+    ctx, fib, s, u, x, op, b = _global(afem)
+    xg, rg = afem.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
+    d = afem.Dist(ctx, 0, 1, backend="nccl", uid=afem.nccl_unique_id())
+    sys_, _ = afem.slab_system(ctx, NX, NY, NZ, 0, 1, inclusions=fib, radius=0.15, materials=LINEAR)
+    d.set_benchmark_dirichlet(sys_, STRAIN)
+    dop = d.matrix_free_operator(sys_, sys_.impose_dirichlet(np.zeros(sys_.n)))
+    assert rel_err(dop.apply(x), op.apply(x)) <= 1e-12
+    xs, rep = d.run_solver(dop, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
+    assert rep["converged"] and abs(rep["iterations"] - rg["iterations"]) <= 2
+    assert rel_err(xs, xg) <= 1e-8
