@@ -80,7 +80,8 @@ def test_threads_backend_matches_single_domain(afem, size):
         assert rel_err(res["y"], y_global[sl]) <= 1e-12
         assert abs(res["dot"] - float(x @ y_global)) <= 1e-12 * abs(float(x @ y_global))
         assert res["rep"]["converged"]
-        assert abs(res["rep"]["iterations"] - rg["iterations"]) <= 2
+        # dot products reduce per slab, then across slabs: a different (fixed) summation order
+        assert abs(res["rep"]["iterations"] - rg["iterations"]) <= max(2, rg["iterations"] // 100)
         assert rel_err(res["x"], xg[sl]) <= 1e-8
     # every rank reports the same history (identical global scalars)
     h0 = results[0]["rep"]["residual_history"]
