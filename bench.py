@@ -18,8 +18,9 @@ benchmark BCs at 1% strain, state u0 = BC-consistent; fp64 matrix-free K(u0) x a
             cores on a z-slab sample of the same mesh (min over 3 reps)
 
 --impl reference runs the CPU path only (oracle port, all host threads) on the same metric/config.
-Multi-GPU (torchrun, N > 1): each rank owns one 128^3 subdomain replica (weak scaling; the slab
-halo exchange is not yet on this path — see DESIGN.md §Multi-GPU).
+Multi-GPU (torchrun, N > 1): weak scaling over z-slabs — the global RVE is 128 x 128 x (128 N)
+elements, each rank owns 128 element layers; every apply adds the shared node planes over NCCL and
+the CG dot products are NCCL allreduces. Time is the max over ranks.
 """
 import argparse
 import json
@@ -195,11 +196,23 @@ def ours(args, rank, world, local_rank):
     ctx = afem.Context(local_rank, stream=stream)
     n = args.n
     fib = afem.fibres(SEED, N_FIBRES)
-    sys_ = afem.System.grid(ctx, 3, n, n, n, inclusions=fib, radius=RADIUS, materials=MATS)
-    sys_.set_benchmark_dirichlet(STRAIN)
+    D = None
+    if world > 1:
+        # weak scaling over z-slabs: the global RVE is n x n x (n * world) elements of the same size
+        # ([0,1]^2 x [0, world]); each rank owns n element layers; NCCL plane halo + allreduces
+        uid = [afem.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        D = afem.Dist(ctx, rank, world, backend="nccl", uid=uid[0])
+        sys_, _ = afem.slab_system(ctx, n, n, n * world, rank, world, lz=float(world), inclusions=fib,
+                                   radius=RADIUS, materials=MATS)
+        D.set_benchmark_dirichlet(sys_, STRAIN, 1.0)
+    else:
+        sys_ = afem.System.grid(ctx, 3, n, n, n, inclusions=fib, radius=RADIUS, materials=MATS)
+        sys_.set_benchmark_dirichlet(STRAIN)
     n_dof, n_elem = sys_.n, sys_.info.n_elem
+    global_dofs = 3 * (n + 1) ** 2 * (n * world + 1)
     u0 = sys_.impose_dirichlet(np.zeros(n_dof))
-    op = afem.matrix_free_operator(sys_, u0)
+    op = D.matrix_free_operator(sys_, u0) if D else afem.matrix_free_operator(sys_, u0)
     assert op.uses_stencil, "structured stencil path not selected"
     vf = float(sys_.mesh()[2].mean())
 
@@ -234,7 +247,7 @@ def ours(args, rank, world, local_rank):
         T = float(t.item())
         dist.barrier()
     t_apply = T / args.steps * 1e-3  # s per apply (max over ranks)
-    value = world * n_dof * args.steps / (T * 1e-3)
+    value = global_dofs * args.steps / (T * 1e-3)
 
     clk = clocks.stop()
 
@@ -243,8 +256,11 @@ def ours(args, rank, world, local_rank):
     # synchronisations need); clocks are sampled again at a 1 s period around it.
     cg = None
     if not args.no_cg:
-        r0 = torch.from_numpy(sys_.constrain_residual(sys_.residual(u0), u0)).cuda()
-        b = -r0
+        r_loc = sys_.residual(u0)
+        if D:  # shared planes hold slab-partial residuals: assemble before constraining
+            r_loc = D.assemble(op, r_loc)
+        b = -torch.from_numpy(sys_.constrain_residual(r_loc, u0)).cuda()
+        solver = D.run_solver if D else afem.run_solver
         cg_clk = ClockSampler(local_rank, period_ms=1000)
         cg_clk.start()
         best = None
@@ -252,7 +268,7 @@ def ours(args, rank, world, local_rank):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record(stream)
-            du, rep = afem.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
+            du, rep = solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
             e1.record(stream)
             torch.cuda.synchronize()
             solve_s = e0.elapsed_time(e1) * 1e-3
@@ -283,12 +299,12 @@ def ours(args, rank, world, local_rank):
         t = torch.tensor([te], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         te = float(t.item())
-    e2e = {"value": world * n_dof * args.e2e_steps / te, "unit": UNIT, "h2d_bytes_per_step": 8 * n_dof,
+    e2e = {"value": global_dofs * args.e2e_steps / te, "unit": UNIT, "h2d_bytes_per_step": 8 * n_dof,
            "d2h_bytes_per_step": 8 * n_dof, "path": "afem_op_apply(op, pinned host x, pinned host y)"}
     if cg is not None:
         bh = b.cpu().numpy()
         t0 = time.perf_counter()
-        _, rep2 = afem.run_solver(op, bh, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
+        _, rep2 = solver(op, bh, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
         e2e["cg_solve_s"] = time.perf_counter() - t0
         e2e["cg_iterations"] = rep2["iterations"]
 
@@ -325,7 +341,9 @@ def ours(args, rank, world, local_rank):
                    "elements": n_elem, "n_dof": n_dof, "nnz_K": sys_.nnz, "fibres": N_FIBRES, "radius": RADIUS,
                    "fibre_volume_fraction": vf, "E": [1.0, 10.0], "nu": 0.3, "strain": STRAIN,
                    "l2": "flushed (256 MiB write) between timed applies",
-                   "parallelism": f"{world} independent subdomain(s), one per GPU"},
+                   "global_dofs": global_dofs,
+                   "parallelism": (f"z-slab decomposition over {world} GPUs (NCCL plane halo + allreduce), "
+                                   f"{n} element layers per GPU" if world > 1 else "1 GPU")},
         "cg": cg, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
     }
     print(json.dumps(line), flush=True)

@@ -273,6 +273,9 @@ afem_status afem_dist_op_create_mf(afem_dist d, afem_system slab, const double* 
 /* run_solver, CG (+ Jacobi), every rank calling collectively; reports are identical on all ranks. */
 afem_status afem_dist_solve(afem_dist d, afem_op op, const afem_solver_cfg* cfg, const double* b, const double* x0,
                             double* x, afem_solve_report* rep, double* history, int32_t hist_cap);
+/* Sum the shared planes of a slab-partial vector (e.g. a local residual) with the neighbours'
+ * partials, in place (collective). */
+afem_status afem_dist_assemble(afem_dist d, afem_op op, double* v);
 /* Global dot over owned dofs (collective). */
 afem_status afem_dist_dot(afem_dist d, afem_op op, const double* a, const double* b, double* out);
 

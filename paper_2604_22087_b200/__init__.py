@@ -168,6 +168,7 @@ def load():
         "afem_dist_op_create_mf": ([vp, vp, vp, vp], i32),
         "afem_dist_solve": ([vp, vp, vp, vp, vp, vp, vp, vp, i32], i32),
         "afem_dist_dot": ([vp, vp, vp, vp, vp], i32),
+        "afem_dist_assemble": ([vp, vp, vp], i32),
     }
     for name, (args, res) in sigs.items():
         f = getattr(L, name)
@@ -634,6 +635,12 @@ class Dist:
         return x, dict(converged=bool(rep.converged), iterations=rep.iterations,
                        residual_history=hist[:min(rep.n_history, cap)].copy(), wall_time=rep.wall_time,
                        failure=rep.failure.decode())
+
+    def assemble(self, op: LinearOperator, v):
+        """Sum the shared planes of a slab-partial vector with the neighbours' partials."""
+        v = v if hasattr(v, "data_ptr") else np.array(v, np.float64)
+        _check(_lib.afem_dist_assemble(self.h, op.h, _ptr(v)))
+        return v
 
     def dot(self, op: LinearOperator, a, b) -> float:
         out = C.c_double()

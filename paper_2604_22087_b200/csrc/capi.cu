@@ -1058,6 +1058,20 @@ afem_status afem_dist_solve(afem_dist d, afem_op op, const afem_solver_cfg* cfg,
   });
 }
 
+afem_status afem_dist_assemble(afem_dist d, afem_op op, double* v) {
+  return guarded([&] {
+    need(d, "dist");
+    need(op, "op");
+    need(v, "v");
+    auto* dop = dynamic_cast<DistMfOp*>(op->op.get());
+    if (!dop) throw std::invalid_argument("afem_dist_assemble: operator is not distributed");
+    Ctx& c = begin(*dop->sys->ctx);
+    Out<double> dv(c, v, dop->n, true);
+    dop->halo_add(dv.d, nullptr, false);
+    dv.finish();
+  });
+}
+
 afem_status afem_dist_dot(afem_dist d, afem_op op, const double* a, const double* b, double* out) {
   return guarded([&] {
     need(d, "dist");

@@ -240,14 +240,16 @@ void DistMfOp::halo_add(double* v, const double* x_for_mask, bool diag_mode) {
   comm->exchange(lo ? send_lo.p : nullptr, lo ? recv_lo.p : nullptr, hi ? send_hi.p : nullptr,
                  hi ? recv_hi.p : nullptr, static_cast<size_t>(np), c.stream);
   const unsigned g = grid_for(np, 256, 148 * 4);
+  const bool reset = diag_mode || x_for_mask;  // neither: plain assembly of partial sums
   if (lo) {
     launch(c, k_add, g, 256, 0, v, recv_lo.p, np);
-    launch(c, k_reset_masked, g, 256, 0, v, x_for_mask, local->mask.p, 1.0, diag_mode ? 0 : 1, np);
+    if (reset) launch(c, k_reset_masked, g, 256, 0, v, x_for_mask, local->mask.p, 1.0, diag_mode ? 0 : 1, np);
   }
   if (hi) {
     launch(c, k_add, g, 256, 0, top, recv_hi.p, np);
-    launch(c, k_reset_masked, g, 256, 0, top, x_for_mask ? x_for_mask + (n - np) : nullptr,
-           local->mask.p + (n - np), 1.0, diag_mode ? 0 : 1, np);
+    if (reset)
+      launch(c, k_reset_masked, g, 256, 0, top, x_for_mask ? x_for_mask + (n - np) : nullptr,
+             local->mask.p + (n - np), 1.0, diag_mode ? 0 : 1, np);
   }
 }
 
