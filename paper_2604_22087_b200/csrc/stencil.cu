@@ -56,9 +56,10 @@ struct StencilPlan {
   StencilParams p;
   DevArray<uint8_t> info;       // per node: bits 0-2 Dirichlet mask, bits 3-7 base phase code
   // correction items (k_stencil_items): mixed-family nodes and the edge columns
-  DevArray<int32_t> it_node;
-  DevArray<uint8_t> it_oct, it_seg, it_mode;
-  DevArray<uint32_t> it_zmask;
+  DevArray<uint64_t> it_rec;
+  DevArray<uint32_t> it_zm;
+  DevArray<double> Ed;   // modulus per phase code (32), device copy for the item kernel
+  int item_blocks = 1;
   // in-tile correction lists (k_stencil_main)
   DevArray<int32_t> c_ptr;
   DevArray<uint32_t> c_word;
@@ -68,10 +69,8 @@ struct StencilPlan {
   int fuse_items = 0;
   DevArray<double> part_main, part_items;  // fused p.Ap partials (main kernel, item kernel)
   DevArray<unsigned int> counter;
-  int item_blocks = 1;
-  DevArray<double> it_dE;
-  DevArray<double> Kg;   // Khat (row-major 24 x 24) in global memory for the item kernel
-  int64_t n_items = 0;   // padded to a multiple of 32
+  DevArray<double> Kg;   // Khat (row-major 24 x 24) in global memory for the correction kernels
+  int64_t n_items = 0;   // tile correction items incl. padding
   int64_t n_fix_nodes = 0, n_edge_nodes = 0;
   int kchunk = 16;
   int nchunks = 1;
@@ -502,105 +501,129 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
 
 
 // Correction items: one thread per (node, octant) pair. y_n receives dE * Khat_rows(o) x_e(o) with
-// dE = E_o - E_base(n) for mixed-family nodes of the main kernel, and dE = E_o (written, not added)
-// for the edge columns the main kernel does not cover. Items of a node are contiguous, in octant
-// order, and never straddle a warp (the plan pads); the segment head sums them with shuffles in a
-// fixed order and updates y — deterministic, no atomics. Khat is staged in shared memory as
-// Ks[q][a][ln] so lanes of different octants read adjacent words (conflict-free).
+// dE = E[octant phase] - E[base phase] (the base of an edge-column node is void, E = 0, and its
+// sum is written, not added). Items are ordered tile-major — (64 x 8 x-y tile, plane, node,
+// octant) — and every CTA walks one contiguous range of 32-item batches, so the x gathers of a
+// CTA stay inside a few planes of one tile and hit L1. Items of a node are contiguous and never
+// straddle a batch; the head sums them with fixed-order shuffles and updates y directly.
+// Deterministic (fixed batch -> CTA mapping, fixed shuffle order), no atomics, no barriers.
+// rec: node (low 32 bits, -1 = padding) | oct << 32 | seg << 35 | edge << 39 | pho << 40 |
+// phb << 45; zm: bit 3m+b = input b of element corner m is zero (Dirichlet or outside).
 constexpr int kItemThreads = 256;
+constexpr uint64_t kPadRec = 0xffffffffull;
 
 struct Items {
-  const int32_t* node;   // -1: padding
-  const uint8_t* oct;    // octant
-  const uint8_t* seg;    // head: number of items of the node (1..8); 0: not a head
-  const uint8_t* mode;   // head: 1 = edge node (write), 0 = add
-  const uint32_t* zmask; // bit 3m+b: input b of element node m is zero (Dirichlet or outside)
-  const double* dE;
-  int64_t n;             // padded count (multiple of 32)
+  const uint64_t* rec;
+  const uint32_t* zm;
+  int64_t n;  // multiple of 32
 };
 
 template <bool DOT>
-__global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, int NZ,
-                                                                 const double* __restrict__ Kg,
+__global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, const double* __restrict__ Kg,
+                                                                 const double* __restrict__ Epar,
                                                                  const double* __restrict__ x,
                                                                  const uint8_t* __restrict__ info, Items it,
                                                                  double* __restrict__ y, DotArgs dot) {
-  double dsum = 0.0;
   __shared__ double Ks[24][3][8];
-  for (int t = threadIdx.x; t < 576; t += blockDim.x) {  // coalesced global read of Khat (row-major)
-    const int r = t / 24, q = t % 24;                    // Ks[q][a][ln] = Khat[3 ln + a][q]
+  __shared__ double Es[32];
+  for (int t = threadIdx.x; t < 576; t += blockDim.x) {  // Ks[q][a][ln] = Khat[3 ln + a][q]
+    const int r = t / 24, q = t % 24;
     Ks[q][r % 3][r / 3] = __ldg(&Kg[t]);
   }
+  if (threadIdx.x < 32) Es[threadIdx.x] = __ldg(&Epar[threadIdx.x]);
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < it.n; base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = base + threadIdx.x;
-    const int32_t node = t < it.n ? it.node[t] : -1;
-    double r[3] = {0.0, 0.0, 0.0};
-    int i = 0, j = 0, k = 0;
-    if (node >= 0) {
-      i = node % NX;
-      const int rr = node / NX;
-      j = rr % NY;
-      k = rr / NY;
-      const int o = it.oct[t];
-      const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
-      const int ei = i - 1 + ox, ej = j - 1 + oy, ek = k - 1 + oz;
-      const int ln = local_node(1 - ox, 1 - oy, 1 - oz);
-      const uint32_t zm = it.zmask[t];
-      double xv[24];
-#pragma unroll
-      for (int m = 0; m < 8; ++m) {  // 24 independent loads in flight
-        const int ii = ei + corner_x(m), jj = ej + corner_y(m), kk = ek + (m >> 2);
-        const bool in = ii >= 0 && ii < NX && jj >= 0 && jj < NY && kk >= 0 && kk < NZ;
-        const int64_t nd = in ? ii + (int64_t)NX * (jj + (int64_t)NY * kk) : 0;
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const double v = __ldg(&x[3 * nd + b]);
-          xv[3 * m + b] = ((zm >> (3 * m + b)) & 1) ? 0.0 : v;
-        }
-      }
-      const double dE = it.dE[t];
+  double dsum = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t nb = it.n >> 5;
+  const int64_t blo = nb * blockIdx.x / gridDim.x, bhi = nb * (blockIdx.x + 1) / gridDim.x;
+  const int NXY = NX * NY;
+  uint64_t nrec = kPadRec;
+  uint32_t nzm = 0;
+  if (blo + warp < bhi) {
+    nrec = __ldg(&it.rec[(blo + warp) * 32 + lane]);
+    nzm = __ldg(&it.zm[(blo + warp) * 32 + lane]);
+  }
+  for (int64_t bt = blo + warp; bt < bhi; bt += nw) {
+    const uint64_t rec = nrec;
+    const uint32_t zm = nzm;
+    if (bt + nw < bhi) {  // next batch's record, one batch ahead
+      nrec = __ldg(&it.rec[(bt + nw) * 32 + lane]);
+      nzm = __ldg(&it.zm[(bt + nw) * 32 + lane]);
+    }
+    const int node = static_cast<int>(static_cast<uint32_t>(rec));
+    const uint32_t w = static_cast<uint32_t>(rec >> 32);
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+    const int L = node >= 0 ? (w >> 3) & 15 : 0;
+    const bool edge = (w >> 7) & 1;
+    // the head's own node: info, current y and x, loaded before the compute (no other thread of
+    // this kernel writes this node's y)
+    uint32_t inf = 0;
+    double yn[3] = {0.0, 0.0, 0.0}, xn3[3] = {0.0, 0.0, 0.0};
+    if (L > 0) {
+      inf = __ldg(&info[node]);
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        double s = 0.0;
-#pragma unroll
-        for (int q = 0; q < 24; ++q) s = fma(Ks[q][a][ln], xv[q], s);
-        r[a] = dE * s;
+        if (!edge) yn[a] = y[3 * (int64_t)node + a];
+        if (DOT || edge) xn3[a] = __ldg(&x[3 * (int64_t)node + a]);
       }
     }
-    const int L = t < it.n ? it.seg[t] : 0;
+    if (node >= 0) {
+      const int i = node % NX, rr = node / NX;
+      const int j = rr % NY, k = rr / NY;
+      const int o = w & 7;
+      const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+      const int ln = local_node(1 - ox, 1 - oy, 1 - oz);
+      const int e0 = (i - 1 + ox) + NX * (j - 1 + oy) + NXY * (k - 1 + oz);  // may lie outside (masked)
+      double xv[24];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {  // a node's 24-byte record in two requests: 16 B aligned + 8 B
+        const int nd = e0 + corner_x(m) + NX * corner_y(m) + NXY * (m >> 2);
+        const uint32_t zb = (zm >> (3 * m)) & 7;
+        const int a0 = zb == 7 ? 0 : 3 * nd;  // all-zero corners (outside) read a safe address
+        const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);  // 16 B-aligned pair
+        const double2 pr = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
+        const double sg = __ldg(x + (odd ? a0 : a0 + 2));
+        const double c0 = odd ? sg : pr.x, c1 = odd ? pr.x : pr.y, c2 = odd ? pr.y : sg;
+        xv[3 * m + 0] = (zb & 1) ? 0.0 : c0;
+        xv[3 * m + 1] = (zb & 2) ? 0.0 : c1;
+        xv[3 * m + 2] = (zb & 4) ? 0.0 : c2;
+      }
+#pragma unroll
+      for (int q = 0; q < 24; ++q) {
+        r0 = fma(Ks[q][0][ln], xv[q], r0);
+        r1 = fma(Ks[q][1][ln], xv[q], r1);
+        r2 = fma(Ks[q][2][ln], xv[q], r2);
+      }
+      const double dE = Es[(w >> 8) & 31] - Es[(w >> 13) & 31];
+      r0 *= dE;
+      r1 *= dE;
+      r2 *= dE;
+    }
 #pragma unroll
     for (int d = 1; d < 8; ++d) {
-      const double v0 = __shfl_down_sync(0xffffffffu, r[0], d);
-      const double v1 = __shfl_down_sync(0xffffffffu, r[1], d);
-      const double v2 = __shfl_down_sync(0xffffffffu, r[2], d);
-      if (d < L) {  // segments never cross the warp, so lane + d < 32 here
-        r[0] += v0;
-        r[1] += v1;
-        r[2] += v2;
+      const double v0 = __shfl_down_sync(0xffffffffu, r0, d);
+      const double v1 = __shfl_down_sync(0xffffffffu, r1, d);
+      const double v2 = __shfl_down_sync(0xffffffffu, r2, d);
+      if (d < L) {  // segments never cross the batch, so lane + d < 32 here
+        r0 += v0;
+        r1 += v1;
+        r2 += v2;
       }
     }
-    if (L > 0 && node >= 0) {
-      (void)lane;
-      const uint8_t inf = __ldg(&info[node]);
+    if (L > 0) {
+      const double rr3[3] = {r0, r1, r2};
       double* yo = y + 3 * (int64_t)node;
-      const double* xn = x + 3 * (int64_t)node;
-      if (it.mode[t]) {
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const double xa = xn[a];
-          const double ya = ((inf >> a) & 1) ? xa : r[a];
+      for (int a = 0; a < 3; ++a) {
+        const bool con = (inf >> a) & 1;
+        if (edge) {  // edge column: the whole row sum, written
+          const double ya = con ? xn3[a] : rr3[a];
           yo[a] = ya;
-          if constexpr (DOT) dsum = fma(xa, ya, dsum);
+          if constexpr (DOT) dsum = fma(xn3[a], ya, dsum);
+        } else if (!con) {
+          yo[a] = yn[a] + rr3[a];
+          if constexpr (DOT) dsum = fma(xn3[a], rr3[a], dsum);
         }
-      } else {
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-          if (!((inf >> a) & 1)) {
-            yo[a] += r[a];
-            if constexpr (DOT) dsum = fma(xn[a], r[a], dsum);
-          }
       }
     }
   }
@@ -810,6 +833,23 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
       for (int dx = -1; dx <= 1; ++dx) std::memcpy(P.HYZ[sy][sz][dx + 1], fam[(dx + 1) + 3 + 9], 9 * 8);
     }
 
+  // z chunks: one full wave of resident CTAs when tiles allow it
+  static bool attrs = false;
+  if (!attrs) {
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
+    attrs = true;
+  }
+  int occ = 1;
+  AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<true, false>, NT, kMainSmem));
+  const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
+  const int64_t tiles = (int64_t)(P.NXm / TXN) * ((P.NY + TY - 1) / TY);
+  int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
+  chunks = std::min(chunks, std::max(1, P.NZ / 8));
+  plan->kchunk = (P.NZ + chunks - 1) / chunks;
+  plan->nchunks = (P.NZ + plan->kchunk - 1) / plan->kchunk;
   const int64_t nn = s.n_nodes;
   plan->info.alloc(nn + 4);  // +4: the main kernel copies the aligned 4-byte word holding a node's byte
   AFEM_CK(cudaMemsetAsync(plan->info.p, 0, nn + 4, c.stream));
@@ -933,86 +973,75 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
     AFEM_CK(cudaStreamSynchronize(c.stream));
     for (const NodeMask& nm : list) (nm.edge ? plan->n_edge_nodes : plan->n_fix_nodes) += 1;
 
-    // k_stencil_items keeps the edge columns only when they are wider than the tile halo.
-    std::vector<int32_t> inode;
-    std::vector<uint8_t> ioct, iseg, imode;
-    std::vector<uint32_t> izm;
-    std::vector<double> idE;
-    auto pad = [&] {
-      inode.push_back(-1); ioct.push_back(0); iseg.push_back(0); imode.push_back(0); izm.push_back(0);
-      idE.push_back(0.0);
-    };
+    // k_stencil_items: every item of a mixed-family node (and of the edge columns, unless the
+    // in-tile variant writes them), ordered (x tile, y tile, plane, node, octant); padded so that no
+    // node's items straddle a 32-item batch.
+    const int ntyc = (P.NY + TY - 1) / TY;
+    struct TItem { uint64_t key; uint64_t rec; uint32_t zm; };
+    std::vector<TItem> ti;
     for (const NodeMask& nm : list) {
       if (plan->fuse_items ? (!nm.edge || plan->edge_fused) : false) continue;
-      const int L = __builtin_popcount(nm.mask);
-      if (L == 0) continue;
-      if ((inode.size() % 32) + L > 32)
-        while (inode.size() % 32) pad();  // a node's items never cross a warp
-      const double Eb = nm.edge ? 0.0 : P.E[hinfo[nm.node] >> 3];
       const int ni = static_cast<int>(nm.node % P.NX);
       const int64_t nr = nm.node / P.NX;
       const int nj = static_cast<int>(nr % P.NY), nk = static_cast<int>(nr / P.NY);
-      bool head = true;
+      const uint64_t lid = ((uint64_t)(ni / TXN) * ntyc + nj / TY) * P.NZ + nk;
+      const uint64_t phb = nm.edge ? static_cast<uint64_t>(kVoid) : static_cast<uint64_t>(hinfo[nm.node] >> 3);
       for (int o = 0; o < 8; ++o) {
         if (!((nm.mask >> o) & 1)) continue;
-        // zero-input mask of the octant element's 8 nodes (outside the domain, or Dirichlet)
-        uint32_t zm = 0;
+        const uint64_t pho = static_cast<uint64_t>(oct_phase(nm.node, o));
+        const uint64_t rec = static_cast<uint64_t>(static_cast<uint32_t>(nm.node)) |
+                             (static_cast<uint64_t>(o) << 32) | ((nm.edge ? 1ull : 0ull) << 39) | (pho << 40) |
+                             (phb << 45);
+        uint32_t zm = 0;  // zero inputs: Dirichlet, or outside the domain
         const int ei = ni - 1 + (o & 1), ej = nj - 1 + ((o >> 1) & 1), ek = nk - 1 + (o >> 2);
         for (int m = 0; m < 8; ++m) {
           const int ii = ei + corner_x(m), jj = ej + corner_y(m), kk = ek + (m >> 2);
           const bool in = ii >= 0 && ii < P.NX && jj >= 0 && jj < P.NY && kk >= 0 && kk < P.NZ;
-          const uint32_t bits = in ? (hinfo[ii + (int64_t)P.NX * (jj + (int64_t)P.NY * kk)] & 7u) : 7u;
-          zm |= bits << (3 * m);
+          zm |= (in ? (hinfo[ii + (int64_t)P.NX * (jj + (int64_t)P.NY * kk)] & 7u) : 7u) << (3 * m);
         }
-        inode.push_back(static_cast<int32_t>(nm.node));
-        ioct.push_back(static_cast<uint8_t>(o));
-        iseg.push_back(head ? static_cast<uint8_t>(L) : 0);
-        imode.push_back(nm.edge ? 1 : 0);
-        izm.push_back(zm);
-        idE.push_back(P.E[oct_phase(nm.node, o)] - Eb);
-        head = false;
+        ti.push_back({(lid << 36) | ((uint64_t)(nj % TY) * TXN + ni % TXN) << 3 | static_cast<uint64_t>(o), rec, zm});
       }
     }
-    while (inode.size() % 32) pad();
-    const size_t n = inode.size();
-    plan->n_items = static_cast<int64_t>(n);
-    if (n) {
-      plan->it_node.alloc(n);
-      plan->it_oct.alloc(n);
-      plan->it_seg.alloc(n);
-      plan->it_mode.alloc(n);
-      plan->it_zmask.alloc(n);
-      plan->it_dE.alloc(n);
-      AFEM_CK(cudaMemcpyAsync(plan->it_node.p, inode.data(), n * 4, cudaMemcpyHostToDevice, c.stream));
-      AFEM_CK(cudaMemcpyAsync(plan->it_oct.p, ioct.data(), n, cudaMemcpyHostToDevice, c.stream));
-      AFEM_CK(cudaMemcpyAsync(plan->it_seg.p, iseg.data(), n, cudaMemcpyHostToDevice, c.stream));
-      AFEM_CK(cudaMemcpyAsync(plan->it_mode.p, imode.data(), n, cudaMemcpyHostToDevice, c.stream));
-      AFEM_CK(cudaMemcpyAsync(plan->it_zmask.p, izm.data(), n * 4, cudaMemcpyHostToDevice, c.stream));
-      AFEM_CK(cudaMemcpyAsync(plan->it_dE.p, idE.data(), n * 8, cudaMemcpyHostToDevice, c.stream));
-      AFEM_CK(cudaStreamSynchronize(c.stream));
+    std::sort(ti.begin(), ti.end(), [](const TItem& a, const TItem& b) { return a.key < b.key; });
+    std::vector<uint64_t> trec;
+    std::vector<uint32_t> tzm;
+    for (size_t q2 = 0; q2 < ti.size();) {
+      size_t e = q2;  // segment: one target node
+      while (e < ti.size() && static_cast<uint32_t>(ti[e].rec) == static_cast<uint32_t>(ti[q2].rec)) ++e;
+      const uint64_t L = e - q2;
+      if ((trec.size() % 32) + L > 32)
+        while (trec.size() % 32) {
+          trec.push_back(kPadRec);
+          tzm.push_back(0);
+        }
+      for (size_t t = q2; t < e; ++t) {
+        trec.push_back(ti[t].rec | (t == q2 ? (L << 35) : 0ull));
+        tzm.push_back(ti[t].zm);
+      }
+      q2 = e;
     }
+    while (trec.size() % 32) {
+      trec.push_back(kPadRec);
+      tzm.push_back(0);
+    }
+    plan->n_items = static_cast<int64_t>(trec.size());
+    plan->it_rec.alloc(std::max<size_t>(trec.size(), 1));
+    plan->it_zm.alloc(std::max<size_t>(tzm.size(), 1));
+    if (!trec.empty()) {
+      AFEM_CK(cudaMemcpyAsync(plan->it_rec.p, trec.data(), trec.size() * 8, cudaMemcpyHostToDevice, c.stream));
+      AFEM_CK(cudaMemcpyAsync(plan->it_zm.p, tzm.data(), tzm.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    }
+    AFEM_CK(cudaStreamSynchronize(c.stream));
   }
-  // z chunks: one full wave of resident CTAs when tiles allow it
-  static bool attrs = false;
-  if (!attrs) {
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
-    attrs = true;
-  }
-  int occ = 1;
-  AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<true, false>, NT, kMainSmem));
-  const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
-  const int64_t tiles = (int64_t)(P.NXm / TXN) * ((P.NY + TY - 1) / TY);
-  int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
-  chunks = std::min(chunks, std::max(1, P.NZ / 8));
-  plan->kchunk = (P.NZ + chunks - 1) / chunks;
-  plan->nchunks = (P.NZ + plan->kchunk - 1) / plan->kchunk;
-  plan->item_blocks = static_cast<int>(grid_for(std::max<int64_t>(plan->n_items, 1), kItemThreads, 4 * c.num_sms));
   const int64_t nb_main = (int64_t)(P.NXm / TXN) * ((P.NY + TY - 1) / TY) * plan->nchunks;
   plan->part_main.alloc(std::max<int64_t>(nb_main, 1));
+  int iocc = 1;  // one wave of resident item CTAs, each walking one contiguous range
+  AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&iocc, k_stencil_items<true>, kItemThreads, 0));
+  plan->item_blocks = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(plan->n_items / 256, (int64_t)std::max(iocc, 1) * c.num_sms)));
   plan->part_items.alloc(plan->item_blocks);
+  plan->Ed.alloc(32);
+  AFEM_CK(cudaMemcpyAsync(plan->Ed.p, P.E, 32 * 8, cudaMemcpyHostToDevice, c.stream));
   plan->counter.alloc(1);
   AFEM_CK(cudaMemsetAsync(plan->counter.p, 0, sizeof(unsigned), c.stream));
   AFEM_CK(cudaStreamSynchronize(c.stream));
@@ -1036,12 +1065,12 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, 
     }
   }
   if (pl.n_items > 0) {
-    const Items it{pl.it_node.p, pl.it_oct.p, pl.it_seg.p, pl.it_mode.p, pl.it_zmask.p, pl.it_dE.p, pl.n_items};
+    const Items it{pl.it_rec.p, pl.it_zm.p, pl.n_items};
     if (dot_out)
-      launch(c, k_stencil_items<true>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, P.NZ, pl.Kg.p, x, pl.info.p, it,
-             y, dot);
+      launch(c, k_stencil_items<true>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.Kg.p, pl.Ed.p, x, pl.info.p,
+             it, y, dot);
     else
-      launch(c, k_stencil_items<false>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, P.NZ, pl.Kg.p, x, pl.info.p,
+      launch(c, k_stencil_items<false>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.Kg.p, pl.Ed.p, x, pl.info.p,
              it, y, dot);
   }
 }

@@ -98,5 +98,5 @@ def test_nccl_backend_single_rank(afem):
     dop = d.matrix_free_operator(sys_, sys_.impose_dirichlet(np.zeros(sys_.n)))
     assert rel_err(dop.apply(x), op.apply(x)) <= 1e-12
     xs, rep = d.run_solver(dop, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
-    assert rep["converged"] and abs(rep["iterations"] - rg["iterations"]) <= 2
+    assert rep["converged"] and abs(rep["iterations"] - rg["iterations"]) <= max(2, rg["iterations"] // 100), (rep, rg)
     assert rel_err(xs, xg) <= 1e-8
