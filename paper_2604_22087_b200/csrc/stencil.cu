@@ -60,13 +60,6 @@ struct StencilPlan {
   DevArray<uint32_t> it_zm;
   DevArray<double> Ed;   // modulus per phase code (32), device copy for the item kernel
   int item_blocks = 1;
-  // in-tile correction lists (k_stencil_main)
-  DevArray<int32_t> c_ptr;
-  DevArray<uint32_t> c_word;
-  DevArray<double> c_coef;
-  int64_t n_citems = 0;
-  int edge_fused = 0;
-  int fuse_items = 0;
   DevArray<double> part_main, part_items;  // fused p.Ap partials (main kernel, item kernel)
   DevArray<unsigned int> counter;
   DevArray<double> Kg;   // Khat (row-major 24 x 24) in global memory for the correction kernels
@@ -207,39 +200,20 @@ struct DotArgs {
   int n_main;  // number of main-kernel partials (read by the items kernel's last block)
 };
 
-// In-tile correction items (see make_stencil_plan): CSR over (x tile, row j, element layer l)
-// lists; item word = tcol (7 bits) | flag << 7 (0: target on the layer's lower plane, 1: upper) |
-// octant << 8 | mode << 11 (0: owned node, add to its accumulator; 1: edge node, first write;
-// 2: edge node, add; 3: padding) | seg << 13 (segment length at the head, 0 elsewhere).
-// coef: dE / E_base for owned targets (the accumulator is scaled by E_base at finalisation), dE
-// for edge targets (written to y directly).
-struct CorrArgs {
-  const int32_t* ptr;
-  const uint32_t* word;
-  const double* coef;
-  const double* Kg;  // Khat row-major (24 x 24)
-  int edge_col;      // 1: the single edge column i = NXm is handled here (right halo of the last tile)
-};
+constexpr int RING = 4;  // plane slots: p (computing), p+1 (landed), p+2 (in flight), one spare
+constexpr size_t kMainSmem = sizeof(double) * RING * (TY + 2) * RS + sizeof(uint32_t) * RING * NT * 4;
 
-constexpr int RING = 3;  // plane slots: p-1, p (both read by the correction phase), p+1 (landing)
-constexpr size_t kMainSmem = sizeof(double) * (RING * (TY + 2) * RS + TY * 2 * TXN * 3 + 576) +
-                             sizeof(uint32_t) * RING * NT * 4;
-
-// OCC: resident CTAs per SM the register budget is sized for (2: 128 regs, 3: 80 regs).
-// CORR: the in-tile correction phase (opt-in, AFEM_STENCIL_FUSE_ITEMS=1).
-template <bool DOT, bool CORR>
+// DOT: also emit the block partial of x.y (the CG p^T A p).
+template <bool DOT>
 __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ StencilParams P,
                                                         const double* __restrict__ x,
                                                         const uint8_t* __restrict__ info, double* __restrict__ y,
-                                                        int kchunk, DotArgs dot, CorrArgs cr) {
+                                                        int kchunk, DotArgs dot) {
   double dsum = 0.0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double (*sm)[TY + 2][RS] = reinterpret_cast<double (*)[TY + 2][RS]>(smem_raw);
-  double (*cbuf)[2][TXN][3] = reinterpret_cast<double (*)[2][TXN][3]>(smem_raw + sizeof(double) * RING * (TY + 2) * RS);
-  double (*Ks)[3][8] =
-      reinterpret_cast<double (*)[3][8]>(smem_raw + sizeof(double) * (RING * (TY + 2) * RS + TY * 2 * TXN * 3));
-  uint32_t (*sinfo)[NT][4] = reinterpret_cast<uint32_t (*)[NT][4]>(
-      smem_raw + sizeof(double) * (RING * (TY + 2) * RS + TY * 2 * TXN * 3 + 576));
+  uint32_t (*sinfo)[NT][4] =
+      reinterpret_cast<uint32_t (*)[NT][4]>(smem_raw + sizeof(double) * RING * (TY + 2) * RS);
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int NX = P.NX, NY = P.NY, NZ = P.NZ;
   const int i0 = blockIdx.x * TXN, j0 = blockIdx.y * TY;
@@ -249,17 +223,12 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
   const int yf = j == 0 ? 1 : (j == NY - 1 ? 2 : 0);
   const int64_t plane = (int64_t)NX * NY;
 
-  for (int t = threadIdx.x; t < 576; t += NT) {  // Ks[q][a][ln] = Khat[3 ln + a][q]
-    const int r = t / 24, q = t % 24;
-    Ks[q][r % 3][r / 3] = __ldg(&cr.Kg[t]);
-  }
-  for (int t = threadIdx.x; t < TY * 2 * TXN * 3; t += NT) (&cbuf[0][0][0][0])[t] = 0.0;
-
   // Plane staging with cp.async (LDGSTS): no registers held across the compute; out-of-domain
   // nodes are zero-filled (src-size 0); Dirichlet masks are applied to the thread's own slots after
   // the wait, before the block barrier. Slots (warp-row mapping): s0/s1/s2 = row ty, columns lane,
   // lane+32, lane+64 (< 66); s3 = rows 8-9 spread over the block. The info byte of each slot's node
   // travels the same way (the aligned 4-byte word holding it, into private shared words).
+  // Plane p lives in ring slot (p + 1) % RING; two planes are in flight while one is computed.
   const int lane = tx;
   const int q3 = ty * 32 + lane;
   const int r3 = TY + q3 / (TXN + 2), c3 = q3 % (TXN + 2);
@@ -275,11 +244,12 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
   };
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(&sm[0][0][0]));
   const uint32_t ibase = static_cast<uint32_t>(__cvta_generic_to_shared(&sinfo[0][threadIdx.x][0]));
-  uint32_t sel = 0;
-  auto fetch = [&](int p, int buf) {
+  auto ring = [](int p) { return (p + 1) & (RING - 1); };
+  auto fetch = [&](int p) -> uint32_t {  // returns the slot selector bits needed to land plane p
+    const int buf = ring(p);
     const bool inplane = p >= 0 && p < NZ;
     const int64_t pb = plane * (inplane ? p : 0);
-    sel = 0;
+    uint32_t sel = 0;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       int r, col;
@@ -303,9 +273,10 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
       sel |= (ok ? static_cast<uint32_t>(node & 3) : 4u) << (4 * s);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
+    return sel;
   };
-  auto land = [&](int buf) {  // wait for own copies, apply own masks
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  auto land = [&](int p, uint32_t sel) {  // own copies of plane p are complete: apply own masks
+    const int buf = ring(p);
     double* sb = &sm[buf][0][0];
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
@@ -328,38 +299,15 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int a = 0; a < 3; ++a) acc[n][r][a] = 0.0;
-  fetch(k0 - 1, 0);
-  land(0);
+  const uint32_t sel0 = fetch(k0 - 1);
+  uint32_t sel1 = fetch(k0);
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  land(k0 - 1, sel0);
   __syncthreads();
-  // Item metadata of the layer processed at step p is prefetched one step earlier (bounds and the
-  // first batch's word/coef), so its load latency hides behind a plane of stencil work.
-  const int lo_p = max(k0, 1), hi_p = min(k1, NZ - 1);
-  auto item_prefetch = [&](int p, int& b0, int& b1, uint32_t& w, double& cf) {
-    b0 = b1 = 0;
-    w = 3u << 11;
-    cf = 0.0;
-    if (CORR && active && p >= lo_p && p <= hi_p) {
-      const int lid = (blockIdx.x * NY + j) * (NZ - 1) + (p - 1);
-      b0 = __ldg(&cr.ptr[lid]);
-      b1 = __ldg(&cr.ptr[lid + 1]);
-      if (b0 + lane < b1) {
-        w = __ldg(&cr.word[b0 + lane]);
-        cf = __ldg(&cr.coef[b0 + lane]);
-      }
-    }
-  };
-  int nb0, nb1;
-  uint32_t nw;
-  double ncf;
-  item_prefetch(k0 - 1, nb0, nb1, nw, ncf);
-  int cur = 0;  // ring slot of plane p
   for (int p = k0 - 1; p <= k1; ++p) {
-    const int nxt = cur == RING - 1 ? 0 : cur + 1, prv = cur == 0 ? RING - 1 : cur - 1;
-    if (p < k1) fetch(p + 1, nxt);
-    const int b0 = nb0, b1 = nb1;
-    const uint32_t w0 = nw;
-    const double cf0 = ncf;
-    item_prefetch(p + 1, nb0, nb1, nw, ncf);
+    uint32_t sel2 = 0;
+    if (p + 2 <= k1) sel2 = fetch(p + 2);
+    else asm volatile("cp.async.commit_group;\n" ::: "memory");
     const int64_t onode = i + (int64_t)NX * (active ? j : 0) + plane * max(p - 1, 0);
     const uint8_t oi0 = __ldg(&info[onode]), oi1 = __ldg(&info[onode + 1]);
     double xo[6];  // the finishing nodes' raw inputs (Dirichlet rows; the fused dot), issued early
@@ -369,91 +317,10 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
     }
     if (active && p >= 0 && p < NZ) {
       const int zc = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
-      const double* s = &sm[cur][0][0];
+      const double* s = &sm[ring(p)][0][0];
       if (yf == 0) plane_dispatch<0>(P, s, tx, ty, zc, acc);
       else if (yf == 1) plane_dispatch<1>(P, s, tx, ty, zc, acc);
       else plane_dispatch<2>(P, s, tx, ty, zc, acc);
-    }
-    // ---- correction items of the element layer (p-1, p): both planes are resident
-    if (CORR && active && p >= lo_p && p <= hi_p) {
-      if (b1 > b0) {  // warp-uniform
-        const double* slo = &sm[prv][0][0];
-        const double* shi = &sm[cur][0][0];
-        for (int base = b0; base < b1; base += 32) {
-          const int t = base + lane;
-          const bool first = base == b0;
-          const uint32_t w = first ? w0 : (t < b1 ? __ldg(&cr.word[t]) : (3u << 11));
-          const int tcol = w & 127, flag = (w >> 7) & 1, o = (w >> 8) & 7, mode = (w >> 11) & 3, L = w >> 13;
-          // chunk ends: lower-plane targets below k0 and upper-plane targets at k1 belong to neighbours
-          const bool skip = mode == 3 || (flag == 0 && p - 1 < k0) || (flag == 1 && p >= k1);
-          double r0 = 0.0, r1 = 0.0, r2 = 0.0;
-          if (!skip) {
-            const int ox = o & 1, oy = (o >> 1) & 1;
-            const int ln = local_node(1 - ox, 1 - oy, 1 - (o >> 2));
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {  // element corner m: row ty+oy+my, col tcol+ox+mx, plane mz
-              const double* sp = ((m >> 2) ? shi : slo) + (ty + oy + corner_y(m)) * RS + 3 * (tcol + ox + corner_x(m));
-#pragma unroll
-              for (int b = 0; b < 3; ++b) {
-                const double xv = sp[b];
-                r0 = fma(Ks[3 * m + b][0][ln], xv, r0);
-                r1 = fma(Ks[3 * m + b][1][ln], xv, r1);
-                r2 = fma(Ks[3 * m + b][2][ln], xv, r2);
-              }
-            }
-            const double cf = first ? cf0 : __ldg(&cr.coef[t]);
-            r0 *= cf;
-            r1 *= cf;
-            r2 *= cf;
-          }
-#pragma unroll
-          for (int d = 1; d < 4; ++d) {  // segments (<= 4 octants of one layer) never cross the warp
-            const double v0 = __shfl_down_sync(0xffffffffu, r0, d);
-            const double v1 = __shfl_down_sync(0xffffffffu, r1, d);
-            const double v2 = __shfl_down_sync(0xffffffffu, r2, d);
-            if (d < L) {
-              r0 += v0;
-              r1 += v1;
-              r2 += v2;
-            }
-          }
-          if (L > 0 && !skip) {
-            if (mode == 0) {
-              cbuf[ty][flag][tcol][0] = r0;
-              cbuf[ty][flag][tcol][1] = r1;
-              cbuf[ty][flag][tcol][2] = r2;
-            } else {  // edge node i0 + tcol on plane p-1+flag: y written (mode 1) or accumulated (mode 2)
-              const int64_t en = i0 + tcol + (int64_t)NX * j + plane * (p - 1 + flag);
-              const uint8_t inf = __ldg(&info[en]);
-              const double rr[3] = {r0, r1, r2};
-#pragma unroll
-              for (int a = 0; a < 3; ++a) {
-                const double xa = x[3 * en + a];
-                const bool con = (inf >> a) & 1;
-                if (mode == 1) {
-                  const double ya = con ? xa : rr[a];
-                  y[3 * en + a] = ya;
-                  if constexpr (DOT) dsum = fma(xa, ya, dsum);
-                } else if (!con) {
-                  y[3 * en + a] += rr[a];
-                  if constexpr (DOT) dsum = fma(xa, rr[a], dsum);
-                }
-              }
-            }
-          }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int n = 0; n < 2; ++n)
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            acc[n][0][a] += cbuf[ty][0][2 * tx + n][a];
-            acc[n][1][a] += cbuf[ty][1][2 * tx + n][a];
-            cbuf[ty][0][2 * tx + n][a] = 0.0;
-            cbuf[ty][1][2 * tx + n][a] = 0.0;
-          }
-        __syncwarp();
-      }
     }
     if (active && p - 1 >= k0) {  // nodes (i, j, p-1) and (i+1, j, p-1) are complete
       const double E0 = P.E[oi0 >> 3], E1 = P.E[oi1 >> 3];
@@ -481,9 +348,12 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
         acc[n][1][a] = acc[n][2][a];
         acc[n][2][a] = 0.0;
       }
-    if (p < k1) land(nxt);
+    if (p < k1) {
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // plane p+1 landed (p+2 may be in flight)
+      land(p + 1, sel1);
+    }
     __syncthreads();
-    cur = nxt;
+    sel1 = sel2;
   }
   if constexpr (DOT) {
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -497,8 +367,6 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
     }
   }
 }
-
-
 
 // Correction items: one thread per (node, octant) pair. y_n receives dE * Khat_rows(o) x_e(o) with
 // dE = E[octant phase] - E[base phase] (the base of an edge-column node is void, E = 0, and its
@@ -836,14 +704,12 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   // z chunks: one full wave of resident CTAs when tiles allow it
   static bool attrs = false;
   if (!attrs) {
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
     attrs = true;
   }
   int occ = 1;
-  AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<true, false>, NT, kMainSmem));
+  AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<true>, NT, kMainSmem));
   const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
   const int64_t tiles = (int64_t)(P.NXm / TXN) * ((P.NY + TY - 1) / TY);
   int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
@@ -895,82 +761,6 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
         }
     std::sort(list.begin(), list.end(), [](const NodeMask& a, const NodeMask& b) { return a.node < b.node; });
 
-    // In-tile lists for k_stencil_main: every correction of a mixed-family node, and (when the edge
-    // is the single column i = NXm, the last tile's right halo) every octant of the edge nodes.
-    // One segment per (target, element layer); CSR over (x tile, row, layer); padded so no segment
-    // crosses a 32-item batch of its list.
-    // Default: corrections run in k_stencil_items (measured faster: ~7 items per warp-step leave
-    // the in-tile batches mostly idle). AFEM_STENCIL_FUSE_ITEMS=1 selects the in-tile variant.
-    const char* fenv = std::getenv("AFEM_STENCIL_FUSE_ITEMS");
-    plan->fuse_items = (fenv && fenv[0] == '1') ? 1 : 0;
-    plan->edge_fused = (plan->fuse_items && P.NX - P.NXm == 1 && P.NXm > 0) ? 1 : 0;
-    const int ntx = P.NXm / TXN;
-    const int64_t nlist = (int64_t)std::max(ntx, 1) * P.NY * std::max(P.NZ - 1, 1);
-    struct CItem { int64_t lid; uint32_t key; uint32_t word; double coef; };  // key orders (flag, tcol, o)
-    std::vector<CItem> ci;
-    bool base_ok = true;
-    for (const NodeMask& nm : list) {
-      if (!plan->fuse_items) break;
-      if (nm.edge && !plan->edge_fused) continue;
-      const int ni = static_cast<int>(nm.node % P.NX);
-      const int64_t nr = nm.node / P.NX;
-      const int nj = static_cast<int>(nr % P.NY), nk = static_cast<int>(nr / P.NY);
-      const int tile = nm.edge ? ntx - 1 : ni / TXN;
-      const int tcol = ni - tile * TXN;  // 0..63 owned, 64 the edge column
-      const double Eb = nm.edge ? 0.0 : P.E[hinfo[nm.node] >> 3];
-      if (!nm.edge && !(Eb != 0.0)) base_ok = false;
-      for (int o = 0; o < 8; ++o) {
-        if (!((nm.mask >> o) & 1)) continue;
-        const int oz = o >> 2;
-        const int layer = nk - 1 + oz;     // element between planes layer and layer+1
-        const uint32_t flag = oz ? 0u : 1u;  // target on the layer's lower (0) or upper (1) plane
-        uint32_t mode = 0;
-        if (nm.edge) mode = (flag == 1 || nk == 0) ? 1u : 2u;  // first touch writes, second adds
-        const double dEo = P.E[oct_phase(nm.node, o)] - Eb;
-        const double coef = nm.edge ? dEo : dEo / Eb;
-        const int64_t lid = ((int64_t)tile * P.NY + nj) * (P.NZ - 1) + layer;
-        const uint32_t word = static_cast<uint32_t>(tcol) | (flag << 7) | (static_cast<uint32_t>(o) << 8) | (mode << 11);
-        ci.push_back({lid, (flag << 16) | (static_cast<uint32_t>(tcol) << 3) | static_cast<uint32_t>(o), word, coef});
-      }
-    }
-    if (!base_ok) return nullptr;
-    std::sort(ci.begin(), ci.end(), [](const CItem& a, const CItem& b) {
-      return a.lid != b.lid ? a.lid < b.lid : a.key < b.key;
-    });
-    std::vector<int32_t> cptr(nlist + 1, 0);
-    std::vector<uint32_t> cword;
-    std::vector<double> ccoef;
-    size_t q = 0;
-    for (int64_t lid = 0; lid < nlist; ++lid) {
-      cptr[lid] = static_cast<int32_t>(cword.size());
-      const size_t lstart = cword.size();
-      while (q < ci.size() && ci[q].lid == lid) {
-        size_t e = q;  // segment: same target (flag, tcol)
-        while (e < ci.size() && ci[e].lid == lid && (ci[e].key >> 3) == (ci[q].key >> 3)) ++e;
-        const uint32_t L = static_cast<uint32_t>(e - q);
-        if (((cword.size() - lstart) % 32) + L > 32)
-          while ((cword.size() - lstart) % 32) {
-            cword.push_back(3u << 11);
-            ccoef.push_back(0.0);
-          }
-        for (size_t t = q; t < e; ++t) {
-          cword.push_back(ci[t].word | (t == q ? (L << 13) : 0u));
-          ccoef.push_back(ci[t].coef);
-        }
-        q = e;
-      }
-    }
-    cptr[nlist] = static_cast<int32_t>(cword.size());
-    plan->c_ptr.alloc(nlist + 1);
-    AFEM_CK(cudaMemcpyAsync(plan->c_ptr.p, cptr.data(), cptr.size() * 4, cudaMemcpyHostToDevice, c.stream));
-    plan->n_citems = static_cast<int64_t>(cword.size());
-    plan->c_word.alloc(std::max<size_t>(cword.size(), 1));
-    plan->c_coef.alloc(std::max<size_t>(ccoef.size(), 1));
-    if (!cword.empty()) {
-      AFEM_CK(cudaMemcpyAsync(plan->c_word.p, cword.data(), cword.size() * 4, cudaMemcpyHostToDevice, c.stream));
-      AFEM_CK(cudaMemcpyAsync(plan->c_coef.p, ccoef.data(), ccoef.size() * 8, cudaMemcpyHostToDevice, c.stream));
-    }
-    AFEM_CK(cudaStreamSynchronize(c.stream));
     for (const NodeMask& nm : list) (nm.edge ? plan->n_edge_nodes : plan->n_fix_nodes) += 1;
 
     // k_stencil_items: every item of a mixed-family node (and of the edge columns, unless the
@@ -980,7 +770,6 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
     struct TItem { uint64_t key; uint64_t rec; uint32_t zm; };
     std::vector<TItem> ti;
     for (const NodeMask& nm : list) {
-      if (plan->fuse_items ? (!nm.edge || plan->edge_fused) : false) continue;
       const int ni = static_cast<int>(nm.node % P.NX);
       const int64_t nr = nm.node / P.NX;
       const int nj = static_cast<int>(nr % P.NY), nk = static_cast<int>(nr / P.NY);
@@ -1054,15 +843,9 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, 
   const dim3 grid(P.NXm / TXN, (P.NY + TY - 1) / TY, pl.nchunks);
   const int nb_main = P.NXm > 0 ? static_cast<int>(grid.x * grid.y * grid.z) : 0;
   const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main};
-  const CorrArgs cr{pl.c_ptr.p, pl.c_word.p, pl.c_coef.p, pl.Kg.p, pl.edge_fused};
   if (P.NXm > 0) {
-    if (pl.fuse_items) {
-      if (dot_out) launch(c, k_stencil_main<true, true>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
-      else launch(c, k_stencil_main<false, true>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
-    } else {
-      if (dot_out) launch(c, k_stencil_main<true, false>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
-      else launch(c, k_stencil_main<false, false>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot, cr);
-    }
+    if (dot_out) launch(c, k_stencil_main<true>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot);
+    else launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot);
   }
   if (pl.n_items > 0) {
     const Items it{pl.it_rec.p, pl.it_zm.p, pl.n_items};

@@ -48,8 +48,8 @@ def test_stencil_matches_oracle(afem, ctx, n):
     assert rel_err(op.diagonal(), o.mf_diagonal(u)) <= TOL
 
 
-# NX = nx+1 nodes: >= 65 runs the 64-wide main kernel; NX mod 64 == 1 fuses the edge column into it,
-# other remainders exercise the separate edge-item kernel; NX < 65 is edge-only.
+# NX = nx+1 nodes: >= 65 runs the 64-wide main kernel plus edge-column items (NX mod 64 of them);
+# NX < 65 is edge-only (every node through the correction-item kernel).
 @pytest.mark.parametrize("shape", [(64, 17, 20), (70, 9, 31), (64, 64, 7), (127, 12, 10), (128, 9, 17),
                                    (33, 17, 20), (31, 31, 31)])
 def test_stencil_matches_general_kernel(afem, ctx, shape):
@@ -74,18 +74,29 @@ def test_stencil_matches_general_kernel(afem, ctx, shape):
 
 
 @pytest.mark.parametrize("shape", [(64, 17, 20), (70, 9, 31)])
-def test_stencil_fused_corrections_variant(afem, ctx, shape, monkeypatch):
-    """The opt-in in-tile correction path (AFEM_STENCIL_FUSE_ITEMS=1) equals the default path."""
+def test_stencil_misaligned_device_input_and_determinism(afem, ctx, shape):
+    """Device inputs only 8-byte aligned (a tensor view at offset 1) give the same result as host
+    inputs (the correction kernel reads node records as 16 + 8 bytes), and repeated applies are
+    bitwise identical."""
+    import torch
     nx, ny, nz = shape
     s = grid(afem, ctx, nx, ny=ny, nz=nz, n_fibres=10, radius=0.1, seed=7)
     s.set_benchmark_dirichlet(0.02)
     u = s.impose_dirichlet(np.zeros(s.n))
-    x = random_vector(s.n, 1.0, 77)
-    y_default = afem.matrix_free_operator(s, u).apply(x)
-    monkeypatch.setenv("AFEM_STENCIL_FUSE_ITEMS", "1")
     op = afem.matrix_free_operator(s, u)
     assert op.uses_stencil
-    assert rel_err(op.apply(x), y_default) <= TOL
+    x = random_vector(s.n, 1.0, 77)
+    y_host = op.apply(x)
+    buf = torch.zeros(s.n + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = torch.from_numpy(x)
+    xd = buf[1:]
+    assert xd.data_ptr() % 16 == 8
+    torch.cuda.synchronize()
+    yd = torch.empty(s.n, dtype=torch.float64, device="cuda")
+    op.apply_device(xd.data_ptr(), yd.data_ptr())
+    ctx.synchronize()
+    assert np.array_equal(yd.cpu().numpy(), y_host)
+    assert np.array_equal(op.apply(x), y_host)
 
 
 def test_stencil_cg_matches_general_kernel_cg(afem, ctx):
