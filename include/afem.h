@@ -56,7 +56,10 @@ typedef struct afem_buffer_s* afem_buffer;
 typedef struct afem_op_s* afem_op;
 
 /* Material{model, E, nu} (material.hpp:15-27). model: 0 linear elastic (plane strain in 2D,
- * isotropic Hooke in 3D), 1 St Venant-Kirchhoff. sigma_y/hardening reserved for J2. */
+ * isotropic Hooke in 3D), 1 St Venant-Kirchhoff (material.hpp:49-69), and the north star's two
+ * laws the reference lacks: 2 compressible Neo-Hookean (psi = mu/2 (J^-2/3 I1 - 3) +
+ * kappa/2 (J-1)^2), 3 small-strain J2 plasticity with linear isotropic hardening (sigma_y,
+ * hardening; quadrature-point history resident on the device). */
 typedef struct {
   int32_t model;
   double E;
@@ -245,6 +248,17 @@ afem_status afem_solve_bvp(afem_system sys, const afem_newton_cfg* cfg, const do
 afem_status afem_load_stepping(afem_system sys, double total_strain, int32_t n_steps,
                                const afem_newton_cfg* cfg, double* u, int32_t* failed_step,
                                int32_t* converged, int32_t* step_iterations);
+
+/* ------------------------------------------------------------------ quadrature-point history (J2)
+ * The reference kernel has no state argument (element.hpp:68-70); J2 systems keep the committed
+ * history (plastic strain [xx,yy,zz,yz,xz,xy], alpha, pad: 8 doubles per Gauss point, element-major)
+ * resident on the device. Residuals, tangents and operators evaluate the return map from the
+ * committed history; afem_load_stepping commits after every converged step. */
+afem_status afem_history_size(afem_system sys, int64_t* n); /* doubles; 0 without a J2 phase */
+afem_status afem_history_commit(afem_system sys, const double* u);
+afem_status afem_history_reset(afem_system sys);
+afem_status afem_history_copy(afem_system sys, double* out);
+afem_status afem_history_set(afem_system sys, const double* in);
 
 /* ------------------------------------------------------------------ multi-GPU slab decomposition
  * (the reference has no distribution — the paper distributes only the PETSc solve,

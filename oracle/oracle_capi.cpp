@@ -122,9 +122,11 @@ static void* create(int32_t dim, int64_t n_nodes, int64_t n_elem, const double* 
     for (int i = 0; i < n_mat; ++i) {
       orc::Material m;
       m.model = mats[i].model; m.E = mats[i].E; m.nu = mats[i].nu;
+      m.sigma_y = mats[i].sigma_y; m.hardening = mats[i].hardening;
       s->materials.push_back(m);
     }
     s->batches = orc::build_batches(s->mesh, s->materials);
+    s->init_history();
     if (pattern) s->pattern = orc::precompute_sparsity(s->batches, s->n_dof(), dim);
     s->table = orc::constraint_table({}, s->n_dof(), dim);
     out = s.release();
@@ -192,8 +194,9 @@ int32_t orc_element_residual(void* sys, int64_t e, const double* ue, double* re)
     for (int k = 0; k < npe; ++k)
       for (int c = 0; c < D; ++c) xc[k * D + c] = s->mesh.coords[(size_t)s->mesh.conn[e * npe + k] * D + c];
     const orc::Material& m = s->materials.at(s->mesh.phase.at(e));
-    if (D == 2) orc::element_internal_force<2, double>(xc.data(), m, 2, ue, re);
-    else orc::element_internal_force<3, double>(xc.data(), m, 2, ue, re);
+    const double* h = s->history.empty() ? nullptr : s->history.data() + (size_t)e * s->nq() * orc::kHist;
+    if (D == 2) orc::element_internal_force<2, double>(xc.data(), m, 2, ue, re, h);
+    else orc::element_internal_force<3, double>(xc.data(), m, 2, ue, re, h);
   });
 }
 
@@ -351,9 +354,34 @@ int32_t orc_load_stepping(void* sys, double total_strain, int32_t n_steps, const
         std::memcpy(u, cur.data(), cur.size() * 8);
         return;
       }
+      // J2: the converged step becomes the committed history (not in the reference, which has no state)
+      if (s->dim() == 2) orc::commit_history<2>(*s, cur.data()); else orc::commit_history<3>(*s, cur.data());
     }
     *converged = 1;
     std::memcpy(u, cur.data(), cur.size() * 8);
+  });
+}
+
+int64_t orc_history_size(void* sys) { return (int64_t)S(sys)->history.size(); }
+
+int32_t orc_history_commit(void* sys, const double* u) {
+  return guarded([&] {
+    auto* s = S(sys);
+    if (s->dim() == 2) orc::commit_history<2>(*s, u); else orc::commit_history<3>(*s, u);
+  });
+}
+
+int32_t orc_history_copy(void* sys, double* out) {
+  return guarded([&] {
+    const auto& h = S(sys)->history;
+    std::memcpy(out, h.data(), h.size() * 8);
+  });
+}
+
+int32_t orc_history_set(void* sys, const double* in) {
+  return guarded([&] {
+    auto& h = S(sys)->history;
+    std::memcpy(h.data(), in, h.size() * 8);
   });
 }
 

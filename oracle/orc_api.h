@@ -35,13 +35,14 @@ enum {
   ORC_E_RUNTIME = 13
 };
 
-/* model: 0 linear elastic (plane strain in 2D), 1 St Venant-Kirchhoff (reference material.hpp:13) */
+/* model: 0 linear elastic (plane strain in 2D), 1 St Venant-Kirchhoff (reference material.hpp:13);
+ * restatement only (the reference has neither): 2 Neo-Hookean, 3 J2 plasticity (sigma_y, hardening). */
 typedef struct {
   int32_t model;
   double E;
   double nu;
-  double sigma_y;   /* reserved (J2) */
-  double hardening; /* reserved (J2) */
+  double sigma_y;   /* J2 */
+  double hardening; /* J2 */
 } orc_material;
 
 /* method: 0 CG, 1 GMRES, 2 BICGSTAB; precond: 0 NONE, 1 JACOBI (reference krylov.hpp:20-21, 43-55) */
@@ -138,6 +139,12 @@ int32_t orc_solve_bvp(void* sys, const orc_newton_cfg* cfg, const double* x0, do
 int32_t orc_load_stepping(void* sys, double total_strain, int32_t n_steps,
                           const orc_newton_cfg* cfg, double* u, int32_t* failed_step,
                           int32_t* converged, int32_t* step_iterations);
+
+/* ---- J2 quadrature-point history (restatement only): n_elem * nq * 8 doubles, element-id indexed */
+int64_t orc_history_size(void* sys);
+int32_t orc_history_commit(void* sys, const double* u);
+int32_t orc_history_copy(void* sys, double* out);
+int32_t orc_history_set(void* sys, const double* in);
 
 #ifdef __cplusplus
 }

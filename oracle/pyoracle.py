@@ -74,7 +74,9 @@ def materials_array(mats):
     arr = (orc_material * len(mats))()
     for i, m in enumerate(mats):
         model, E, nu = m[0], m[1], m[2]
-        arr[i] = orc_material(int(model), float(E), float(nu), 0.0, 0.0)
+        sy = float(m[3]) if len(m) > 3 else 0.0
+        hh = float(m[4]) if len(m) > 4 else 0.0
+        arr[i] = orc_material(int(model), float(E), float(nu), sy, hh)
     return arr
 
 
@@ -130,6 +132,12 @@ class Oracle:
         for k, v in sig.items():
             getattr(L, k).argtypes = v
             getattr(L, k).restype = C.c_int32
+        if kind == "restate":  # J2 history exists only in the restatement (the reference has no state)
+            L.orc_history_size.restype = C.c_int64
+            L.orc_history_size.argtypes = [vp]
+            for k in ("orc_history_commit", "orc_history_copy", "orc_history_set"):
+                getattr(L, k).argtypes = [vp, vp]
+                getattr(L, k).restype = C.c_int32
 
     def check(self, st):
         if st != 0:
@@ -327,3 +335,16 @@ class OracleSystem:
         self._c(self.o.lib.orc_load_stepping(self.h, total_strain, n_steps, C.byref(cfg), _p(u),
                                              C.byref(failed), C.byref(conv), _p(its, C.c_int32)))
         return u, dict(converged=bool(conv.value), failed_step=failed.value, step_iterations=its)
+
+    def history(self):
+        out = np.zeros(self.o.lib.orc_history_size(self.h))
+        self._c(self.o.lib.orc_history_copy(self.h, _p(out)))
+        return out
+
+    def set_history(self, h):
+        h = np.ascontiguousarray(h, np.float64)
+        self._c(self.o.lib.orc_history_set(self.h, _p(h)))
+
+    def commit_history(self, u):
+        u = np.ascontiguousarray(u, np.float64)
+        self._c(self.o.lib.orc_history_commit(self.h, _p(u)))

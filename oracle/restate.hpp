@@ -70,20 +70,42 @@ template <int L> inline Dual<L> operator/(const Dual<L>& a, const Dual<L>& b) {
 template <int L> inline Dual<L> operator/(const Dual<L>& a, double b) {
   const double inv = 1.0 / b; Dual<L> r(a.v * inv); for (int k = 0; k < L; ++k) r.d[k] = a.d[k] * inv; return r; }
 template <int L> inline Dual<L>& operator+=(Dual<L>& a, const Dual<L>& b) { a = a + b; return a; }
+// sqrt / pow(x, double) (dual.hpp:162-177): the only transcendental primitives the reference's Dual has.
+template <int L> inline Dual<L> sqrt(const Dual<L>& a) {
+  const double sv = std::sqrt(a.v);
+  Dual<L> r(sv);
+  const double g = 0.5 / sv;
+  for (int k = 0; k < L; ++k) r.d[k] = g * a.d[k];
+  return r;
+}
+template <int L> inline Dual<L> pow(const Dual<L>& a, double p) {
+  Dual<L> r(std::pow(a.v, p));
+  const double g = p * std::pow(a.v, p - 1.0);
+  for (int k = 0; k < L; ++k) r.d[k] = g * a.d[k];
+  return r;
+}
+inline double sqrt(double x) { return std::sqrt(x); }
+inline double pow(double x, double p) { return std::pow(x, p); }
 inline double value_of(double x) { return x; }
 template <int L> inline double value_of(const Dual<L>& x) { return x.v; }
 
 // ---------------------------------------------------------------- material (material.hpp:13-69)
-enum Model { LINEAR = 0, SVK = 1 };
+// NEOHOOKE and J2 are the north star's config-3/4 laws; the reference stops at SVK (material.hpp:13).
+enum Model { LINEAR = 0, SVK = 1, NEOHOOKE = 2, J2 = 3 };
+constexpr int kHist = 8;  // J2 history words per Gauss point: eps_p [xx,yy,zz,yz,xz,xy], alpha, pad
 struct Material {
   int model = LINEAR;
   double E = 1.0, nu = 0.3;
+  double sigma_y = 0.0, hardening = 0.0;  // J2 only
+  double kappa() const { return lambda() + 2.0 * mu() / 3.0; }
   double lambda() const { return E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)); }  // material.hpp:20
   double mu() const { return E / (2.0 * (1.0 + nu)); }                        // material.hpp:21
   void validate() const {                                                     // material.hpp:23-26
     if (!(E > 0.0)) throw std::invalid_argument("material: E must be > 0");
     if (!(nu > -1.0 && nu < 0.5)) throw std::invalid_argument("material: nu must be in (-1, 0.5)");
-    if (model != LINEAR && model != SVK) throw std::invalid_argument("material: unsupported model");
+    if (model < LINEAR || model > J2) throw std::invalid_argument("material: unsupported model");
+    if (model == J2 && !(sigma_y > 0.0 && hardening >= 0.0))
+      throw std::invalid_argument("material: J2 needs sigma_y > 0 and hardening >= 0");
   }
 };
 
@@ -141,12 +163,67 @@ inline void shape_grad(int dim, const GP& q, double dn[8][3]) {
 
 // ---------------------------------------------------------------- element kernel (element.hpp:68-125)
 // coords: npe*D doubles; u, out: ndpe values.
+// Small-strain J2 radial return at one Gauss point (the north star's config-4 law): committed
+// history h (kHist words, may be null = virgin), total strain eps (3x3, plane strain in 2D) ->
+// stress sig; h_new (may be null) receives the updated history. The yield test is decided on
+// values (like the reference's value-only comparisons, dual.hpp:137-160) and sqrt is taken only
+// on the plastic branch, so the AD tangent is the consistent tangent.
+template <class T>
+void j2_stress(const Material& mat, const T (&eps)[3][3], const double* h, T (&sig)[3][3], double* h_new) {
+  const double mu = mat.mu(), kappa = mat.kappa();
+  double ep[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, alpha = 0.0;
+  if (h) {
+    ep[0][0] = h[0]; ep[1][1] = h[1]; ep[2][2] = h[2];
+    ep[1][2] = ep[2][1] = h[3]; ep[0][2] = ep[2][0] = h[4]; ep[0][1] = ep[1][0] = h[5];
+    alpha = h[6];
+  }
+  T ee[3][3];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) ee[a][b] = eps[a][b] - ep[a][b];
+  const T tr = ee[0][0] + ee[1][1] + ee[2][2];
+  T str[3][3];
+  T ss(0.0);
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      str[a][b] = 2.0 * mu * (a == b ? ee[a][b] - tr / 3.0 : ee[a][b]);
+      ss += str[a][b] * str[a][b];
+    }
+  const T q2 = 1.5 * ss;
+  const double sY = mat.sigma_y + mat.hardening * alpha;
+  T fac(1.0);
+  double da_v = 0.0, q_v = 0.0;
+  if (value_of(q2) > sY * sY) {
+    const T q = sqrt(q2);
+    const T da = (q - sY) / (3.0 * mu + mat.hardening);
+    fac = 1.0 - 3.0 * mu * da / q;
+    da_v = value_of(da);
+    q_v = value_of(q);
+  }
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) sig[a][b] = a == b ? fac * str[a][b] + kappa * tr : fac * str[a][b];
+  if (h_new) {
+    double hn[kHist];
+    for (int k = 0; k < kHist; ++k) hn[k] = h ? h[k] : 0.0;
+    if (da_v > 0.0) {
+      const double f = da_v * 1.5 / q_v;
+      hn[0] += f * value_of(str[0][0]); hn[1] += f * value_of(str[1][1]); hn[2] += f * value_of(str[2][2]);
+      hn[3] += f * value_of(str[1][2]); hn[4] += f * value_of(str[0][2]); hn[5] += f * value_of(str[0][1]);
+      hn[6] += da_v;
+    }
+    for (int k = 0; k < kHist; ++k) h_new[k] = hn[k];
+  }
+}
+
+// hist: the element's committed Gauss-point history (nq * kHist words, J2 only; may be null).
+// hist_new: if non-null, receives the updated history (history commit; J2 only).
 template <int D, class T>
 void element_internal_force(const double* coords, const Material& mat, int gauss_points,
-                            const T* u, T* out) {
+                            const T* u, T* out, const double* hist = nullptr, double* hist_new = nullptr) {
+  int qi = -1;
   constexpr int npe = ET<D>::npe, nd = ET<D>::ndpe;
   for (int k = 0; k < nd; ++k) out[k] = T(0.0);
   for (const GP& gp : gauss_rule(D, gauss_points)) {
+    ++qi;
     double dn[8][3];
     shape_grad(D, gp, dn);
     double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
@@ -222,6 +299,61 @@ void element_internal_force(const double* coords, const Material& mat, int gauss
           out[3 * i + 2] += wdet * (g[i][0] * sxz + g[i][1] * syz + g[i][2] * szz);
         }
       }
+    } else if (mat.model == J2) {
+      T eps[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) eps[a][b] = T(0.0);
+      for (int a = 0; a < D; ++a)
+        for (int b = 0; b < D; ++b) {
+          T hab(0.0), hba(0.0);
+          for (int i = 0; i < npe; ++i) { hab += u[D * i + a] * g[i][b]; hba += u[D * i + b] * g[i][a]; }
+          eps[a][b] = 0.5 * (hab + hba);
+        }
+      T sig[3][3];
+      j2_stress<T>(mat, eps, hist ? hist + qi * kHist : nullptr, sig, hist_new ? hist_new + qi * kHist : nullptr);
+      for (int i = 0; i < npe; ++i)
+        for (int a = 0; a < D; ++a) {
+          T t(0.0);
+          for (int b = 0; b < D; ++b) t += sig[a][b] * g[i][b];
+          out[D * i + a] += wdet * t;
+        }
+    } else if (mat.model == NEOHOOKE) {
+      // psi = mu/2 (J^{-2/3} I1 - 3) + kappa/2 (J - 1)^2 (pow-only form: the reference's Dual has
+      // no log, dual.hpp:162-177). P = mu J^{-2/3} F - (mu/3) I1 J^{-5/3} cof F + kappa (J-1) cof F.
+      // Plane strain in 2D: F33 = 1.
+      T F[3][3];
+      for (int a = 0; a < D; ++a)
+        for (int b = 0; b < D; ++b) {
+          T h(0.0);
+          for (int i = 0; i < npe; ++i) h += u[D * i + a] * g[i][b];
+          F[a][b] = a == b ? h + 1.0 : h;
+        }
+      T C[3][3];
+      if constexpr (D == 2) {
+        C[0][0] = F[1][1]; C[0][1] = -F[1][0]; C[1][0] = -F[0][1]; C[1][1] = F[0][0];
+      } else {
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) {
+            const int a1 = (a + 1) % 3, a2 = (a + 2) % 3, b1 = (b + 1) % 3, b2 = (b + 2) % 3;
+            C[a][b] = F[a1][b1] * F[a2][b2] - F[a1][b2] * F[a2][b1];
+          }
+      }
+      T J(0.0), I1(D == 2 ? 1.0 : 0.0);
+      for (int b = 0; b < D; ++b) J += F[0][b] * C[0][b];
+      for (int a = 0; a < D; ++a)
+        for (int b = 0; b < D; ++b) I1 += F[a][b] * F[a][b];
+      if (!(value_of(J) > 0.0)) throw InvertedElementError("stress_neohooke: deformation gradient determinant <= 0");
+      const double mu = mat.mu(), kappa = mat.kappa();
+      const T a23 = pow(J, -2.0 / 3.0);
+      const T c1 = mu * a23;
+      const T c2 = (mu / 3.0) * I1 * a23 / J;
+      const T c3 = kappa * (J - 1.0);
+      for (int i = 0; i < npe; ++i)
+        for (int a = 0; a < D; ++a) {
+          T t(0.0);
+          for (int b = 0; b < D; ++b) t += (c1 * F[a][b] + (c3 - c2) * C[a][b]) * g[i][b];
+          out[D * i + a] += wdet * t;
+        }
     } else {  // St Venant-Kirchhoff (element.hpp:107-123, material.hpp:49-69)
       T F[3][3];
       for (int a = 0; a < D; ++a)
@@ -405,6 +537,7 @@ struct Batch {
   std::vector<double> coords;    // size * npe * dim
   Material material;
   int quadrature = 2;
+  const double* hist = nullptr;  // System::history (element-id indexed), J2 systems only
   std::size_t size() const { return element_ids.size(); }
 };
 
@@ -421,7 +554,16 @@ struct System {
   Pattern pattern;
   ConstraintTable table;
   std::vector<Constraint> constraints;
+  // committed Gauss-point history (J2): n_elem * nq * kHist, element-id indexed; empty otherwise.
+  std::vector<double> history;
   int dim() const { return mesh.dim; }
+  int nq() const { return mesh.dim == 2 ? 4 : 8; }
+  void init_history() {
+    bool j2 = false;
+    for (const auto& m : materials) j2 |= m.model == J2;
+    history.assign(j2 ? (std::size_t)mesh.n_elem() * nq() * kHist : 0, 0.0);
+    for (auto& b : batches) b.hist = history.empty() ? nullptr : history.data();
+  }
   int64_t n_dof() const { return mesh.n_dof(); }
 };
 
@@ -479,7 +621,27 @@ inline Pattern precompute_sparsity(const std::vector<Batch>& batches, int64_t n_
 
 template <int D, class T>
 inline void batch_kernel(const Batch& b, std::size_t e, const T* u, T* out) {
-  element_internal_force<D, T>(&b.coords[e * ET<D>::npe * D], b.material, b.quadrature, u, out);
+  const double* h = b.hist ? b.hist + (std::size_t)b.element_ids[e] * (D == 2 ? 4 : 8) * kHist : nullptr;
+  element_internal_force<D, T>(&b.coords[e * ET<D>::npe * D], b.material, b.quadrature, u, out, h);
+}
+
+// History commit (J2): every Gauss point's committed history advances to the return-mapped state at u.
+template <int D>
+void commit_history(System& s, const double* u) {
+  if (s.history.empty()) return;
+  constexpr int nd = ET<D>::ndpe, nq = D == 2 ? 4 : 8;
+  double ue[nd], re[nd];
+  for (const auto& b : s.batches) {
+    if (b.material.model != J2) continue;
+    for (std::size_t e = 0; e < b.size(); ++e) {
+      const int* dofs = &b.dof_map[e * nd];
+      for (int k = 0; k < nd; ++k) ue[k] = u[dofs[k]];
+      double* h = s.history.data() + (std::size_t)b.element_ids[e] * nq * kHist;
+      double hn[nq * kHist];
+      element_internal_force<D, double>(&b.coords[e * ET<D>::npe * D], b.material, b.quadrature, ue, re, h, hn);
+      std::copy(hn, hn + nq * kHist, h);
+    }
+  }
 }
 
 // assemble_residual (assembly.hpp:126-139)

@@ -18,7 +18,7 @@ __all__ = [
     "AfemError", "InvalidArgument", "OutOfRange", "LogicError", "DomainError", "LeaseError",
     "StaleEpochError", "CapabilityError", "FactorizationError", "InvertedElementError", "CudaError",
     "Context", "System", "Values", "HandoffBuffer", "LinearOperator", "explicit_operator",
-    "matrix_free_operator", "run_solver", "fibres", "LINEAR", "SVK", "EXPLICIT", "MATRIX_FREE",
+    "matrix_free_operator", "run_solver", "fibres", "LINEAR", "SVK", "NEOHOOKE", "J2", "EXPLICIT", "MATRIX_FREE",
     "CG", "GMRES", "NONE", "JACOBI", "lib_path", "load",
 ]
 
@@ -26,6 +26,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libafem_b200.so")
 
 LINEAR, SVK = 0, 1                 # MaterialModel (material.hpp:13)
+NEOHOOKE, J2 = 2, 3                # north-star laws beyond the reference (configs 3 and 4)
 EXPLICIT, MATRIX_FREE = 0, 1       # OperatorKind (backend.hpp:20)
 CG, GMRES = 0, 1                   # SolverMethod (krylov.hpp:20)
 NONE, JACOBI = 0, 1                # PreconKind (krylov.hpp:21)
@@ -157,6 +158,11 @@ def load():
         "afem_solve": ([vp, vp, vp, vp, vp, vp, vp, i32], i32),
         "afem_solve_bvp": ([vp, vp, vp, vp, vp, vp, i32], i32),
         "afem_load_stepping": ([vp, f64, i32, vp, vp, vp, vp, vp], i32),
+        "afem_history_size": ([vp, vp], i32),
+        "afem_history_commit": ([vp, vp], i32),
+        "afem_history_reset": ([vp], i32),
+        "afem_history_copy": ([vp, vp], i32),
+        "afem_history_set": ([vp, vp], i32),
         "afem_slab_range": ([i32, i32, i32, vp, vp], i32),
         "afem_nccl_unique_id": ([vp], i32),
         "afem_dist_create_nccl": ([vp, vp, i32, i32, vp], i32),
@@ -208,9 +214,12 @@ def _i32(a):
 
 
 def _mats(mats):
+    """Materials as (model, E, nu) or (model, E, nu, sigma_y, hardening) tuples."""
     arr = (afem_material * len(mats))()
     for i, m in enumerate(mats):
-        arr[i] = afem_material(int(m[0]), float(m[1]), float(m[2]), 0.0, 0.0)
+        sy = float(m[3]) if len(m) > 3 else 0.0
+        hh = float(m[4]) if len(m) > 4 else 0.0
+        arr[i] = afem_material(int(m[0]), float(m[1]), float(m[2]), sy, hh)
     return arr
 
 
@@ -405,6 +414,28 @@ class System:
         _check(_lib.afem_load_stepping(self.h, total_strain, n_steps, C.byref(cfg), _ptr(u), C.byref(failed),
                                        C.byref(conv), _ptr(its)))
         return u, dict(converged=bool(conv.value), failed_step=failed.value, step_iterations=its)
+
+    # ---- J2 quadrature-point history (device resident; include/afem.h)
+    def history_size(self) -> int:
+        n = C.c_int64()
+        _check(_lib.afem_history_size(self.h, C.byref(n)))
+        return n.value
+
+    def history(self):
+        out = np.zeros(self.history_size())
+        _check(_lib.afem_history_copy(self.h, _ptr(out)))
+        return out
+
+    def set_history(self, h):
+        h = _f64(h)
+        _check(_lib.afem_history_set(self.h, _ptr(h)))
+
+    def commit_history(self, u):
+        u = _f64(u)
+        _check(_lib.afem_history_commit(self.h, _ptr(u)))
+
+    def reset_history(self):
+        _check(_lib.afem_history_reset(self.h))
 
 
 class Values:

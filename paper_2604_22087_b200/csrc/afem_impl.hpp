@@ -42,6 +42,7 @@ struct SysView {
   const uint8_t* mask;
   const double* presc;
   int* err;
+  const double* hist;  // committed quadrature-point history (J2), n_elem*nq*kHist, or null
 };
 
 struct StencilPlan;  // structured fast path (stencil.cu)
@@ -65,6 +66,11 @@ struct System {
   DevArray<double> presc;
   std::vector<Constraint> constraints;
   DevArray<int> err;
+  // committed quadrature-point history (allocated, zeroed, when any phase is J2): element-major,
+  // nq slots of kHist doubles (DESIGN.md §Data layout). Stays resident across Newton iterations
+  // and load steps; history_commit advances it from a converged state.
+  DevArray<double> hist;
+  bool has_history() const { return hist.p != nullptr; }
   // structured grid metadata (afem_system_create_grid)
   bool grid = false;
   int nx = 0, ny = 0, nz = 0;
@@ -72,11 +78,11 @@ struct System {
 
   SysView view() const {
     return SysView{dim, npe, n_nodes, n_elem, n_dof, coords.p, conn.p, phase.p, d_mats.p, inc_ptr.p, inc.p,
-                   adj_ptr.p, adj.p, mask.p, presc.p, err.p};
+                   adj_ptr.p, adj.p, mask.p, presc.p, err.p, hist.p};
   }
   int64_t device_bytes() const {
     return coords.bytes() + conn.bytes() + phase.bytes() + elem_order.bytes() + inc_ptr.bytes() + inc.bytes() +
-           adj_ptr.bytes() + adj.bytes() + mask.bytes() + presc.bytes();
+           adj_ptr.bytes() + adj.bytes() + mask.bytes() + presc.bytes() + hist.bytes();
   }
 };
 
@@ -135,7 +141,10 @@ std::vector<Constraint> benchmark_bcs(const System& s, double strain);
 void pattern_export(System& s, int64_t* d_row_ptr, int32_t* d_rows, int32_t* d_cols);
 void batch_export(System& s, int b, int64_t* size, int32_t* h_ids, int32_t* h_dof_map);
 void check_err(System& s);
-DMat make_dmat(int model, double E, double nu);
+DMat make_dmat(int model, double E, double nu, double sigma_y = 0.0, double hardening = 0.0);
+// J2 history: commit the return-mapped state at u; reset to virgin.
+void history_commit(System& s, const double* u);
+void history_reset(System& s);
 
 // ---- assembly.cu
 void residual(System& s, const double* u, double* r);

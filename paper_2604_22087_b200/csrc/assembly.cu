@@ -44,6 +44,10 @@ __device__ __forceinline__ void load_dofs_masked(const SysView& s, int64_t e, co
   }
 }
 
+__device__ __forceinline__ const double* qp_hist(const SysView& s, int64_t e, int q, int nq) {
+  return s.hist ? s.hist + (e * nq + q) * kHist : nullptr;
+}
+
 // R(u) rows of node n (assembly.hpp:126-139 with element_internal_force, element.hpp:68-125).
 template <int D>
 __global__ void __launch_bounds__(128) k_residual(SysView s, const double* u, double* r) {
@@ -69,7 +73,7 @@ __global__ void __launch_bounds__(128) k_residual(SysView s, const double* u, do
         if (!qp_geometry<D>(xc, q, g, wdet)) err |= ERR_DETJ;
         double H[D][D], P[D][D];
         grad_u<D>(ue, g, H);
-        piola<D>(m, H, P, err);
+        piola<D>(m, H, P, err, qp_hist(s, e, q, nq));
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           double t = 0.0;
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(128) k_mf_apply(SysView s, const double* state
         double H[D][D], dH[D][D], dP[D][D];
         grad_u<D>(xe, g, dH);
         if (m.model != MODEL_LINEAR) grad_u<D>(ue, g, H);
-        piola_jvp<D>(m, H, dH, dP);
+        piola_jvp<D>(m, H, dH, dP, qp_hist(s, e, q, nq));
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           double t = 0.0;
@@ -132,6 +136,28 @@ __global__ void __launch_bounds__(128) k_mf_apply(SysView s, const double* state
     for (int a = 0; a < D; ++a) {
       const int64_t d = D * n + a;
       y[d] = mask[d] ? x[d] : acc[a];
+    }
+  }
+}
+
+// history_commit: advance every J2 quadrature point's committed history to the return-mapped
+// state at u (one thread per element, in place: each slot is read and written by its owner only).
+template <int D>
+__global__ void __launch_bounds__(128) k_history_commit(SysView s, const double* u, double* hist) {
+  constexpr int npe = EL<D>::npe, nq = EL<D>::nq, nd = EL<D>::nd;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s.n_elem; e += (int64_t)gridDim.x * blockDim.x) {
+    const DMat m = s.mats[s.phase[e]];
+    if (m.model != MODEL_J2) continue;
+    double xc[npe][D], ue[nd];
+    load_coords<D>(s, e, xc);
+    load_dofs<D>(s, e, u, ue);
+    for (int q = 0; q < nq; ++q) {
+      double g[npe][D], wdet;
+      qp_geometry<D>(xc, q, g, wdet);
+      double H[D][D];
+      grad_u<D>(ue, g, H);
+      double* hq = hist + (e * nq + q) * kHist;
+      j2_commit<D>(m, H, hq, hq);
     }
   }
 }
@@ -177,7 +203,7 @@ __global__ void __launch_bounds__(128) k_jacobian(SysView s, const double* u, do
         double H[D][D];
         grad_u<D>(ue, g, H);
         TangentQP<D> t;
-        tangent_qp<D>(m, H, t, err);
+        tangent_qp<D>(m, H, t, err, qp_hist(s, e, q, nq));
         double gn[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) gn[c] = g[ln][c];
@@ -232,7 +258,7 @@ __global__ void __launch_bounds__(128) k_diagonal(SysView s, const double* u, do
         double H[D][D];
         grad_u<D>(ue, g, H);
         TangentQP<D> t;
-        tangent_qp<D>(m, H, t, err);
+        tangent_qp<D>(m, H, t, err, qp_hist(s, e, q, nq));
         double gn[D], blk[D][D];
 #pragma unroll
         for (int c = 0; c < D; ++c) gn[c] = g[ln][c];
@@ -358,6 +384,17 @@ void diagonal(System& s, const double* u, double* d) {
 void mf_apply_general(System& s, const double* state, const uint8_t* mask, const double* x, double* y) {
   if (s.dim == 2) launch(*s.ctx, k_mf_apply<2>, node_grid(s, 128), 128, 0, s.view(), state, mask, x, y);
   else launch(*s.ctx, k_mf_apply<3>, node_grid(s, 128), 128, 0, s.view(), state, mask, x, y);
+}
+
+void history_commit(System& s, const double* u) {
+  if (!s.has_history()) return;
+  const unsigned g = grid_for(s.n_elem, 128, 148 * 64);
+  if (s.dim == 2) launch(*s.ctx, k_history_commit<2>, g, 128, 0, s.view(), u, s.hist.p);
+  else launch(*s.ctx, k_history_commit<3>, g, 128, 0, s.view(), u, s.hist.p);
+}
+
+void history_reset(System& s) {
+  if (s.has_history()) AFEM_CK(cudaMemsetAsync(s.hist.p, 0, s.hist.bytes(), s.ctx->stream));
 }
 
 void eliminate(System& s, double* values, double* residual_, const double* u) {

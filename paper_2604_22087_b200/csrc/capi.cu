@@ -219,7 +219,7 @@ System& SYS(afem_system s) {
 std::vector<DMat> to_dmats(int32_t n, const afem_material* m) {
   if (n < 0 || (n > 0 && !m)) throw std::invalid_argument("materials: bad table");
   std::vector<DMat> out;
-  for (int i = 0; i < n; ++i) out.push_back(make_dmat(m[i].model, m[i].E, m[i].nu));
+  for (int i = 0; i < n; ++i) out.push_back(make_dmat(m[i].model, m[i].E, m[i].nu, m[i].sigma_y, m[i].hardening));
   return out;
 }
 
@@ -949,9 +949,58 @@ afem_status afem_load_stepping(afem_system sys, double total_strain, int32_t n_s
         du.finish();
         return;
       }
+      history_commit(s, du.d);  // J2: the converged step becomes the committed history
     }
     if (converged) *converged = 1;
     du.finish();
+  });
+}
+
+afem_status afem_history_size(afem_system sys, int64_t* n) {
+  return guarded([&] {
+    System& s = SYS(sys);
+    need(n, "n");
+    *n = static_cast<int64_t>(s.hist.n);
+  });
+}
+
+afem_status afem_history_commit(afem_system sys, const double* u) {
+  return guarded([&] {
+    System& s = SYS(sys);
+    need(u, "u");
+    In<double> du(*s.ctx, u, s.n_dof);
+    history_commit(s, du.d);
+    AFEM_CK(cudaStreamSynchronize(s.ctx->stream));
+  });
+}
+
+afem_status afem_history_reset(afem_system sys) {
+  return guarded([&] {
+    System& s = SYS(sys);
+    history_reset(s);
+    AFEM_CK(cudaStreamSynchronize(s.ctx->stream));
+  });
+}
+
+afem_status afem_history_copy(afem_system sys, double* out) {
+  return guarded([&] {
+    System& s = SYS(sys);
+    need(out, "out");
+    if (!s.has_history()) throw std::invalid_argument("history: system has no J2 phase");
+    Out<double> o(*s.ctx, out, s.hist.n, false);
+    AFEM_CK(cudaMemcpyAsync(o.d, s.hist.p, s.hist.bytes(), cudaMemcpyDeviceToDevice, s.ctx->stream));
+    o.finish();
+  });
+}
+
+afem_status afem_history_set(afem_system sys, const double* in) {
+  return guarded([&] {
+    System& s = SYS(sys);
+    need(in, "in");
+    if (!s.has_history()) throw std::invalid_argument("history: system has no J2 phase");
+    In<double> d(*s.ctx, in, s.hist.n);
+    AFEM_CK(cudaMemcpyAsync(s.hist.p, d.d, s.hist.bytes(), cudaMemcpyDeviceToDevice, s.ctx->stream));
+    AFEM_CK(cudaStreamSynchronize(s.ctx->stream));
   });
 }
 

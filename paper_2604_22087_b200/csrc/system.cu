@@ -16,7 +16,7 @@
 
 namespace afem {
 
-DMat make_dmat(int model, double E, double nu) {
+DMat make_dmat(int model, double E, double nu, double sigma_y, double hardening) {
   DMat m{};
   m.model = model;
   m.E = E;
@@ -27,6 +27,9 @@ DMat make_dmat(int model, double E, double nu) {
   m.c11 = c * (1.0 - nu);
   m.c12 = c * nu;
   m.c33 = c * (1.0 - 2.0 * nu) / 2.0;
+  m.kappa = m.lam + 2.0 * m.mu / 3.0;
+  m.sy = sigma_y;
+  m.hh = hardening;
   return m;
 }
 
@@ -335,7 +338,9 @@ std::unique_ptr<System> make_system(Ctx& c, int dim, int64_t n_nodes, int64_t n_
   for (const DMat& m : mats) {  // Material::validate (material.hpp:23-26)
     if (!(m.E > 0.0)) throw std::invalid_argument("material: E must be > 0");
     if (!(m.nu > -1.0 && m.nu < 0.5)) throw std::invalid_argument("material: nu must be in (-1, 0.5)");
-    if (m.model != MODEL_LINEAR && m.model != MODEL_SVK) throw std::invalid_argument("material: unsupported model");
+    if (m.model < MODEL_LINEAR || m.model > MODEL_J2) throw std::invalid_argument("material: unsupported model");
+    if (m.model == MODEL_J2 && !(m.sy > 0.0 && m.hh >= 0.0))
+      throw std::invalid_argument("material: J2 needs sigma_y > 0 and hardening >= 0");
   }
   auto s = std::make_unique<System>();
   s->ctx = &c;
@@ -352,6 +357,12 @@ std::unique_ptr<System> make_system(Ctx& c, int dim, int64_t n_nodes, int64_t n_
   AFEM_CK(cudaMemcpyAsync(s->coords.p, d_coords, s->coords.bytes(), cudaMemcpyDeviceToDevice, c.stream));
   AFEM_CK(cudaMemcpyAsync(s->conn.p, d_conn, s->conn.bytes(), cudaMemcpyDeviceToDevice, c.stream));
   build_topology(*s, d_phase);
+  bool j2 = false;
+  for (const DMat& m : mats) j2 |= m.model == MODEL_J2;
+  if (j2) {
+    s->hist.alloc((size_t)n_elem * (dim == 2 ? 4 : 8) * kHist);
+    history_reset(*s);
+  }
   return s;
 }
 
