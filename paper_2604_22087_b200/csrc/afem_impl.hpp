@@ -71,6 +71,10 @@ struct System {
   // and load steps; history_commit advances it from a converged state.
   DevArray<double> hist;
   bool has_history() const { return hist.p != nullptr; }
+  // structured grids: uniform-brick Gauss-point geometry (g_i(q), w detJ(q)) and the element-vector
+  // scratch of the element-centric kernels (elemgrid.cu), allocated on first use
+  std::vector<double> grid_geo;
+  DevArray<double> ev;
   // structured grid metadata (afem_system_create_grid)
   bool grid = false;
   int nx = 0, ny = 0, nz = 0;
@@ -82,7 +86,7 @@ struct System {
   }
   int64_t device_bytes() const {
     return coords.bytes() + conn.bytes() + phase.bytes() + elem_order.bytes() + inc_ptr.bytes() + inc.bytes() +
-           adj_ptr.bytes() + adj.bytes() + mask.bytes() + presc.bytes() + hist.bytes();
+           adj_ptr.bytes() + adj.bytes() + mask.bytes() + presc.bytes() + hist.bytes() + ev.bytes();
   }
 };
 
@@ -156,6 +160,13 @@ void constrain_residual(System& s, double* residual, const double* u);
 void csr_apply(System& s, const double* values, const double* x, double* y);
 void csr_diagonal(System& s, const double* values, double* d);
 void impose_dirichlet(System& s, double* u);
+
+// ---- elemgrid.cu (structured grids: element-centric evaluation + ordered node gather)
+void grid_geometry(System& s);
+bool grid_elem_path(const System& s);
+void grid_residual(System& s, const double* u, double* r);
+void grid_diagonal(System& s, const double* u, double* d);
+void grid_mf_apply(System& s, const double* state, const uint8_t* mask, const double* x, double* y);
 
 // ---- blas.cu (deterministic reductions; results in device scalars or host)
 double dot(Ctx& c, const double* x, const double* y, int64_t n);

@@ -362,6 +362,11 @@ inline unsigned node_grid(const System& s, int threads) { return grid_for(s.n_no
 }  // namespace
 
 void residual(System& s, const double* u, double* r) {
+  if (grid_elem_path(s)) {
+    grid_residual(s, u, r);
+    check_err(s);
+    return;
+  }
   if (s.dim == 2) launch(*s.ctx, k_residual<2>, node_grid(s, 128), 128, 0, s.view(), u, r);
   else launch(*s.ctx, k_residual<3>, node_grid(s, 128), 128, 0, s.view(), u, r);
   check_err(s);
@@ -374,6 +379,11 @@ void jacobian(System& s, const double* u, double* values) {
 }
 
 void diagonal(System& s, const double* u, double* d) {
+  if (grid_elem_path(s)) {
+    grid_diagonal(s, u, d);
+    check_err(s);
+    return;
+  }
   if (s.dim == 2) launch(*s.ctx, k_diagonal<2>, node_grid(s, 128), 128, 0, s.view(), u, d);
   else launch(*s.ctx, k_diagonal<3>, node_grid(s, 128), 128, 0, s.view(), u, d);
   check_err(s);
@@ -382,6 +392,10 @@ void diagonal(System& s, const double* u, double* d) {
 // Asynchronous (no error check): used inside Krylov loops; the state was validated at operator
 // creation by the diagonal assembly.
 void mf_apply_general(System& s, const double* state, const uint8_t* mask, const double* x, double* y) {
+  if (grid_elem_path(s)) {
+    grid_mf_apply(s, state, mask, x, y);
+    return;
+  }
   if (s.dim == 2) launch(*s.ctx, k_mf_apply<2>, node_grid(s, 128), 128, 0, s.view(), state, mask, x, y);
   else launch(*s.ctx, k_mf_apply<3>, node_grid(s, 128), 128, 0, s.view(), state, mask, x, y);
 }

@@ -1,0 +1,216 @@
+// Element-centric kernels for structured grid systems (afem_system_create_grid): residual,
+// matrix-free JVP and Jacobi diagonal of ANY constitutive law (linear, SVK, Neo-Hookean, J2).
+//
+// The general node-centric kernels (assembly.cu) re-evaluate an element's quadrature loop once per
+// incident node (8x in 3D). On a uniform grid every element is the same brick, so the shape-function
+// gradients g_i(q) and w detJ(q) are computed once per system (GridGeo, passed as a __grid_constant__
+// parameter: uniform broadcast reads, no per-element geometry) and the element kernel evaluates the
+// constitutive update once per Gauss point, writing the element's nd-vector to a scratch array:
+//     k_grid_elem<MODE>  thread per element: gather u_e (and x_e), qp loop, ev[e] = f_e
+//     k_gather           thread per node: y_n = sum over the node's incident (element, corner) pairs
+//                        in the reference's (batch, element) order (assembly.hpp:130-137)
+// The reduction order is the node-centric kernels' (and the reference's), so results stay
+// deterministic run to run with no atomics. Algorithmic traffic per element: u_e/x_e gathers
+// (L2-resident neighbours), J2 history (nq*64 B), 2*nd*8 B of scratch.
+#include <cstdlib>
+#include <cstring>
+
+#include "afem_impl.hpp"
+
+namespace afem {
+
+namespace {
+
+template <int D>
+struct GeoT {
+  double g[EL<D>::nq][EL<D>::npe][D];
+  double wdet[EL<D>::nq];
+};
+
+// Uniform-brick geometry from element 0 (the same device math as the general kernels).
+template <int D>
+__global__ void k_grid_geometry(const double* coords, const int32_t* conn, double* out, int* err) {
+  constexpr int npe = EL<D>::npe, nq = EL<D>::nq;
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double xc[npe][D];
+  for (int k = 0; k < npe; ++k)
+    for (int c = 0; c < D; ++c) xc[k][c] = coords[(int64_t)conn[k] * D + c];
+  for (int q = 0; q < nq; ++q) {
+    double g[npe][D], wdet;
+    if (!qp_geometry<D>(xc, q, g, wdet)) atomicOr(err, ERR_DETJ);
+    for (int i = 0; i < npe; ++i)
+      for (int b = 0; b < D; ++b) out[(q * npe + i) * D + b] = g[i][b];
+    out[nq * npe * D + q] = wdet;
+  }
+}
+
+enum : int { EV_RESIDUAL = 0, EV_JVP = 1, EV_DIAG = 2 };
+
+template <int D>
+__device__ __forceinline__ void elem_nodes(int64_t e, int nx, int ny, int64_t (&nd)[EL<D>::npe]) {
+  const int ex = static_cast<int>(e % nx);
+  const int64_t r = e / nx;
+  const int ey = static_cast<int>(r % ny);
+  const int64_t ez = r / ny;
+  const int64_t NX = nx + 1, NXY = NX * (ny + 1);
+  const int64_t n0 = ex + NX * ey + NXY * ez;
+  nd[0] = n0; nd[1] = n0 + 1; nd[2] = n0 + 1 + NX; nd[3] = n0 + NX;
+  if constexpr (D == 3) {
+    nd[4] = n0 + NXY; nd[5] = n0 + 1 + NXY; nd[6] = n0 + 1 + NX + NXY; nd[7] = n0 + NX + NXY;
+  }
+}
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(128) k_grid_elem(const __grid_constant__ GeoT<D> G, SysView s, int nx, int ny,
+                                                   const double* __restrict__ u, const uint8_t* __restrict__ mask,
+                                                   const double* __restrict__ x, double* __restrict__ ev) {
+  constexpr int npe = EL<D>::npe, nq = EL<D>::nq, nd = EL<D>::nd;
+  int err = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s.n_elem; e += (int64_t)gridDim.x * blockDim.x) {
+    const DMat m = s.mats[s.phase[e]];
+    const bool lin = m.model == MODEL_LINEAR;
+    int64_t nodes[npe];
+    elem_nodes<D>(e, nx, ny, nodes);
+    double ue[nd], xe[nd];
+#pragma unroll
+    for (int k = 0; k < npe; ++k)
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const int64_t d = nodes[k] * D + c;
+        ue[k * D + c] = (MODE == EV_JVP && lin) ? 0.0 : __ldg(&u[d]);
+        if constexpr (MODE == EV_JVP) xe[k * D + c] = mask[d] ? 0.0 : __ldg(&x[d]);
+      }
+    double f[nd];
+#pragma unroll
+    for (int k = 0; k < nd; ++k) f[k] = 0.0;
+    const double* hbase = s.hist ? s.hist + e * nq * kHist : nullptr;
+#pragma unroll 1
+    for (int q = 0; q < nq; ++q) {
+      const double wdet = G.wdet[q];
+      const double* hq = hbase ? hbase + q * kHist : nullptr;
+      double H[D][D];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          double t = 0.0;
+#pragma unroll
+          for (int i = 0; i < npe; ++i) t += ue[D * i + a] * G.g[q][i][b];
+          H[a][b] = t;
+        }
+      if constexpr (MODE == EV_DIAG) {
+        TangentQP<D> t;
+        tangent_qp<D>(m, H, t, err, hq);
+#pragma unroll
+        for (int i = 0; i < npe; ++i) {
+          double gi[D], blk[D][D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) gi[c] = G.g[q][i][c];
+          tangent_block<D>(t, gi, gi, blk);
+#pragma unroll
+          for (int a = 0; a < D; ++a) f[D * i + a] += wdet * blk[a][a];
+        }
+      } else {
+        double P[D][D];
+        if constexpr (MODE == EV_RESIDUAL) {
+          piola<D>(m, H, P, err, hq);
+        } else {
+          double dH[D][D];
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+              double t = 0.0;
+#pragma unroll
+              for (int i = 0; i < npe; ++i) t += xe[D * i + a] * G.g[q][i][b];
+              dH[a][b] = t;
+            }
+          piola_jvp<D>(m, H, dH, P, hq);
+        }
+#pragma unroll
+        for (int i = 0; i < npe; ++i)
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            double t = 0.0;
+#pragma unroll
+            for (int b = 0; b < D; ++b) t += P[a][b] * G.g[q][i][b];
+            f[D * i + a] += wdet * t;
+          }
+      }
+    }
+    double2* o = reinterpret_cast<double2*>(ev + e * nd);
+#pragma unroll
+    for (int k = 0; k < nd / 2; ++k) o[k] = make_double2(f[2 * k], f[2 * k + 1]);
+  }
+  if (err) atomicOr(s.err, err);
+}
+
+// y_n = sum of the node's element contributions in (batch, element) order; JVP: unit rows on
+// constrained dofs (backend.hpp:146-147).
+template <int D>
+__global__ void __launch_bounds__(256) k_gather(SysView s, const double* __restrict__ ev, const uint8_t* __restrict__ mask,
+                                                const double* __restrict__ x, double* __restrict__ y) {
+  constexpr int npe = EL<D>::npe, nd = EL<D>::nd;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < s.n_nodes; n += (int64_t)gridDim.x * blockDim.x) {
+    double acc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) acc[a] = 0.0;
+    for (int64_t p = s.inc_ptr[n]; p < s.inc_ptr[n + 1]; ++p) {
+      const uint32_t v = __ldg(&s.inc[p]);
+      const double* src = ev + (int64_t)(v / npe) * nd + (v % npe) * D;
+#pragma unroll
+      for (int a = 0; a < D; ++a) acc[a] += __ldg(&src[a]);
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const int64_t d = D * n + a;
+      y[d] = (mask && mask[d]) ? x[d] : acc[a];
+    }
+  }
+}
+
+template <int D, int MODE>
+void run(System& s, const double* u, const uint8_t* mask, const double* x, double* y) {
+  GeoT<D> G;
+  static_assert(sizeof(GeoT<D>) == sizeof(double) * (EL<D>::nq * EL<D>::npe * D + EL<D>::nq), "layout");
+  std::memcpy(&G, s.grid_geo.data(), sizeof G);
+  if (!s.ev.p) s.ev.alloc((size_t)s.n_elem * EL<D>::nd);
+  launch(*s.ctx, k_grid_elem<D, MODE>, grid_for(s.n_elem, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, u, mask, x,
+         s.ev.p);
+  launch(*s.ctx, k_gather<D>, grid_for(s.n_nodes, 256, 148 * 32), 256, 0, s.view(), s.ev.p,
+         MODE == EV_JVP ? mask : nullptr, x, y);
+}
+
+}  // namespace
+
+void grid_geometry(System& s) {
+  const size_t n = s.dim == 2 ? (4 * 4 * 2 + 4) : (8 * 8 * 3 + 8);
+  DevArray<double> d(n);
+  if (s.dim == 2) launch(*s.ctx, k_grid_geometry<2>, 1, 32, 0, s.coords.p, s.conn.p, d.p, s.err.p);
+  else launch(*s.ctx, k_grid_geometry<3>, 1, 32, 0, s.coords.p, s.conn.p, d.p, s.err.p);
+  s.grid_geo.resize(n);
+  AFEM_CK(cudaMemcpyAsync(s.grid_geo.data(), d.p, n * 8, cudaMemcpyDeviceToHost, s.ctx->stream));
+  AFEM_CK(cudaStreamSynchronize(s.ctx->stream));
+}
+
+bool grid_elem_path(const System& s) {
+  static const bool off = std::getenv("AFEM_NO_GRID_ELEM") != nullptr;
+  return s.grid && !s.grid_geo.empty() && !off;
+}
+
+void grid_residual(System& s, const double* u, double* r) {
+  if (s.dim == 2) run<2, EV_RESIDUAL>(s, u, nullptr, nullptr, r);
+  else run<3, EV_RESIDUAL>(s, u, nullptr, nullptr, r);
+}
+
+void grid_diagonal(System& s, const double* u, double* d) {
+  if (s.dim == 2) run<2, EV_DIAG>(s, u, nullptr, nullptr, d);
+  else run<3, EV_DIAG>(s, u, nullptr, nullptr, d);
+}
+
+void grid_mf_apply(System& s, const double* state, const uint8_t* mask, const double* x, double* y) {
+  if (s.dim == 2) run<2, EV_JVP>(s, state, mask, x, y);
+  else run<3, EV_JVP>(s, state, mask, x, y);
+}
+
+}  // namespace afem

@@ -389,6 +389,7 @@ std::unique_ptr<System> make_grid_system(Ctx& c, int dim, int nx, int ny, int nz
   s->grid = true;
   s->nx = nx; s->ny = ny; s->nz = dim == 3 ? nz : 0;
   s->lx = lx; s->ly = ly; s->lz = dim == 3 ? lz : 0.0;
+  grid_geometry(*s);
   return s;
 }
 

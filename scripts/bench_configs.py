@@ -1,0 +1,152 @@
+#!/usr/bin/env python
+"""Measurements for BASELINE.json configs 3 and 4 on one B200 (bench.py covers config 2).
+
+  C3  3D Neo-Hookean hex8 RVE N^3 (default 192): matrix Neo-Hookean E=1 nu=0.3, fibres linear
+      E=10; Newton-Krylov with the assembled CSR tangent + GMRES(30)+Jacobi.
+  C4  3D J2 hex8 RVE N^3 (default 256): matrix J2 (E=1, nu=0.3, sigma_y=0.002, H=0.1), fibres
+      linear E=10; quadrature-point history resident in HBM; strain ramped to 0.02 in 10 steps.
+
+Per config at full size it times every hot-path kernel through the C ABI with device buffers
+(torch allocations, CUDA events on the context stream, min over reps): residual, tangent
+assembly (CSR values), Dirichlet elimination, CSR SpMV, matrix-free JVP, Jacobi diagonal,
+history commit. Then it runs the complete nonlinear solve at a reduced size (--solve-n) on the
+GPU and the same solve on the CPU restatement (oracle/, 1 thread) for the speed-up line.
+Prints one JSON object per config.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2604_22087_b200 as afem  # noqa: E402
+
+SEED, N_FIBRES, RADIUS = 12345, 40, 0.05
+CONFIGS = {
+    3: dict(mats=[(afem.NEOHOOKE, 1.0, 0.3), (afem.LINEAR, 10.0, 0.3)], strain=0.05, steps=1, n=192,
+            workload="C3 hex8 Neo-Hookean RVE, Newton + assembled CSR tangent + GMRES(30)/Jacobi"),
+    4: dict(mats=[(afem.J2, 1.0, 0.3, 0.002, 0.1), (afem.LINEAR, 10.0, 0.3)], strain=0.02, steps=10, n=256,
+            workload="C4 hex8 J2 RVE, quadrature-point history in HBM, 10 load steps"),
+}
+
+
+def timed(fn, reps, stream):
+    best = float("inf")
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        best = min(best, a.elapsed_time(b) * 1e-3)
+    return best
+
+
+def kernels(cfg, n, reps):
+    L = afem.load()
+    ctx = afem.Context(0)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    fib = afem.fibres(SEED, N_FIBRES)
+    s = afem.System.grid(ctx, 3, n, n, n, inclusions=fib, radius=RADIUS, materials=cfg["mats"])
+    s.set_benchmark_dirichlet(cfg["strain"] / cfg["steps"])
+    nd, nnz, ne = s.n, s.nnz, s.info.n_elem
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(1)
+    u = (torch.rand(nd, dtype=torch.float64, device=dev, generator=g) - 0.5) * (0.02 / n)
+    x = torch.rand(nd, dtype=torch.float64, device=dev, generator=g) - 0.5
+    r = torch.empty_like(u)
+    y = torch.empty_like(u)
+    d = torch.empty_like(u)
+    vals = torch.empty(nnz, dtype=torch.float64, device=dev)
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    ck = afem._check
+    out = dict(n=n, n_dof=nd, n_elem=ne, nnz=nnz, device_gb=round(s.info.device_bytes / 1e9, 2))
+    if s.history_size():
+        ck(L.afem_history_commit(s.h, P(u * 0.5)))
+        out["history_gb"] = round(s.history_size() * 8 / 1e9, 2)
+    out["residual_ms"] = timed(lambda: ck(L.afem_residual(s.h, P(u), P(r))), reps, stream) * 1e3
+    out["diagonal_ms"] = timed(lambda: ck(L.afem_diagonal(s.h, P(u), P(d))), reps, stream) * 1e3
+    out["jacobian_ms"] = timed(lambda: ck(L.afem_jacobian(s.h, P(u), P(vals))), reps, stream) * 1e3
+    rr = r.clone()
+    out["eliminate_ms"] = timed(lambda: ck(L.afem_eliminate(s.h, P(vals), P(rr), P(u))), 1, stream) * 1e3
+    out["csr_spmv_ms"] = timed(lambda: ck(L.afem_csr_apply(s.h, P(vals), P(x), P(y))), reps, stream) * 1e3
+    out["csr_spmv_gbs"] = (12 * nnz + 16 * nd) / (out["csr_spmv_ms"] * 1e-3) / 1e9
+    del vals
+    torch.cuda.empty_cache()
+    op = C.c_void_p()
+    ck(L.afem_op_create_mf(s.h, P(u), C.byref(op)))
+    out["mf_apply_ms"] = timed(lambda: ck(L.afem_op_apply_async(op, P(x), P(y))), reps, stream) * 1e3
+    out["mf_dof_per_s"] = nd / (out["mf_apply_ms"] * 1e-3)
+    ck(L.afem_op_destroy(op))
+    if s.history_size():
+        out["history_commit_ms"] = timed(lambda: ck(L.afem_history_commit(s.h, P(u))), reps, stream) * 1e3
+    return out
+
+
+def solve_small(cfg, n, cfgno, cpu):
+    from oracle.pyoracle import Oracle
+    ctx = afem.Context(0)
+    fib = afem.fibres(SEED, N_FIBRES)
+    s = afem.System.grid(ctx, 3, n, n, n, inclusions=fib, radius=RADIUS, materials=cfg["mats"])
+    kw = dict(rtol=1e-8, lin_rtol=1e-10, lin_max_iter=100000)
+    if cfgno == 3:
+        kw.update(method=afem.GMRES, operator_kind=afem.EXPLICIT)
+    t = time.perf_counter()
+    if cfg["steps"] == 1:
+        s.set_benchmark_dirichlet(cfg["strain"])
+        u, rep = s.solve_bvp(**kw)
+        its = [rep["iterations"]]
+        ok = rep["converged"]
+        lin = rep["total_linear_iterations"]
+    else:
+        u, rep = s.load_stepping(cfg["strain"], cfg["steps"], **kw)
+        its, ok, lin = list(map(int, rep["step_iterations"])), rep["converged"], None
+    res = dict(n=n, n_dof=s.n, gpu_s=time.perf_counter() - t, converged=bool(ok), newton_iterations=its,
+               linear_iterations=lin)
+    if cpu:
+        o = Oracle("restate")
+        coords, conn, phase = s.mesh()
+        os_ = o.system(3, coords, conn, phase, cfg["mats"], grid=(n, n, n, 1.0, 1.0, 1.0))
+        okw = dict(kw)
+        okw["method"] = 1 if cfgno == 3 else 0
+        t = time.perf_counter()
+        if cfg["steps"] == 1:
+            os_.set_dirichlet(*o.bcs(3, n, n, n, 1.0, cfg["strain"]))
+            uo, ro = os_.solve_bvp(**okw)
+            res["cpu_newton_iterations"] = [ro["iterations"]]
+        else:
+            uo, ro = os_.load_stepping(cfg["strain"], cfg["steps"], **okw)
+            res["cpu_newton_iterations"] = list(map(int, ro["step_iterations"]))
+        res["cpu_s"] = time.perf_counter() - t
+        res["cpu_cores"] = 1
+        res["cpu_kind"] = "port (oracle/restate.hpp, single thread)"
+        res["rel_diff_u"] = float(np.abs(u - uo).max() / np.abs(uo).max())
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="3,4")
+    ap.add_argument("--n", type=int, default=0, help="override the full size")
+    ap.add_argument("--solve-n", type=int, default=24)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    a = ap.parse_args()
+    for c in map(int, a.configs.split(",")):
+        cfg = CONFIGS[c]
+        rec = dict(config=c, workload=cfg["workload"], dtype="f64", data="synthetic")
+        rec["kernels"] = kernels(cfg, a.n or cfg["n"], a.reps)
+        torch.cuda.empty_cache()
+        rec["solve"] = solve_small(cfg, a.solve_n, c, not a.no_cpu)
+        print(json.dumps(rec), flush=True)
+
+
+if __name__ == "__main__":
+    main()

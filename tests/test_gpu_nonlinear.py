@@ -126,3 +126,31 @@ def test_inverted_element_raises(afem, ctx):
 def test_j2_material_validation(afem, ctx):
     with pytest.raises(afem.InvalidArgument):
         afem.System.grid(ctx, 3, 2, 2, 2, materials=[(3, 1.0, 0.3, 0.0, 0.1)])
+
+
+@pytest.mark.parametrize("mats", [NH_MIX, J2_MIX, [(1, 1.0, 0.3), (0, 10.0, 0.3)], [(0, 1.0, 0.3), (0, 10.0, 0.3)]],
+                         ids=["neohooke", "j2", "svk", "linear"])
+def test_general_mesh_kernels_all_laws(afem, ctx, orc, mats):
+    """Distorted (non-grid) hex8 mesh: the node-centric general kernels vs the restatement, and the
+    element-centric grid kernels vs the general kernels on the same undistorted mesh."""
+    n = 4
+    fib = afem.fibres(12345, 4)
+    g = afem.System.grid(ctx, 3, n, n, n, inclusions=fib, radius=0.2, materials=mats)
+    coords, conn, phase = g.mesh()
+    flat = afem.System(ctx, 3, coords, conn, phase, mats)  # same mesh through the general path
+    u = random_vector(g.n, 0.03, 21)
+    x = random_vector(g.n, 1.0, 22)
+    if g.history_size():
+        g.commit_history(u * 0.7)
+        flat.commit_history(u * 0.7)
+    assert rel_err(g.residual(u), flat.residual(u)) <= 1e-13
+    assert rel_err(g.diagonal(u), flat.diagonal(u)) <= 1e-13
+    assert rel_err(afem.matrix_free_operator(g, u).apply(x), afem.matrix_free_operator(flat, u).apply(x)) <= 1e-13
+    dist = coords + random_vector(len(coords), 0.02, 23)
+    s = afem.System(ctx, 3, dist, conn, phase, mats)
+    o = orc.system(3, dist, conn, phase, mats)
+    if s.history_size():
+        s.commit_history(u * 0.7)
+        o.commit_history(u * 0.7)
+        assert rel_err(s.history(), o.history()) <= TOL
+    assembly_parity(afem, s, o, u, x)
