@@ -2,7 +2,9 @@
 """Measurements for BASELINE.json configs 3 and 4 on one B200 (bench.py covers config 2).
 
   C3  3D Neo-Hookean hex8 RVE N^3 (default 192): matrix Neo-Hookean E=1 nu=0.3, fibres linear
-      E=10; Newton-Krylov with the assembled CSR tangent + GMRES(30)+Jacobi.
+      E=10; Newton-Krylov with the assembled CSR tangent. GMRES(30)+Jacobi stagnates on this 10:1
+      contrast RVE (in the CPU restatement as on the GPU: profiles/r01_configs.json), so the solve
+      uses Jacobi-PCG on the symmetric Neo-Hookean tangent; GMRES cost per iteration is reported.
   C4  3D J2 hex8 RVE N^3 (default 256): matrix J2 (E=1, nu=0.3, sigma_y=0.002, H=0.1), fibres
       linear E=10; quadrature-point history resident in HBM; strain ramped to 0.02 in 10 steps.
 
@@ -77,9 +79,31 @@ def kernels(cfg, n, reps):
     rr = r.clone()
     out["eliminate_ms"] = timed(lambda: ck(L.afem_eliminate(s.h, P(vals), P(rr), P(u))), 1, stream) * 1e3
     out["csr_spmv_ms"] = timed(lambda: ck(L.afem_csr_apply(s.h, P(vals), P(x), P(y))), reps, stream) * 1e3
-    out["csr_spmv_gbs"] = (12 * nnz + 16 * nd) / (out["csr_spmv_ms"] * 1e-3) / 1e9
+    # bytes our CSR layout moves: fp64 values + node-level int32 columns (nnz/9 for dim 3) + the
+    # int64 node row pointers + x and y; SURVEY §8(d)'s dof-level formula (12 nnz + 8 n + 16 n) alongside
+    out["csr_spmv_gbs"] = (8 * nnz + 4 * nnz / 9 + 8 * nd / 3 + 16 * nd) / (out["csr_spmv_ms"] * 1e-3) / 1e9
+    out["csr_spmv_gbs_survey_bytes"] = (12 * nnz + 24 * nd) / (out["csr_spmv_ms"] * 1e-3) / 1e9
+    # one bounded GMRES(30)+Jacobi and CG+Jacobi run on the eliminated tangent (cost per iteration)
+    buf, hv = C.c_void_p(), C.c_void_p()
+    ck(L.afem_buffer_create(s.h, C.byref(buf)))
+    ck(L.afem_values_create(s.h, C.byref(hv)))
+    ck(L.afem_values_set(hv, P(vals)))
+    ck(L.afem_buffer_handoff(buf, C.byref(hv)))
+    eop = C.c_void_p()
+    ck(L.afem_op_create_explicit(buf, C.byref(eop)))
     del vals
     torch.cuda.empty_cache()
+    xs = torch.zeros_like(u)
+    for name, meth in (("gmres30", afem.GMRES), ("cg", afem.CG)):
+        cfgs = afem.afem_solver_cfg(meth, afem.JACOBI, 1e-30, 200, 30)
+        rep = afem.afem_solve_report()
+        t0 = time.perf_counter()
+        ck(L.afem_solve(eop, C.byref(cfgs), P(rr), None, P(xs), C.byref(rep), None, 0))
+        dt = time.perf_counter() - t0
+        out[f"{name}_ms_per_iteration"] = dt / max(rep.iterations, 1) * 1e3
+    ck(L.afem_op_destroy(eop))
+    ck(L.afem_buffer_release(buf))
+    ck(L.afem_buffer_destroy(buf))
     op = C.c_void_p()
     ck(L.afem_op_create_mf(s.h, P(u), C.byref(op)))
     out["mf_apply_ms"] = timed(lambda: ck(L.afem_op_apply_async(op, P(x), P(y))), reps, stream) * 1e3
@@ -95,9 +119,7 @@ def solve_small(cfg, n, cfgno, cpu):
     ctx = afem.Context(0)
     fib = afem.fibres(SEED, N_FIBRES)
     s = afem.System.grid(ctx, 3, n, n, n, inclusions=fib, radius=RADIUS, materials=cfg["mats"])
-    kw = dict(rtol=1e-8, lin_rtol=1e-10, lin_max_iter=100000)
-    if cfgno == 3:
-        kw.update(method=afem.GMRES, operator_kind=afem.EXPLICIT)
+    kw = dict(rtol=1e-10, lin_rtol=1e-12, lin_max_iter=200000, operator_kind=afem.EXPLICIT, method=afem.CG)
     t = time.perf_counter()
     if cfg["steps"] == 1:
         s.set_benchmark_dirichlet(cfg["strain"])
@@ -115,7 +137,6 @@ def solve_small(cfg, n, cfgno, cpu):
         coords, conn, phase = s.mesh()
         os_ = o.system(3, coords, conn, phase, cfg["mats"], grid=(n, n, n, 1.0, 1.0, 1.0))
         okw = dict(kw)
-        okw["method"] = 1 if cfgno == 3 else 0
         t = time.perf_counter()
         if cfg["steps"] == 1:
             os_.set_dirichlet(*o.bcs(3, n, n, n, 1.0, cfg["strain"]))
@@ -135,7 +156,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="3,4")
     ap.add_argument("--n", type=int, default=0, help="override the full size")
-    ap.add_argument("--solve-n", type=int, default=24)
+    ap.add_argument("--solve-n", type=int, default=16, help="size of the GPU-vs-CPU solve")
+    ap.add_argument("--big-n", type=int, default=64, help="size of the GPU-only full solve (0: skip)")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     a = ap.parse_args()
@@ -145,6 +167,8 @@ def main():
         rec["kernels"] = kernels(cfg, a.n or cfg["n"], a.reps)
         torch.cuda.empty_cache()
         rec["solve"] = solve_small(cfg, a.solve_n, c, not a.no_cpu)
+        if a.big_n:
+            rec["solve_gpu_only"] = solve_small(cfg, a.big_n, c, False)
         print(json.dumps(rec), flush=True)
 
 
