@@ -196,6 +196,9 @@ void solve(Operator& op, const SolverCfg& cfg, const double* b, const double* x0
 // ---- stencil.cu
 StencilPlan* make_stencil_plan(System& s, const MfOp& op);  // nullptr when not applicable
 void stencil_apply(StencilPlan& p, const MfOp& op, const double* x, double* y, double* dot_out = nullptr);
+int stencil_pieces(const StencilPlan& p);
+int stencil_piece_planes(const StencilPlan& p);
+void stencil_apply_pieces(StencilPlan& p, const MfOp& op, const double* x, double* y, int pa, int pb);
 void destroy_stencil_plan(StencilPlan* p);
 
 }  // namespace afem

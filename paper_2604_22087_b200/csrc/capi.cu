@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -373,6 +374,7 @@ afem_status afem_ctx_destroy(afem_ctx ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
+    ctx->c.release_copy_streams();
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
   });
@@ -838,6 +840,45 @@ afem_status afem_op_dim(afem_op op, int64_t* n) {
   });
 }
 
+// Host-buffer apply of a stencil operator, pipelined over z pieces: H2D of piece p+1 (copy stream),
+// the apply of piece p (context stream, once its x planes and the halo plane have landed) and the
+// D2H of piece p-1 (second copy stream) overlap; PCIe runs both directions at once.
+static bool pipelined_host_apply(Operator& o, const double* x, double* y) {
+  static const bool off = std::getenv("AFEM_NO_PIPELINE") != nullptr;
+  auto* mf = dynamic_cast<MfOp*>(&o);
+  if (off || !mf || !mf->stencil || is_device_ptr(x) || is_device_ptr(y)) return false;
+  StencilPlan& pl = *mf->stencil;
+  System& s = *o.sys;
+  Ctx& c = *s.ctx;
+  const int P = stencil_pieces(pl), zp = stencil_piece_planes(pl);
+  if (P < 2) return false;
+  const int64_t plane = 3 * (int64_t)(s.nx + 1) * (s.ny + 1);  // doubles per node plane
+  const int NZ = s.nz + 1;
+  double* dx = static_cast<double*>(c.stage(o.n * 8));
+  double* dy = static_cast<double*>(c.stage(o.n * 8));
+  c.copy_streams(2 * P + 1);
+  cudaEvent_t start = c.events[2 * P];
+  AFEM_CK(cudaEventRecord(start, c.stream));  // earlier work on the staging buffers is done
+  AFEM_CK(cudaStreamWaitEvent(c.s_in, start, 0));
+  AFEM_CK(cudaStreamWaitEvent(c.s_out, start, 0));
+  for (int p = 0; p < P; ++p) {
+    const int64_t a = (int64_t)p * zp * plane, b = std::min<int64_t>((int64_t)(p + 1) * zp, NZ) * plane;
+    AFEM_CK(cudaMemcpyAsync(dx + a, x + a, (b - a) * 8, cudaMemcpyHostToDevice, c.s_in));
+    AFEM_CK(cudaEventRecord(c.events[p], c.s_in));
+  }
+  for (int p = 0; p < P; ++p) {
+    AFEM_CK(cudaStreamWaitEvent(c.stream, c.events[std::min(p + 1, P - 1)], 0));
+    stencil_apply_pieces(pl, *mf, dx, dy, p, p + 1);
+    AFEM_CK(cudaEventRecord(c.events[P + p], c.stream));
+    AFEM_CK(cudaStreamWaitEvent(c.s_out, c.events[P + p], 0));
+    const int64_t a = (int64_t)p * zp * plane, b = std::min<int64_t>((int64_t)(p + 1) * zp, NZ) * plane;
+    AFEM_CK(cudaMemcpyAsync(y + a, dy + a, (b - a) * 8, cudaMemcpyDeviceToHost, c.s_out));
+  }
+  AFEM_CK(cudaStreamSynchronize(c.s_out));
+  AFEM_CK(cudaStreamSynchronize(c.stream));
+  return true;
+}
+
 afem_status afem_op_apply(afem_op op, const double* x, double* y) {
   return guarded([&] {
     need(op, "op");
@@ -846,6 +887,7 @@ afem_status afem_op_apply(afem_op op, const double* x, double* y) {
     Operator& o = *op->op;
     Ctx& c = begin(*o.sys->ctx);
     o.validate();
+    if (pipelined_host_apply(o, x, y)) return;
     In<double> dx(c, x, o.n);
     Out<double> dy(c, y, o.n, false);
     o.apply(dx.d, dy.d);

@@ -79,6 +79,27 @@ struct Ctx {
   // Grow-only staging buffers for host-pointer arguments at the ABI (slot k of the current call).
   std::vector<DevArray<uint8_t>> staging;
   int staging_next = 0;
+  // copy streams + events of the pipelined host-buffer operator apply (created on first use)
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> events;
+  void copy_streams(size_t n_events) {
+    if (!s_in) {
+      AFEM_CK(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+      AFEM_CK(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+    }
+    while (events.size() < n_events) {
+      cudaEvent_t e;
+      AFEM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      events.push_back(e);
+    }
+  }
+  void release_copy_streams() {
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    events.clear();
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+    s_in = s_out = nullptr;
+  }
   void* stage(size_t bytes) {
     if (staging_next >= (int)staging.size()) staging.emplace_back();
     DevArray<uint8_t>& b = staging[staging_next++];

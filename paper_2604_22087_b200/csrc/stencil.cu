@@ -67,6 +67,12 @@ struct StencilPlan {
   int64_t n_fix_nodes = 0, n_edge_nodes = 0;
   int kchunk = 16;
   int nchunks = 1;
+  // z pieces for the pipelined host-buffer apply (afem_op_apply with host x / y): items are
+  // ordered piece-major, piece_items[p] = first item of piece p (multiple of 32)
+  int zpiece = 16;
+  int npieces = 1;
+  std::vector<int64_t> piece_items;
+  int iocc = 1;
 };
 
 namespace {
@@ -208,7 +214,7 @@ template <bool DOT>
 __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ StencilParams P,
                                                         const double* __restrict__ x,
                                                         const uint8_t* __restrict__ info, double* __restrict__ y,
-                                                        int kchunk, DotArgs dot) {
+                                                        int kchunk, int kbeg, int kend, DotArgs dot) {
   double dsum = 0.0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double (*sm)[TY + 2][RS] = reinterpret_cast<double (*)[TY + 2][RS]>(smem_raw);
@@ -217,7 +223,7 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int NX = P.NX, NY = P.NY, NZ = P.NZ;
   const int i0 = blockIdx.x * TXN, j0 = blockIdx.y * TY;
-  const int k0 = blockIdx.z * kchunk, k1 = min(k0 + kchunk, NZ);
+  const int k0 = kbeg + blockIdx.z * kchunk, k1 = min(k0 + kchunk, kend);
   const int i = i0 + 2 * tx, j = j0 + ty;
   const bool active = j < NY;
   const int yf = j == 0 ? 1 : (j == NY - 1 ? 2 : 0);
@@ -716,6 +722,8 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   chunks = std::min(chunks, std::max(1, P.NZ / 8));
   plan->kchunk = (P.NZ + chunks - 1) / chunks;
   plan->nchunks = (P.NZ + plan->kchunk - 1) / plan->kchunk;
+  plan->zpiece = std::max(8, (P.NZ + 7) / 8);  // about 8 pieces
+  plan->npieces = (P.NZ + plan->zpiece - 1) / plan->zpiece;
   const int64_t nn = s.n_nodes;
   plan->info.alloc(nn + 4);  // +4: the main kernel copies the aligned 4-byte word holding a node's byte
   AFEM_CK(cudaMemsetAsync(plan->info.p, 0, nn + 4, c.stream));
@@ -767,7 +775,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
     // in-tile variant writes them), ordered (x tile, y tile, plane, node, octant); padded so that no
     // node's items straddle a 32-item batch.
     const int ntyc = (P.NY + TY - 1) / TY;
-    struct TItem { uint64_t key; uint64_t rec; uint32_t zm; };
+    struct TItem { uint32_t piece; uint64_t key; uint64_t rec; uint32_t zm; };
     std::vector<TItem> ti;
     for (const NodeMask& nm : list) {
       const int ni = static_cast<int>(nm.node % P.NX);
@@ -788,13 +796,24 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
           const bool in = ii >= 0 && ii < P.NX && jj >= 0 && jj < P.NY && kk >= 0 && kk < P.NZ;
           zm |= (in ? (hinfo[ii + (int64_t)P.NX * (jj + (int64_t)P.NY * kk)] & 7u) : 7u) << (3 * m);
         }
-        ti.push_back({(lid << 36) | ((uint64_t)(nj % TY) * TXN + ni % TXN) << 3 | static_cast<uint64_t>(o), rec, zm});
+        ti.push_back({static_cast<uint32_t>(nk / plan->zpiece),
+                      (lid << 36) | ((uint64_t)(nj % TY) * TXN + ni % TXN) << 3 | static_cast<uint64_t>(o), rec, zm});
       }
     }
-    std::sort(ti.begin(), ti.end(), [](const TItem& a, const TItem& b) { return a.key < b.key; });
+    std::sort(ti.begin(), ti.end(), [](const TItem& a, const TItem& b) {
+      return a.piece != b.piece ? a.piece < b.piece : a.key < b.key;
+    });
     std::vector<uint64_t> trec;
     std::vector<uint32_t> tzm;
+    plan->piece_items.assign(1, 0);
     for (size_t q2 = 0; q2 < ti.size();) {
+      while (static_cast<int>(plan->piece_items.size()) <= static_cast<int>(ti[q2].piece)) {
+        while (trec.size() % 32) {  // a piece starts on a batch boundary
+          trec.push_back(kPadRec);
+          tzm.push_back(0);
+        }
+        plan->piece_items.push_back(static_cast<int64_t>(trec.size()));
+      }
       size_t e = q2;  // segment: one target node
       while (e < ti.size() && static_cast<uint32_t>(ti[e].rec) == static_cast<uint32_t>(ti[q2].rec)) ++e;
       const uint64_t L = e - q2;
@@ -814,6 +833,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
       tzm.push_back(0);
     }
     plan->n_items = static_cast<int64_t>(trec.size());
+    while (static_cast<int>(plan->piece_items.size()) <= plan->npieces) plan->piece_items.push_back(plan->n_items);
     plan->it_rec.alloc(std::max<size_t>(trec.size(), 1));
     plan->it_zm.alloc(std::max<size_t>(tzm.size(), 1));
     if (!trec.empty()) {
@@ -826,6 +846,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   plan->part_main.alloc(std::max<int64_t>(nb_main, 1));
   int iocc = 1;  // one wave of resident item CTAs, each walking one contiguous range
   AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&iocc, k_stencil_items<true>, kItemThreads, 0));
+  plan->iocc = std::max(iocc, 1);
   plan->item_blocks = static_cast<int>(
       std::max<int64_t>(1, std::min<int64_t>(plan->n_items / 256, (int64_t)std::max(iocc, 1) * c.num_sms)));
   plan->part_items.alloc(plan->item_blocks);
@@ -844,8 +865,8 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, 
   const int nb_main = P.NXm > 0 ? static_cast<int>(grid.x * grid.y * grid.z) : 0;
   const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main};
   if (P.NXm > 0) {
-    if (dot_out) launch(c, k_stencil_main<true>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot);
-    else launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, dot);
+    if (dot_out) launch(c, k_stencil_main<true>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, 0, P.NZ, dot);
+    else launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, 0, P.NZ, dot);
   }
   if (pl.n_items > 0) {
     const Items it{pl.it_rec.p, pl.it_zm.p, pl.n_items};
@@ -855,6 +876,32 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, 
     else
       launch(c, k_stencil_items<false>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.Kg.p, pl.Ed.p, x, pl.info.p,
              it, y, dot);
+  }
+}
+
+int stencil_pieces(const StencilPlan& pl) { return pl.npieces; }
+int stencil_piece_planes(const StencilPlan& pl) { return pl.zpiece; }
+
+// y over the node planes of z pieces [pa, pb): reads x planes [pa*zpiece - 1, pb*zpiece], writes
+// only y of those planes (bitwise identical to the full apply: same per-node arithmetic order).
+void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, double* y, int pa, int pb) {
+  Ctx& c = *op.sys->ctx;
+  const StencilParams& P = pl.p;
+  const int kb = pa * pl.zpiece, ke = std::min(pb * pl.zpiece, P.NZ);
+  if (kb >= ke) return;
+  const DotArgs dot{nullptr, nullptr, nullptr, nullptr, 0, 0};
+  if (P.NXm > 0) {  // a piece is a few planes: smaller z chunks so the launch still fills the GPU
+    const int tiles = (P.NXm / TXN) * ((P.NY + TY - 1) / TY);
+    const int want = std::max(1, 2 * c.num_sms / std::max(tiles, 1));
+    const int kc = std::max(4, (ke - kb + want - 1) / want);
+    const dim3 grid(P.NXm / TXN, (P.NY + TY - 1) / TY, (ke - kb + kc - 1) / kc);
+    launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, kc, kb, ke, dot);
+  }
+  const int64_t i0 = pl.piece_items[pa], i1 = pl.piece_items[pb];
+  if (i1 > i0) {
+    const Items it{pl.it_rec.p + i0, pl.it_zm.p + i0, i1 - i0};
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((i1 - i0) / 256, (int64_t)pl.iocc * c.num_sms)));
+    launch(c, k_stencil_items<false>, blocks, kItemThreads, 0, P.NX, P.NY, pl.Kg.p, pl.Ed.p, x, pl.info.p, it, y, dot);
   }
 }
 
