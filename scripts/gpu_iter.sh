@@ -11,12 +11,12 @@ d = json.loads(open(f"gpurun_out/bench_{sys.argv[1]}.json").read().strip().split
 print("apply_us", round(d["ms_per_step"] * 1e3, 1), "hbm_frac", round(d["roofline"]["frac"], 3),
       "cg_s", d["cg"]["solve_s"], "cg_it", d["cg"]["iterations"], "e2e", d["e2e"]["value"])
 PY
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_stencil -c 8 python bench.py --steps 3 --warmup 1 --no-cpu --no-cg --e2e-steps 1 > gpurun_out/ncu_$TAG.txt 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_stencil|k_fix" -c 9 python bench.py --steps 3 --warmup 1 --no-cpu --no-cg --e2e-steps 1 > gpurun_out/ncu_$TAG.txt 2>&1
 python - "$TAG" <<'PY'
 import re, sys
 name = None
 for line in open(f"gpurun_out/ncu_{sys.argv[1]}.txt"):
-    m = re.search(r"(k_stencil_\w+<\d>)", line)
+    m = re.search(r"(k_(?:stencil|fix)_\w+)", line)
     if m and "void" in line:
         name = m.group(1)
     elif "gpu__time_duration.sum" in line and name:
