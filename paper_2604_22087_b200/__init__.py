@@ -609,7 +609,18 @@ def slab_range(nz: int, size: int, rank: int):
     return z0.value, z1.value
 
 
+def _nccl_first():
+    """libafem_b200 binds NCCL with dlopen("libnccl.so.2") and reuses an already-loaded copy. Load
+    torch's (the process's NCCL of record) first, so that a later `import torch` does not meet an
+    older system libnccl under the same soname."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
+    _nccl_first()
     buf = C.create_string_buffer(128)
     _check(load().afem_nccl_unique_id(buf))
     return buf.raw
@@ -639,6 +650,7 @@ class Dist:
         L = load()
         h = C.c_void_p()
         if backend == "nccl":
+            _nccl_first()
             buf = C.create_string_buffer(uid, 128)
             _check(L.afem_dist_create_nccl(ctx.h, buf, rank, size, C.byref(h)))
         else:

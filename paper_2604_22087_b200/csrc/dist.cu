@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -45,7 +46,9 @@ static NcclApi& nccl() {
   static NcclApi api;
   static bool loaded = false;
   if (loaded) return api;
+  // the process's NCCL if one is loaded (e.g. torch's), else AFEM_NCCL_LIBRARY, else the default
   void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  if (!h && std::getenv("AFEM_NCCL_LIBRARY")) h = dlopen(std::getenv("AFEM_NCCL_LIBRARY"), RTLD_NOW | RTLD_GLOBAL);
   if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!h) throw std::runtime_error(std::string("NCCL unavailable: ") + dlerror());
   auto sym = [&](const char* n) {
@@ -239,6 +242,14 @@ void DistMfOp::halo_add(double* v, const double* x_for_mask, bool diag_mode) {
   if (hi) copy(c, top, send_hi.p, np);
   comm->exchange(lo ? send_lo.p : nullptr, lo ? recv_lo.p : nullptr, hi ? send_hi.p : nullptr,
                  hi ? recv_hi.p : nullptr, static_cast<size_t>(np), c.stream);
+  halo_finish(v, x_for_mask, diag_mode);
+}
+
+void DistMfOp::halo_finish(double* v, const double* x_for_mask, bool diag_mode) {
+  Ctx& c = *sys->ctx;
+  const int64_t np = plane;
+  const bool lo = comm->rank > 0, hi = comm->rank < comm->size - 1;
+  double* top = v + (n - np);
   const unsigned g = grid_for(np, 256, 148 * 4);
   const bool reset = diag_mode || x_for_mask;  // neither: plain assembly of partial sums
   if (lo) {
@@ -253,9 +264,32 @@ void DistMfOp::halo_add(double* v, const double* x_for_mask, bool diag_mode) {
   }
 }
 
+// Halo exchange overlapped with the interior: the z pieces holding the two shared node planes are
+// applied first, the planes go to the neighbours straight from y on a second stream (NCCL
+// send/recv), the interior pieces run meanwhile on the context stream, which then waits for the
+// exchange and adds the received partial sums. Same arithmetic as apply + halo_add.
 void DistMfOp::apply(const double* x, double* y) {
-  local->apply(x, y);
-  halo_add(y, x, false);
+  StencilPlan* pl = local->stencil;
+  const int P = pl ? stencil_pieces(*pl) : 0;
+  if (comm->size == 1 || P < 3) {
+    local->apply(x, y);
+    halo_add(y, x, false);
+    return;
+  }
+  Ctx& c = *sys->ctx;
+  const int64_t np = plane;
+  const bool lo = comm->rank > 0, hi = comm->rank < comm->size - 1;
+  stencil_apply_pieces(*pl, *local, x, y, 0, 1);
+  stencil_apply_pieces(*pl, *local, x, y, P - 1, P);
+  c.copy_streams(2);
+  AFEM_CK(cudaEventRecord(c.events[0], c.stream));
+  AFEM_CK(cudaStreamWaitEvent(c.s_in, c.events[0], 0));
+  comm->exchange(lo ? y : nullptr, lo ? recv_lo.p : nullptr, hi ? y + (n - np) : nullptr, hi ? recv_hi.p : nullptr,
+                 static_cast<size_t>(np), c.s_in);
+  AFEM_CK(cudaEventRecord(c.events[1], c.s_in));
+  stencil_apply_pieces(*pl, *local, x, y, 1, P - 1);
+  AFEM_CK(cudaStreamWaitEvent(c.stream, c.events[1], 0));
+  halo_finish(y, x, false);
 }
 
 void DistMfOp::diagonal(double* d) { copy(*sys->ctx, diag.p, d, n); }

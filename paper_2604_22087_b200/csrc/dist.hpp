@@ -43,6 +43,8 @@ struct DistMfOp : Operator {
   void diagonal(double* d) override;
   bool uses_stencil() const override { return local && local->uses_stencil(); }
   void halo_add(double* v, const double* x_for_mask, bool diag_mode);
+  // the received neighbour partials added into v's shared planes (+ unit Dirichlet rows)
+  void halo_finish(double* v, const double* x_for_mask, bool diag_mode);
 };
 
 std::unique_ptr<DistMfOp> make_dist_mf_op(System& s, Comm* comm, std::unique_ptr<MfOp> local);

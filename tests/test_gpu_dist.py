@@ -22,10 +22,10 @@ def afem():
     return m
 
 
-def _global(afem):
+def _global(afem, nz=NZ):
     ctx = afem.Context(0)
     fib = afem.fibres(12345, 6)
-    s = afem.System.grid(ctx, 3, NX, NY, NZ, inclusions=fib, radius=0.15, materials=LINEAR)
+    s = afem.System.grid(ctx, 3, NX, NY, nz, inclusions=fib, radius=0.15, materials=LINEAR)
     s.set_benchmark_dirichlet(STRAIN)
     u = s.impose_dirichlet(np.zeros(s.n))
     x = np.random.default_rng(1).uniform(-1, 1, s.n)
@@ -34,14 +34,14 @@ def _global(afem):
     return ctx, fib, s, u, x, op, b
 
 
-def _run_threads(afem, size, fib, x, b, results):
+def _run_threads(afem, size, fib, x, b, results, nz=NZ):
     group = afem.ThreadGroup(size)
     plane = 3 * (NX + 1) * (NY + 1)
 
     def work(rank):
         try:
             ctx = afem.Context(0)
-            sys_, (z0, z1) = afem.slab_system(ctx, NX, NY, NZ, rank, size, inclusions=fib, radius=0.15,
+            sys_, (z0, z1) = afem.slab_system(ctx, NX, NY, nz, rank, size, inclusions=fib, radius=0.15,
                                               materials=LINEAR)
             d = afem.Dist(ctx, rank, size, backend="threads", group=group)
             d.set_benchmark_dirichlet(sys_, STRAIN)
@@ -63,13 +63,15 @@ def _run_threads(afem, size, fib, x, b, results):
     return plane
 
 
-@pytest.mark.parametrize("size", [2, 3])
-def test_threads_backend_matches_single_domain(afem, size):
-    ctx, fib, s, u, x, op, b = _global(afem)
+# nz 24: slabs of <= 13 node planes (one-shot apply, then the plane exchange); nz 64: slabs of
+# >= 3 z pieces, which run the overlapped apply (shared-plane pieces, exchange, interior pieces)
+@pytest.mark.parametrize("size,nz", [(2, 24), (3, 24), (2, 64), (3, 64)])
+def test_threads_backend_matches_single_domain(afem, size, nz):
+    ctx, fib, s, u, x, op, b = _global(afem, nz)
     y_global = op.apply(x)
     xg, rg = afem.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
     results = {}
-    plane = _run_threads(afem, size, fib, x, b, results)
+    plane = _run_threads(afem, size, fib, x, b, results, nz)
     for r in range(size):
         assert not isinstance(results[r], Exception), results[r]
     for r in range(size):
