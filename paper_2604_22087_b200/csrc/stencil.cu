@@ -49,7 +49,7 @@ struct StencilParams {
   double K[24][24];            // uniform-brick element stiffness at E = 1
   double E[32];                // modulus per phase code (E[kVoid] = 0)
   int NX, NY, NZ;              // node counts per axis
-  int NXm;                     // columns covered by 64-wide tiles
+  int NXm;                     // node columns the main kernel covers (tiles of 64; the last may be partial)
 };
 
 struct StencilPlan {
@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
   const int k0 = kbeg + blockIdx.z * kchunk, k1 = min(k0 + kchunk, kend);
   const int i = i0 + 2 * tx, j = j0 + ty;
   const bool active = j < NY;
+  const bool v0 = i < P.NXm, v1 = i + 1 < P.NXm;  // the lane's two nodes exist (ragged last tile)
   const int yf = j == 0 ? 1 : (j == NY - 1 ? 2 : 0);
   const int64_t plane = (int64_t)NX * NY;
 
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
     double xo[6];  // the finishing nodes' raw inputs (Dirichlet rows; the fused dot), issued early
     if constexpr (DOT) {
 #pragma unroll
-      for (int a = 0; a < 6; ++a) xo[a] = __ldg(&x[3 * onode + a]);
+      for (int a = 0; a < 6; ++a) xo[a] = (a < 3 ? v0 : v1) ? __ldg(&x[3 * onode + a]) : 0.0;
     }
     if (active && p >= 0 && p < NZ) {
       const int zc = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
@@ -336,13 +337,13 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
         if constexpr (DOT) {
           const double y0 = ((oi0 >> a) & 1) ? xo[a] : E0 * acc[0][0][a];
           const double y1 = ((oi1 >> a) & 1) ? xo[3 + a] : E1 * acc[1][0][a];
-          yo[a] = y0;
-          yo[3 + a] = y1;
-          dsum = fma(xo[a], y0, dsum);
+          if (v0) yo[a] = y0;
+          if (v1) yo[3 + a] = y1;
+          dsum = fma(xo[a], y0, dsum);  // xo = 0 on missing nodes
           dsum = fma(xo[3 + a], y1, dsum);
         } else {
-          yo[a] = ((oi0 >> a) & 1) ? __ldg(&x[3 * onode + a]) : E0 * acc[0][0][a];
-          yo[3 + a] = ((oi1 >> a) & 1) ? __ldg(&x[3 * onode + 3 + a]) : E1 * acc[1][0][a];
+          if (v0) yo[a] = ((oi0 >> a) & 1) ? __ldg(&x[3 * onode + a]) : E0 * acc[0][0][a];
+          if (v1) yo[3 + a] = ((oi1 >> a) & 1) ? __ldg(&x[3 * onode + 3 + a]) : E1 * acc[1][0][a];
         }
       }
     }
@@ -634,7 +635,9 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   P.NX = s.nx + 1;
   P.NY = s.ny + 1;
   P.NZ = s.nz + 1;
-  P.NXm = (P.NX / TXN) * TXN;
+  // A ragged last tile of >= 8 columns runs in the main kernel (masked lanes); narrower remainders
+  // go to the correction items as edge columns (a mostly idle 64-wide tile would cost more).
+  P.NXm = (P.NX % TXN) >= 8 ? P.NX : (P.NX / TXN) * TXN;
   for (int k = 0; k < 32; ++k) P.E[k] = 0.0;
   for (size_t k = 0; k < s.mats.size(); ++k) P.E[k] = s.mats[k].E;
 
@@ -717,7 +720,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   int occ = 1;
   AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<true>, NT, kMainSmem));
   const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
-  const int64_t tiles = (int64_t)(P.NXm / TXN) * ((P.NY + TY - 1) / TY);
+  const int64_t tiles = (int64_t)((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY);
   int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
   chunks = std::min(chunks, std::max(1, P.NZ / 8));
   plan->kchunk = (P.NZ + chunks - 1) / chunks;
@@ -842,7 +845,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
     }
     AFEM_CK(cudaStreamSynchronize(c.stream));
   }
-  const int64_t nb_main = (int64_t)(P.NXm / TXN) * ((P.NY + TY - 1) / TY) * plan->nchunks;
+  const int64_t nb_main = (int64_t)((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY) * plan->nchunks;
   plan->part_main.alloc(std::max<int64_t>(nb_main, 1));
   int iocc = 1;  // one wave of resident item CTAs, each walking one contiguous range
   AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&iocc, k_stencil_items<true>, kItemThreads, 0));
@@ -861,7 +864,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
 void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, double* dot_out) {
   Ctx& c = *op.sys->ctx;
   const StencilParams& P = pl.p;
-  const dim3 grid(P.NXm / TXN, (P.NY + TY - 1) / TY, pl.nchunks);
+  const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TY - 1) / TY, pl.nchunks);
   const int nb_main = P.NXm > 0 ? static_cast<int>(grid.x * grid.y * grid.z) : 0;
   const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main};
   if (P.NXm > 0) {
@@ -891,10 +894,10 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
   if (kb >= ke) return;
   const DotArgs dot{nullptr, nullptr, nullptr, nullptr, 0, 0};
   if (P.NXm > 0) {  // a piece is a few planes: smaller z chunks so the launch still fills the GPU
-    const int tiles = (P.NXm / TXN) * ((P.NY + TY - 1) / TY);
+    const int tiles = ((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY);
     const int want = std::max(1, 2 * c.num_sms / std::max(tiles, 1));
     const int kc = std::max(4, (ke - kb + want - 1) / want);
-    const dim3 grid(P.NXm / TXN, (P.NY + TY - 1) / TY, (ke - kb + kc - 1) / kc);
+    const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TY - 1) / TY, (ke - kb + kc - 1) / kc);
     launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, kc, kb, ke, dot);
   }
   const int64_t i0 = pl.piece_items[pa], i1 = pl.piece_items[pb];

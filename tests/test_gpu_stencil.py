@@ -48,9 +48,9 @@ def test_stencil_matches_oracle(afem, ctx, n):
     assert rel_err(op.diagonal(), o.mf_diagonal(u)) <= TOL
 
 
-# NX = nx+1 nodes: >= 65 runs the 64-wide main kernel plus edge-column items (NX mod 64 of them);
-# NX < 65 is edge-only (every node through the correction-item kernel).
-@pytest.mark.parametrize("shape", [(64, 17, 20), (70, 9, 31), (64, 64, 7), (127, 12, 10), (128, 9, 17),
+# NX = nx+1 nodes: 64-wide main-kernel tiles; a ragged remainder of >= 8 columns runs as a masked
+# last tile (100, 160, 33, 31), a narrower one through the correction items as edge columns.
+@pytest.mark.parametrize("shape", [(64, 17, 20), (70, 9, 31), (64, 64, 7), (127, 12, 10), (128, 9, 17), (100, 9, 13), (160, 11, 9),
                                    (33, 17, 20), (31, 31, 31)])
 def test_stencil_matches_general_kernel(afem, ctx, shape):
     nx, ny, nz = shape
@@ -73,7 +73,7 @@ def test_stencil_matches_general_kernel(afem, ctx, shape):
         assert rel_err(ops.apply(x), opg.apply(x)) <= TOL
 
 
-@pytest.mark.parametrize("shape", [(64, 17, 20), (70, 9, 31)])
+@pytest.mark.parametrize("shape", [(64, 17, 20), (70, 9, 31), (100, 9, 13)])
 def test_stencil_misaligned_device_input_and_determinism(afem, ctx, shape):
     """Device inputs only 8-byte aligned (a tensor view at offset 1) give the same result as host
     inputs (the correction kernel reads node records as 16 + 8 bytes), and repeated applies are
