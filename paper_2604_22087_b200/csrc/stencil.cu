@@ -383,7 +383,8 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
 // straddle a batch; the head sums them with fixed-order shuffles and updates y directly.
 // Deterministic (fixed batch -> CTA mapping, fixed shuffle order), no atomics, no barriers.
 // rec: node (low 32 bits, -1 = padding) | oct << 32 | seg << 35 | edge << 39 | pho << 40 |
-// phb << 45; zm: bit 3m+b = input b of element corner m is zero (Dirichlet or outside).
+// phb << 45 | rem << 50 (items left in the segment, this one included); zm: bit 3m+b = input b of
+// element corner m is zero (Dirichlet or outside).
 constexpr int kItemThreads = 256;
 constexpr uint64_t kPadRec = 0xffffffffull;
 
@@ -474,12 +475,15 @@ __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, 
       r1 *= dE;
       r2 *= dE;
     }
+    // segmented tree sum: rem = items from this lane to its segment's end (<= 8, never crossing the
+    // batch); after the step with offset d every lane holds the sum of [lane, min(lane + 2d, end))
+    const int rem = static_cast<int>((rec >> 50) & 15);
 #pragma unroll
-    for (int d = 1; d < 8; ++d) {
+    for (int d = 1; d < 8; d <<= 1) {
       const double v0 = __shfl_down_sync(0xffffffffu, r0, d);
       const double v1 = __shfl_down_sync(0xffffffffu, r1, d);
       const double v2 = __shfl_down_sync(0xffffffffu, r2, d);
-      if (d < L) {  // segments never cross the batch, so lane + d < 32 here
+      if (d < rem) {
         r0 += v0;
         r1 += v1;
         r2 += v2;
@@ -826,7 +830,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
           tzm.push_back(0);
         }
       for (size_t t = q2; t < e; ++t) {
-        trec.push_back(ti[t].rec | (t == q2 ? (L << 35) : 0ull));
+        trec.push_back(ti[t].rec | (t == q2 ? (L << 35) : 0ull) | (static_cast<uint64_t>(e - t) << 50));
         tzm.push_back(ti[t].zm);
       }
       q2 = e;
