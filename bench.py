@@ -6,7 +6,9 @@ Workload (BASELINE.json configs[1], "config 2"): 3D linear-elastic hex8 RVE, 128
 benchmark BCs at 1% strain, state u0 = BC-consistent; fp64 matrix-free K(u0) x and Jacobi-PCG.
 
   step      one matrix-free operator apply y = K x over the whole mesh (inputs resident in HBM);
-            L2 is flushed (256 MiB write) between timed applies, outside the timed events
+            L2 is flushed between timed applies, outside the timed events, by streaming a 256 MiB
+            buffer through it (written once, read before every apply, so L2 holds clean lines and
+            the apply does not pay the write-back of the flush)
   value     whole-job DOFs/s = n_dof * steps * n_gpus / max-over-ranks(sum of apply times)
   e2e       the same metric through the C ABI (afem_op_apply) with pinned HOST x/y buffers:
             H2D of x and D2H of y inside every step
@@ -219,7 +221,8 @@ def ours(args, rank, world, local_rank):
     g = torch.Generator(device="cuda").manual_seed(SEED + rank)
     x = torch.rand(n_dof, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
     y = torch.empty_like(x)
-    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    flush = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    sink = torch.empty((), dtype=torch.float64, device="cuda")
 
     for _ in range(args.warmup):
         op.apply_device(x.data_ptr(), y.data_ptr())
@@ -233,7 +236,7 @@ def ours(args, rank, world, local_rank):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     l0 = ctx.launches
     for k in range(args.steps):
-        flush.fill_(float(k))
+        torch.sum(flush, dim=0, out=sink)  # read-only L2 flush
         evs[k][0].record(stream)
         op.apply_device(x.data_ptr(), y.data_ptr())
         evs[k][1].record(stream)
@@ -340,7 +343,7 @@ def ours(args, rank, world, local_rank):
         "config": {"workload": f"C2 hex8 {n}^3 linear-elastic fibre RVE, matrix-free K(u0)x + Jacobi-PCG",
                    "elements": n_elem, "n_dof": n_dof, "nnz_K": sys_.nnz, "fibres": N_FIBRES, "radius": RADIUS,
                    "fibre_volume_fraction": vf, "E": [1.0, 10.0], "nu": 0.3, "strain": STRAIN,
-                   "l2": "flushed (256 MiB write) between timed applies",
+                   "l2": "flushed between timed applies (256 MiB buffer read through L2)",
                    "global_dofs": global_dofs,
                    "parallelism": (f"z-slab decomposition over {world} GPUs (NCCL plane halo + allreduce), "
                                    f"{n} element layers per GPU" if world > 1 else "1 GPU")},
