@@ -113,6 +113,8 @@ struct Operator {
   virtual bool apply_dot(const double*, double*, double*) { return false; }
   virtual void diagonal(double* d) = 0;                 // device pointer
   virtual bool uses_stencil() const { return false; }
+  // pattern-ordered CSR values when the operator is the assembled matrix (persistent small-n CG)
+  virtual const double* csr_values() const { return nullptr; }
 };
 
 struct ExplicitOp : Operator {
@@ -121,6 +123,7 @@ struct ExplicitOp : Operator {
   void validate() const override;
   void apply(const double* x, double* y) override;
   void diagonal(double* d) override;
+  const double* csr_values() const override { return buf->store.p; }
 };
 
 struct MfOp : Operator {

@@ -9,8 +9,15 @@
 // convergence on the recurrence residual, then re-verification with a fresh apply and a restart
 // from the true residual if the recurrence drifted; pAp <= 0 reports a failure string;
 // b = 0 uses an absolute test.
+// Small assembled systems (config 1 is 8 450 dofs) are launch-latency bound: there the whole
+// iteration loop runs in ONE persistent cooperative kernel (CSR SpMV warp-per-node, the x/r/z
+// update and the p update, three grid syncs per iteration; every block reduces the per-block
+// partials in the same fixed order, so the scalars are identical everywhere and deterministic).
+#include <cooperative_groups.h>
+
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "afem_impl.hpp"
@@ -180,6 +187,171 @@ __global__ void k_scale_into(const double* w, double inv_s, double* v, int64_t n
     v[i] = w[i] / inv_s;
 }
 
+
+// Block sum of NV values (all threads get the result).
+template <int NV>
+__device__ __forceinline__ void block_allsum(double (&v)[NV], double* sh /* NV * 32 */) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double t = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) sh[k * 32 + w] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double t = lane < nw ? sh[k * 32 + lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    v[k] = t;
+  }
+  __syncthreads();
+}
+
+// Fixed-order sum of gridDim.x partials (stride NV), identical in every block.
+template <int NV>
+__device__ __forceinline__ void grid_partials_sum(const double* part, double (&v)[NV], double* sh) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += __ldcg(&part[b * NV + k]);
+  block_allsum<NV>(v, sh);
+}
+
+// The whole Jacobi-PCG iteration loop for an assembled (CSR) operator; st holds rz etc. from
+// k_cg_start. Writes hist[it] per iteration and the final state back to st.
+template <int D>
+__global__ void __launch_bounds__(256) k_cg_persistent(SysView s, const double* __restrict__ vals, double* x,
+                                                       double* r, double* p, double* ap, const double* inv,
+                                                       int64_t n, CgDev* st, double* hist, double* part_a,
+                                                       double* part_b) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[2 * 32];
+  const int lane = threadIdx.x & 31;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t warp = tid >> 5, nwarps = nth >> 5;
+  double rz = st->rz;
+  const double denom = st->denom, rtol = st->rtol;
+  const int max_iter = st->max_iter;
+  int it = st->it, fail = 0, conv = 0;
+  while (true) {
+    // (1) ap = A p, one warp per node (its D rows are contiguous), and p.ap
+    double pap_loc = 0.0;
+    for (int64_t nd = warp; nd < s.n_nodes; nd += nwarps) {
+      const int64_t a0 = s.adj_ptr[nd];
+      const int deg = static_cast<int>(s.adj_ptr[nd + 1] - a0);
+      const int len = D * deg;
+      double acc[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) acc[a] = 0.0;
+      for (int jj = lane; jj < len; jj += 32) {
+        const double xv = __ldcg(&p[(int64_t)D * s.adj[a0 + jj / D] + jj % D]);
+#pragma unroll
+        for (int a = 0; a < D; ++a) acc[a] += vals[(int64_t)D * D * a0 + (int64_t)a * len + jj] * xv;
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        double v = acc[a];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) {
+          ap[D * nd + a] = v;
+          pap_loc += __ldcg(&p[D * nd + a]) * v;
+        }
+      }
+    }
+    double t1[1] = {pap_loc};
+    block_allsum<1>(t1, sh);
+    if (threadIdx.x == 0) part_a[blockIdx.x] = t1[0];
+    grid.sync();
+    grid_partials_sum<1>(part_a, t1, sh);
+    const double pap = t1[0];
+    if (!(pap > 0.0)) {  // krylov.hpp:377-381
+      fail = 1;
+      break;
+    }
+    const double alpha = rz / pap;
+    // (2) x += alpha p; r -= alpha ap; (r.r, r.z)
+    double rr = 0.0, rzn = 0.0;
+    for (int64_t i = tid; i < n; i += nth) {
+      const double pi = __ldcg(&p[i]);
+      x[i] += alpha * pi;
+      const double ri = r[i] - alpha * __ldcg(&ap[i]);
+      r[i] = ri;
+      const double zi = inv ? ri * inv[i] : ri;
+      rr += ri * ri;
+      rzn += ri * zi;
+    }
+    double t2[2] = {rr, rzn};
+    block_allsum<2>(t2, sh);
+    if (threadIdx.x == 0) {
+      part_b[2 * blockIdx.x] = t2[0];
+      part_b[2 * blockIdx.x + 1] = t2[1];
+    }
+    grid.sync();
+    grid_partials_sum<2>(part_b, t2, sh);
+    ++it;
+    const double h = sqrt(t2[0]) / denom;
+    if (blockIdx.x == 0 && threadIdx.x == 0) hist[it] = h;
+    if (h <= rtol) {
+      conv = 1;
+      break;
+    }
+    const double beta = t2[1] / rz;
+    rz = t2[1];
+    if (it >= max_iter) break;
+    // (3) p = z + beta p (same element mapping as (2): own elements only)
+    for (int64_t i = tid; i < n; i += nth) {
+      const double zi = inv ? r[i] * inv[i] : r[i];
+      p[i] = zi + beta * __ldcg(&p[i]);
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->it = it;
+    st->rz = rz;
+    st->fail = fail;
+    st->conv = conv;
+    st->done = 1;
+  }
+}
+
+// Cooperative launch of k_cg_persistent (false when the device / size does not qualify).
+bool cg_persistent(Operator& op, double* x, double* r, double* p, double* ap, const double* inv, CgDev* st,
+                   double* hist) {
+  static const bool off = std::getenv("AFEM_NO_PERSISTENT_CG") != nullptr;
+  const double* vals = op.csr_values();
+  System& s = *op.sys;
+  Ctx& c = *s.ctx;
+  if (off || !vals || op.n > (int64_t)1 << 21) return false;
+  int coop = 0;
+  AFEM_CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c.device));
+  if (!coop) return false;
+  auto kern = s.dim == 2 ? k_cg_persistent<2> : k_cg_persistent<3>;
+  int per_sm = 0;
+  AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+  if (per_sm < 1) return false;
+  // one warp per node, at most two blocks per SM (measured best on config 1: 10.4 us per iteration)
+  static const int cap = std::getenv("AFEM_PCG_BLOCKS") ? std::atoi(std::getenv("AFEM_PCG_BLOCKS")) : 2 * c.num_sms;
+  const int64_t want = (s.n_nodes * 32 + 255) / 256;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, cap),
+                                                                               (int64_t)per_sm * c.num_sms)));
+  static thread_local DevArray<double> parts;
+  if (parts.n < (size_t)3 * blocks) parts.alloc(3 * (size_t)blocks);
+  SysView v = s.view();
+  int64_t n = op.n;
+  double* part_a = parts.p;
+  double* part_b = parts.p + blocks;
+  void* args[] = {&v, (void*)&vals, &x, &r, &p, &ap, (void*)&inv, &n, &st, &hist, &part_a, &part_b};
+  AFEM_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), blocks, 256, args, 0, c.stream));
+  ++c.launches;
+  return true;
+}
+
 struct Timer {
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   double seconds() const { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
@@ -236,7 +408,9 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
     if (rep.history.back() > cfg.rtol && rep.iterations < cfg.max_iter) {
       launch(c, k_cg_start, rg, kRedThreads, 0, r.p, inv, p.p, n, c.red_partials.p, c.red_counter.p, st.p);
       int chunk = 4;
-      while (true) {
+      if (cg_persistent(op, x, r.p, p.p, ap.p, inv, st.p, hist.p)) {
+        hs = fetch(c, st.p);
+      } else while (true) {
         for (int k = 0; k < chunk; ++k) {
           // fused operators write p^T A p straight into st->pap; others get the reduction kernel
           double* pap_dev = reinterpret_cast<double*>(reinterpret_cast<char*>(st.p) + offsetof(CgDev, pap));
