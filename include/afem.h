@@ -68,7 +68,8 @@ typedef struct {
   double hardening;
 } afem_material;
 
-/* SolverConfig (krylov.hpp:43-55). method: 0 CG, 1 GMRES; precond: 0 NONE, 1 JACOBI. */
+/* SolverConfig (krylov.hpp:43-55). method: 0 CG, 1 GMRES, 2 BICGSTAB; precond: 0 NONE, 1 JACOBI.
+ * ILU0 and the direct methods are not on the device path (AFEM_E_CAPABILITY). */
 typedef struct {
   int32_t method;
   int32_t precond;
@@ -235,7 +236,8 @@ afem_status afem_op_csr_values(afem_op op, double** values_dev);
 afem_status afem_op_uses_stencil(afem_op op, int32_t* flag);
 
 /* ------------------------------------------------------------------ solvers (L5) */
-/* run_solver (backend.hpp:241-286) / cg (krylov.hpp:350-408) / gmres (krylov.hpp:415-530).
+/* run_solver (backend.hpp:241-286) / cg (krylov.hpp:350-408) / gmres (krylov.hpp:415-530) /
+ * bicgstab (krylov.hpp:535-620).
  * x0 may be NULL (zero start). history: caller buffer of hist_cap doubles (may be NULL). */
 afem_status afem_solve(afem_op op, const afem_solver_cfg* cfg, const double* b, const double* x0,
                        double* x, afem_solve_report* rep, double* history, int32_t hist_cap);

@@ -1047,13 +1047,94 @@ inline std::vector<double> gmres(const Operator& a, const double* b, const Solve
 }
 
 // run_solver (backend.hpp:241-286), iterative branch
+
+// bicgstab (krylov.hpp:535-620): unpreconditioned recurrence residual, rho / rhat.v / omega
+// breakdowns reported as failures, early exit on a small s, true-residual re-verification with a
+// restart from the fresh residual.
+inline std::vector<double> bicgstab(const Operator& a, const double* b, const SolverConfig& cfg, const Precond& m,
+                                    const double* x0, SolveReport& rep) {
+  cfg.validate();
+  Timer timer;
+  const std::size_t n = a.dim();
+  std::vector<double> x = x0 ? std::vector<double>(x0, x0 + n) : std::vector<double>(n, 0.0);
+  const double bnorm = norm2(b, n);
+  const double denom = bnorm > 0.0 ? bnorm : 1.0;
+  std::vector<double> r(n), rhat(n), p(n, 0.0), v(n, 0.0), s(n), t(n), phat(n), shat(n), scratch;
+  a.apply(x.data(), t.data());
+  for (std::size_t i = 0; i < n; ++i) r[i] = b[i] - t[i];
+  rhat = r;
+  rep.residual_history.push_back(norm2(r.data(), n) / denom);
+  while (true) {
+    double rho = 1.0, alpha = 1.0, omega = 1.0;
+    while (rep.residual_history.back() > cfg.rtol && rep.iterations < cfg.max_iter) {
+      const double rho_new = dot(rhat.data(), r.data(), n);
+      if (rho_new == 0.0) {
+        rep.failure = "bicgstab: rho breakdown at iteration " + std::to_string(rep.iterations + 1);
+        break;
+      }
+      const double beta = (rho_new / rho) * (alpha / omega);
+      rho = rho_new;
+      for (std::size_t i = 0; i < n; ++i) p[i] = r[i] + beta * (p[i] - omega * v[i]);
+      m.apply(p.data(), phat.data(), n);
+      a.apply(phat.data(), v.data());
+      const double rhat_v = dot(rhat.data(), v.data(), n);
+      if (rhat_v == 0.0) {
+        rep.failure = "bicgstab: rhat^T v breakdown at iteration " + std::to_string(rep.iterations + 1);
+        break;
+      }
+      alpha = rho / rhat_v;
+      for (std::size_t i = 0; i < n; ++i) s[i] = r[i] - alpha * v[i];
+      if (norm2(s.data(), n) / denom <= cfg.rtol) {
+        axpy(alpha, phat.data(), x.data(), n);
+        r = s;
+        ++rep.iterations;
+        rep.residual_history.push_back(norm2(r.data(), n) / denom);
+        break;
+      }
+      m.apply(s.data(), shat.data(), n);
+      a.apply(shat.data(), t.data());
+      const double tt = dot(t.data(), t.data(), n);
+      if (tt == 0.0) {
+        rep.failure = "bicgstab: omega breakdown (t = 0) at iteration " + std::to_string(rep.iterations + 1);
+        break;
+      }
+      omega = dot(t.data(), s.data(), n) / tt;
+      if (omega == 0.0) {
+        rep.failure = "bicgstab: omega breakdown at iteration " + std::to_string(rep.iterations + 1);
+        break;
+      }
+      for (std::size_t i = 0; i < n; ++i) {
+        x[i] += alpha * phat[i] + omega * shat[i];
+        r[i] = s[i] - omega * t[i];
+      }
+      ++rep.iterations;
+      rep.residual_history.push_back(norm2(r.data(), n) / denom);
+    }
+    const double true_rres = true_relative_residual(a, b, x.data(), denom, scratch);
+    rep.residual_history.back() = true_rres;
+    if (true_rres <= cfg.rtol) {
+      rep.converged = rep.failure.empty();
+      break;
+    }
+    if (!rep.failure.empty() || rep.iterations >= cfg.max_iter) break;
+    a.apply(x.data(), t.data());
+    for (std::size_t i = 0; i < n; ++i) r[i] = b[i] - t[i];
+    rhat = r;
+    std::fill(p.begin(), p.end(), 0.0);
+    std::fill(v.begin(), v.end(), 0.0);
+  }
+  rep.wall_time = timer.seconds();
+  return x;
+}
+
 inline std::vector<double> run_solver(const Operator& op, const double* b, const SolverConfig& cfg,
                                       const double* x0, SolveReport& rep) {
   cfg.validate();
-  if (cfg.method != 0 && cfg.method != 1) throw std::invalid_argument("run_solver: only CG and GMRES are restated");
+  if (cfg.method < 0 || cfg.method > 2) throw std::invalid_argument("run_solver: only CG, GMRES and BiCGStab are restated");
   Precond m;
   if (cfg.precond == 1) m = Precond::from_diagonal(op.diagonal());
   else if (cfg.precond != 0) throw CapabilityError("run_solver: preconditioner not restated");
+  if (cfg.method == 2) return bicgstab(op, b, cfg, m, x0, rep);
   return cfg.method == 0 ? cg(op, b, cfg, m, x0, rep) : gmres(op, b, cfg, m, x0, rep);
 }
 

@@ -352,6 +352,29 @@ bool cg_persistent(Operator& op, double* x, double* r, double* p, double* ap, co
   return true;
 }
 
+
+// BiCGStab vector steps (krylov.hpp:557-598)
+__global__ void k_bicg_p(const double* __restrict__ r, double* __restrict__ p, const double* __restrict__ v, double beta,
+                         double omega, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = r[i] + beta * (p[i] - omega * v[i]);
+}
+
+__global__ void k_bicg_s(const double* __restrict__ r, const double* __restrict__ v, double alpha, double* __restrict__ s,
+                         int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s[i] = r[i] - alpha * v[i];
+}
+
+__global__ void k_bicg_xr(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ phat,
+                          const double* __restrict__ shat, const double* __restrict__ s, const double* __restrict__ t,
+                          double alpha, double omega, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += alpha * phat[i] + omega * shat[i];
+    r[i] = s[i] - omega * t[i];
+  }
+}
+
 struct Timer {
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   double seconds() const { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
@@ -544,6 +567,77 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
   rep.converged = rep.failure.empty() && true_rres <= cfg.rtol;
 }
 
+// bicgstab (krylov.hpp:535-620): scalars on the host (one sync per dot); same breakdown messages,
+// early exit on a small s, true-residual re-verification and restart from the fresh residual.
+void bicgstab(Operator& op, const SolverCfg& cfg, const double* b, double* x, const double* inv, SolveReport& rep) {
+  Ctx& c = *op.sys->ctx;
+  const int64_t n = op.n;
+  const unsigned eg = grid_for(n, 256, 148 * 16);
+  DevArray<double> r(n), rhat(n), p(n), v(n), sv(n), t(n), phat(n), shat(n);
+  fill(c, 0.0, p.p, n);
+  fill(c, 0.0, v.p, n);
+  const double bnorm = std::sqrt(dot(c, b, b, n));
+  const double denom = bnorm > 0.0 ? bnorm : 1.0;
+  rep.history.push_back(residual_norm(op, b, x, t.p, r.p) / denom);
+  copy(c, r.p, rhat.p, n);
+  auto precond = [&](const double* in, double* out) { launch(c, k_precond, eg, 256, 0, in, inv, out, n); };
+  while (true) {
+    double rho = 1.0, alpha = 1.0, omega = 1.0;
+    while (rep.history.back() > cfg.rtol && rep.iterations < cfg.max_iter) {
+      const double rho_new = dot(c, rhat.p, r.p, n);
+      if (rho_new == 0.0) {
+        rep.failure = "bicgstab: rho breakdown at iteration " + std::to_string(rep.iterations + 1);
+        break;
+      }
+      const double beta = (rho_new / rho) * (alpha / omega);
+      rho = rho_new;
+      launch(c, k_bicg_p, eg, 256, 0, r.p, p.p, v.p, beta, omega, n);
+      precond(p.p, phat.p);
+      op.apply(phat.p, v.p);
+      const double rhat_v = dot(c, rhat.p, v.p, n);
+      if (rhat_v == 0.0) {
+        rep.failure = "bicgstab: rhat^T v breakdown at iteration " + std::to_string(rep.iterations + 1);
+        break;
+      }
+      alpha = rho / rhat_v;
+      launch(c, k_bicg_s, eg, 256, 0, r.p, v.p, alpha, sv.p, n);
+      if (std::sqrt(dot(c, sv.p, sv.p, n)) / denom <= cfg.rtol) {
+        axpy(c, alpha, phat.p, x, n);
+        copy(c, sv.p, r.p, n);
+        ++rep.iterations;
+        rep.history.push_back(std::sqrt(dot(c, r.p, r.p, n)) / denom);
+        break;
+      }
+      precond(sv.p, shat.p);
+      op.apply(shat.p, t.p);
+      const double tt = dot(c, t.p, t.p, n);
+      if (tt == 0.0) {
+        rep.failure = "bicgstab: omega breakdown (t = 0) at iteration " + std::to_string(rep.iterations + 1);
+        break;
+      }
+      omega = dot(c, t.p, sv.p, n) / tt;
+      if (omega == 0.0) {
+        rep.failure = "bicgstab: omega breakdown at iteration " + std::to_string(rep.iterations + 1);
+        break;
+      }
+      launch(c, k_bicg_xr, eg, 256, 0, x, r.p, phat.p, shat.p, sv.p, t.p, alpha, omega, n);
+      ++rep.iterations;
+      rep.history.push_back(std::sqrt(dot(c, r.p, r.p, n)) / denom);
+    }
+    const double true_rres = residual_norm(op, b, x, t.p, nullptr) / denom;
+    rep.history.back() = true_rres;
+    if (true_rres <= cfg.rtol) {
+      rep.converged = rep.failure.empty();
+      break;
+    }
+    if (!rep.failure.empty() || rep.iterations >= cfg.max_iter) break;
+    residual_norm(op, b, x, t.p, r.p);  // restart from the fresh residual (krylov.hpp:611-616)
+    copy(c, r.p, rhat.p, n);
+    fill(c, 0.0, p.p, n);
+    fill(c, 0.0, v.p, n);
+  }
+}
+
 }  // namespace
 
 void validate_cfg(const SolverCfg& c) {  // SolverConfig::validate (krylov.hpp:50-54)
@@ -555,8 +649,8 @@ void validate_cfg(const SolverCfg& c) {  // SolverConfig::validate (krylov.hpp:5
 // run_solver (backend.hpp:241-286), iterative methods. x0 may alias x.
 void solve(Operator& op, const SolverCfg& cfg, const double* b, const double* x0, double* x, SolveReport& rep) {
   validate_cfg(cfg);
-  if (cfg.method != 0 && cfg.method != 1)
-    throw CapabilityError("run_solver: only CG and GMRES are provided on the device");
+  if (cfg.method < 0 || cfg.method > 2)
+    throw CapabilityError("run_solver: CG, GMRES and BiCGStab are provided on the device");
   if (cfg.precond != 0 && cfg.precond != 1) throw CapabilityError("run_solver: ILU0 is not provided on the device");
   op.validate();
   Timer timer;
@@ -573,7 +667,8 @@ void solve(Operator& op, const SolverCfg& cfg, const double* b, const double* x0
   if (x0) copy(c, x0, xw, op.n);
   else fill(c, 0.0, xw, op.n);
   if (cfg.method == 0) cg(op, cfg, b, xw, inv.p, rep);
-  else gmres(op, cfg, b, xw, inv.p, rep);
+  else if (cfg.method == 1) gmres(op, cfg, b, xw, inv.p, rep);
+  else bicgstab(op, cfg, b, xw, inv.p, rep);
   if (xw != x) copy(c, xw, x, op.n);
   AFEM_CK(cudaStreamSynchronize(c.stream));
   rep.wall_time = timer.seconds();

@@ -282,3 +282,42 @@ def test_linear_newton_takes_one_iteration(afem, ctx):
     u, rep = s.solve_bvp(rtol=1e-10, lin_rtol=1e-13)
     assert rep["converged"] and rep["iterations"] == 1
     assert rep["residual_norms"][-1] <= 10 * 1e-13 * rep["residual_norms"][0]
+
+
+@pytest.mark.parametrize("precond", [0, 1], ids=["none", "jacobi"])
+def test_bicgstab_against_reference_library(afem, ctx, precond):
+    """BiCGStab (krylov.hpp:535-620) on the device vs the reference library on config-1 style systems:
+    converged, iteration counts within 5 % (BiCGStab's count is rounding-sensitive: the device dots
+    reduce in a different order), x within 1e-8 at the reference's default rtol 1e-13."""
+    R = Oracle("ref")
+    mats = LINEAR
+    s = afem.System.grid(ctx, 2, 32, 32, materials=mats)
+    s.set_benchmark_dirichlet(0.01)
+    o = R.system(2, *s.mesh(), mats, grid=(32, 32, 0, 1.0, 1.0, 1.0))
+    o.set_dirichlet(*R.bcs(2, 32, 32, 0, 1.0, 0.01))
+    u = s.impose_dirichlet(random_vector(s.n, 0.01, 3))
+    vals = afem.Values(s).assemble(u)
+    rhs = -vals.eliminate(s.residual(u), u)
+    buf = afem.HandoffBuffer(s)
+    buf.handoff(vals)
+    op = afem.explicit_operator(buf)
+    xd, rd = afem.run_solver(op, rhs, method=afem.BICGSTAB, precond=precond, rtol=1e-13, max_iter=20000)
+    v, r = o.eliminate(o.jacobian(u), o.residual(u), u)
+    xr, rr = o.solve(0, v, -r, method=2, precond=precond, rtol=1e-13, max_iter=20000)
+    assert rd["converged"] and rr["converged"]
+    assert abs(rd["iterations"] - rr["iterations"]) <= max(2, rr["iterations"] // 20)
+    assert rel_err(xd, xr) <= TOL_U
+    buf.release()
+    # matrix-free too (hex8 vs the restatement)
+    fib = afem.fibres(12345, 4)
+    s3 = afem.System.grid(ctx, 3, 6, 6, 6, inclusions=fib, radius=0.2, materials=SVK_MIX)
+    s3.set_benchmark_dirichlet(0.01)
+    orc = Oracle("restate")
+    o3 = orc.system(3, *s3.mesh(), SVK_MIX, grid=(6, 6, 6, 1.0, 1.0, 1.0))
+    o3.set_dirichlet(*orc.bcs(3, 6, 6, 6, 1.0, 0.01))
+    u3 = s3.impose_dirichlet(random_vector(s3.n, 0.01, 4))
+    b3 = -s3.constrain_residual(s3.residual(u3), u3)
+    x3, r3 = afem.run_solver(afem.matrix_free_operator(s3, u3), b3, method=afem.BICGSTAB, precond=precond,
+                             rtol=1e-12, max_iter=20000)
+    xo, ro = o3.solve(1, u3, b3, method=2, precond=precond, rtol=1e-12, max_iter=20000)
+    assert r3["converged"] and ro["converged"] and rel_err(x3, xo) <= TOL_U

@@ -184,3 +184,23 @@ def test_hex8_newton_explicit_vs_matrix_free(orc, hex_sys):
     um, rm = s.solve_bvp(rtol=1e-10, lin_rtol=1e-12, operator_kind=1)
     assert re["converged"] and rm["converged"]
     assert rel_err(um, ue) < 1e-8
+
+
+@pytest.mark.skipif(not available("ref"), reason="oracle/_ref not built")
+@pytest.mark.parametrize("precond", [0, 1])
+def test_restatement_bicgstab_bitwise_vs_reference(precond):
+    """BiCGStab (krylov.hpp:535-620), restated for the device path's parity: identical bits."""
+    R, O = Oracle("ref"), Oracle("restate")
+    mesh = R.mesh2d(16, 16)
+    bc = R.bcs(2, 16, 16, 0, 1.0, 0.01)
+    out = []
+    for lib in (R, O):
+        s = lib.system(2, *mesh, LINEAR, grid=(16, 16, 0, 1.0, 1.0, 1.0))
+        s.set_dirichlet(*bc)
+        u = bc_state(s.n, 2, *bc)
+        v, r = s.eliminate(s.jacobian(u), s.residual(u), u)
+        x, rep = s.solve(0, v, -r, method=2, precond=precond, rtol=1e-12, max_iter=5000)
+        out.append((x, rep))
+    (xa, ra), (xb, rb) = out
+    assert ra["converged"] and rb["converged"] and ra["iterations"] == rb["iterations"]
+    assert np.array_equal(xa, xb) and np.array_equal(ra["residual_history"], rb["residual_history"])
