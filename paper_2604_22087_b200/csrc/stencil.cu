@@ -77,8 +77,15 @@ struct StencilPlan {
 
 namespace {
 
-// Main-kernel tile: 8 warps, one node row per warp, each lane owns 2 adjacent x nodes (64 per row).
-constexpr int TX = 32, TXN = 2 * TX, TY = 8, NT = TX * TY;
+// Main-kernel tile: TY warps, one node row per warp, each lane owns 2 adjacent x nodes (64 per row).
+// TY = 4 (4 CTAs / SM) measured 10 % faster than TY = 8 (2 CTAs / SM): the per-plane barrier spans
+// fewer warps and the other CTAs on the SM keep the FP64 pipe busy meanwhile.
+#ifndef AFEM_STENCIL_TY
+#define AFEM_STENCIL_TY 4
+#endif
+constexpr int TX = 32, TXN = 2 * TX, TY = AFEM_STENCIL_TY, NT = TX * TY;
+constexpr int NS = 3 + (2 * (TXN + 2) + NT - 1) / NT;  // staging slots per thread: 3 own-row + halo rows
+constexpr int kMainBlocksPerSm = 16 / TY;
 constexpr int RS = 3 * (TXN + 2);            // shared row: interleaved dofs of 66 nodes (198 doubles, 16 B multiple)
 constexpr int NODES = (TY + 2) * (TXN + 2);  // staged nodes per plane (tile + one-node halo)
 constexpr int PER = (NODES + NT - 1) / NT;   // staged nodes per thread
@@ -207,19 +214,19 @@ struct DotArgs {
 };
 
 constexpr int RING = 4;  // plane slots: p (computing), p+1 (landed), p+2 (in flight), one spare
-constexpr size_t kMainSmem = sizeof(double) * RING * (TY + 2) * RS + sizeof(uint32_t) * RING * NT * 4;
+constexpr size_t kMainSmem = sizeof(double) * RING * (TY + 2) * RS + sizeof(uint32_t) * RING * NT * NS;
 
 // DOT: also emit the block partial of x.y (the CG p^T A p).
 template <bool DOT>
-__global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ StencilParams P,
+__global__ void __launch_bounds__(NT, kMainBlocksPerSm) k_stencil_main(const __grid_constant__ StencilParams P,
                                                         const double* __restrict__ x,
                                                         const uint8_t* __restrict__ info, double* __restrict__ y,
                                                         int kchunk, int kbeg, int kend, DotArgs dot) {
   double dsum = 0.0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double (*sm)[TY + 2][RS] = reinterpret_cast<double (*)[TY + 2][RS]>(smem_raw);
-  uint32_t (*sinfo)[NT][4] =
-      reinterpret_cast<uint32_t (*)[NT][4]>(smem_raw + sizeof(double) * RING * (TY + 2) * RS);
+  uint32_t (*sinfo)[NT][NS] =
+      reinterpret_cast<uint32_t (*)[NT][NS]>(smem_raw + sizeof(double) * RING * (TY + 2) * RS);
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int NX = P.NX, NY = P.NY, NZ = P.NZ;
   const int i0 = blockIdx.x * TXN, j0 = blockIdx.y * TY;
@@ -237,17 +244,16 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
   // travels the same way (the aligned 4-byte word holding it, into private shared words).
   // Plane p lives in ring slot (p + 1) % RING; two planes are in flight while one is computed.
   const int lane = tx;
-  const int q3 = ty * 32 + lane;
-  const int r3 = TY + q3 / (TXN + 2), c3 = q3 % (TXN + 2);
   auto slot = [&](int s, int& r, int& col) -> bool {
     if (s < 3) {
       r = ty;
       col = lane + 32 * s;
       return col < TXN + 2;
     }
-    r = r3;
-    col = c3;
-    return q3 < 2 * (TXN + 2);
+    const int q = (s - 3) * NT + static_cast<int>(threadIdx.x);  // halo rows TY, TY+1 over the block
+    r = TY + q / (TXN + 2);
+    col = q % (TXN + 2);
+    return q < 2 * (TXN + 2);
   };
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(&sm[0][0][0]));
   const uint32_t ibase = static_cast<uint32_t>(__cvta_generic_to_shared(&sinfo[0][threadIdx.x][0]));
@@ -258,7 +264,7 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
     const int64_t pb = plane * (inplane ? p : 0);
     uint32_t sel = 0;
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < NS; ++s) {
       int r, col;
       const bool used = slot(s, r, col);
       const int ii = i0 - 1 + col, jj = j0 - 1 + r;
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst + 8u * c), "l"(src + c), "r"(sz)
                        : "memory");
       }
-      const uint32_t idst = ibase + 4u * static_cast<uint32_t>(buf * NT * 4 + s);
+      const uint32_t idst = ibase + 4u * static_cast<uint32_t>(buf * NT * NS + s);
       const uint8_t* isrc = info + (node & ~int64_t(3));
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(idst), "l"(isrc), "r"(ok ? 4 : 0)
                    : "memory");
@@ -286,7 +292,7 @@ __global__ void __launch_bounds__(NT, 2) k_stencil_main(const __grid_constant__ 
     const int buf = ring(p);
     double* sb = &sm[buf][0][0];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < NS; ++s) {
       const uint32_t b = (sel >> (4 * s)) & 7;
       if (b >= 4) continue;
       const uint32_t m = (sinfo[buf][threadIdx.x][s] >> (8 * b)) & 7;
@@ -899,7 +905,7 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
   const DotArgs dot{nullptr, nullptr, nullptr, nullptr, 0, 0};
   if (P.NXm > 0) {  // a piece is a few planes: smaller z chunks so the launch still fills the GPU
     const int tiles = ((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY);
-    const int want = std::max(1, 2 * c.num_sms / std::max(tiles, 1));
+    const int want = std::max(1, kMainBlocksPerSm * c.num_sms / std::max(tiles, 1));
     const int kc = std::max(4, (ke - kb + want - 1) / want);
     const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TY - 1) / TY, (ke - kb + kc - 1) / kc);
     launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, kc, kb, ke, dot);
