@@ -75,11 +75,9 @@ inline afem_solver_cfg to_afem(const SolverConfig& c) {
   if (c.method != SolverMethod::CG && c.method != SolverMethod::GMRES && c.method != SolverMethod::BICGSTAB)
     throw CapabilityError(std::string("b200 backend: solver method ") + to_string(c.method) +
                           " is not on the device path (CG, GMRES, BICGSTAB)");
-  if (c.preconditioner == PreconKind::ILU0)
-    throw CapabilityError("b200 backend: ILU0 is not on the device path (NONE, JACOBI)");
   afem_solver_cfg a{};
   a.method = c.method == SolverMethod::GMRES ? 1 : (c.method == SolverMethod::BICGSTAB ? 2 : 0);
-  a.precond = c.preconditioner == PreconKind::JACOBI ? 1 : 0;
+  a.precond = c.preconditioner == PreconKind::JACOBI ? 1 : (c.preconditioner == PreconKind::ILU0 ? 2 : 0);
   a.rtol = c.rtol;
   a.max_iter = c.max_iter;
   a.restart = c.gmres_restart;

@@ -68,8 +68,9 @@ typedef struct {
   double hardening;
 } afem_material;
 
-/* SolverConfig (krylov.hpp:43-55). method: 0 CG, 1 GMRES, 2 BICGSTAB; precond: 0 NONE, 1 JACOBI.
- * ILU0 and the direct methods are not on the device path (AFEM_E_CAPABILITY). */
+/* SolverConfig (krylov.hpp:43-55). method: 0 CG, 1 GMRES, 2 BICGSTAB; precond: 0 NONE, 1 JACOBI,
+ * 2 ILU0 (assembled operators only: AFEM_E_CAPABILITY on a matrix-free one, like backend.hpp:282).
+ * The banded direct methods are not on the device path. */
 typedef struct {
   int32_t method;
   int32_t precond;

@@ -884,9 +884,61 @@ struct SolveReport {
 struct Precond {
   bool jacobi = false;
   std::vector<double> inv;
+  // ILU(0) (krylov.hpp:116-192): factor values on the pattern, diagonal positions
+  bool ilu = false;
+  const Pattern* pat = nullptr;
+  std::vector<double> lu;
+  std::vector<int64_t> diag;
   void apply(const double* r, double* z, std::size_t n) const {
+    if (ilu) {
+      const auto& rp = pat->row_ptr;
+      const auto& ci = pat->cols;
+      for (std::size_t i = 0; i < n; ++i) {
+        double s = r[i];
+        for (int64_t k = rp[i]; k < rp[i + 1] && ci[k] < (int)i; ++k) s -= lu[k] * z[ci[k]];
+        z[i] = s;
+      }
+      for (int64_t i = (int64_t)n - 1; i >= 0; --i) {
+        double s = z[i];
+        const int64_t dk = diag[i];
+        for (int64_t k = dk + 1; k < rp[i + 1]; ++k) s -= lu[k] * z[ci[k]];
+        z[i] = s / lu[dk];
+      }
+      return;
+    }
     if (!jacobi) { std::copy(r, r + n, z); return; }
     for (std::size_t i = 0; i < n; ++i) z[i] = r[i] * inv[i];
+  }
+  static Precond ilu0(const Pattern& p, const std::vector<double>& values) {  // krylov.hpp:120-152
+    Precond m;
+    m.ilu = true;
+    m.pat = &p;
+    m.lu = values;
+    const int64_t n = p.n_dof;
+    m.diag.assign(n, -1);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t k = p.row_ptr[i]; k < p.row_ptr[i + 1]; ++k)
+        if (p.cols[k] == i) m.diag[i] = k;
+    for (int64_t i = 0; i < n; ++i)
+      if (m.diag[i] < 0) throw FactorizationError("ilu0: structurally missing diagonal at row " + std::to_string(i));
+    for (int64_t i = 0; i < n; ++i) {
+      for (int64_t kk = p.row_ptr[i]; kk < p.row_ptr[i + 1]; ++kk) {
+        const int k = p.cols[kk];
+        if (k >= i) break;
+        const double ukk = m.lu[m.diag[k]];
+        if (ukk == 0.0) throw FactorizationError("ilu0: zero pivot at row " + std::to_string(k));
+        const double lik = m.lu[kk] / ukk;
+        m.lu[kk] = lik;
+        for (int64_t uk = m.diag[k] + 1; uk < p.row_ptr[k + 1]; ++uk) {
+          const int j = p.cols[uk];
+          const auto b = p.cols.begin() + p.row_ptr[i], e = p.cols.begin() + p.row_ptr[i + 1];
+          const auto it = std::lower_bound(b, e, j);
+          if (it != e && *it == j) m.lu[it - p.cols.begin()] -= lik * m.lu[uk];
+        }
+      }
+      if (m.lu[m.diag[i]] == 0.0) throw FactorizationError("ilu0: zero pivot at row " + std::to_string(i));
+    }
+    return m;
   }
   static Precond from_diagonal(const std::vector<double>& d) {  // krylov.hpp:83-92
     Precond p; p.jacobi = true; p.inv.resize(d.size());
@@ -1133,7 +1185,11 @@ inline std::vector<double> run_solver(const Operator& op, const double* b, const
   if (cfg.method < 0 || cfg.method > 2) throw std::invalid_argument("run_solver: only CG, GMRES and BiCGStab are restated");
   Precond m;
   if (cfg.precond == 1) m = Precond::from_diagonal(op.diagonal());
-  else if (cfg.precond != 0) throw CapabilityError("run_solver: preconditioner not restated");
+  else if (cfg.precond == 2) {  // ilu0_setup(op.csr()) (backend.hpp:282; csr() gate :151-156)
+    const auto* e = dynamic_cast<const ExplicitOperator*>(&op);
+    if (!e) throw CapabilityError("assembled matrix required, but the operator is matrix-free");
+    m = Precond::ilu0(*e->p, e->values);
+  } else if (cfg.precond != 0) throw CapabilityError("run_solver: preconditioner not restated");
   if (cfg.method == 2) return bicgstab(op, b, cfg, m, x0, rep);
   return cfg.method == 0 ? cg(op, b, cfg, m, x0, rep) : gmres(op, b, cfg, m, x0, rep);
 }

@@ -46,6 +46,7 @@ struct SysView {
 };
 
 struct StencilPlan;  // structured fast path (stencil.cu)
+struct IluLevels;    // ILU(0) dependency levels of a pattern (ilu.cu)
 
 struct System {
   Ctx* ctx = nullptr;
@@ -75,6 +76,7 @@ struct System {
   // scratch of the element-centric kernels (elemgrid.cu), allocated on first use
   std::vector<double> grid_geo;
   DevArray<double> ev;
+  std::shared_ptr<IluLevels> ilu_levels;  // built on the first ILU(0) setup
   // structured grid metadata (afem_system_create_grid)
   bool grid = false;
   int nx = 0, ny = 0, nz = 0;
@@ -195,6 +197,14 @@ struct SolveReport {
 };
 void validate_cfg(const SolverCfg& c);
 void solve(Operator& op, const SolverCfg& cfg, const double* b, const double* x0, double* x, SolveReport& rep);
+
+// ---- ilu.cu (Ilu0Preconditioner, krylov.hpp:116-192)
+struct Ilu0 {
+  System* s = nullptr;
+  DevArray<double> f;  // L (strict lower, unit diagonal implied) and U in the pattern's slots
+  void setup(System& sys, const double* values);  // FactorizationError on a zero pivot
+  void apply(const double* r, double* z) const;   // z = U^-1 L^-1 r
+};
 
 // ---- stencil.cu
 StencilPlan* make_stencil_plan(System& s, const MfOp& op);  // nullptr when not applicable

@@ -477,7 +477,62 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
   }
 }
 
-void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const double* inv, SolveReport& rep) {
+// The preconditioner of a solve: Jacobi (inverse diagonal, fused into the CG kernels), ILU(0), or none.
+struct Pc {
+  const double* inv = nullptr;
+  const Ilu0* ilu = nullptr;
+  void apply(Ctx& c, const double* in, double* out, int64_t n) const {
+    if (ilu) ilu->apply(in, out);
+    else launch(c, k_precond, grid_for(n, 256, 148 * 16), 256, 0, in, inv, out, n);
+  }
+};
+
+// cg (krylov.hpp:350-408) with a general preconditioner (ILU(0)): host scalars, one sync per dot.
+void cg_generic(Operator& op, const SolverCfg& cfg, const double* b, double* x, const Pc& pc, SolveReport& rep) {
+  Ctx& c = *op.sys->ctx;
+  const int64_t n = op.n;
+  DevArray<double> r(n), z(n), p(n), ap(n), scratch(n);
+  const double bnorm = std::sqrt(dot(c, b, b, n));
+  const double denom = bnorm > 0.0 ? bnorm : 1.0;
+  rep.history.push_back(residual_norm(op, b, x, ap.p, r.p) / denom);
+  while (true) {
+    if (rep.history.back() > cfg.rtol && rep.iterations < cfg.max_iter) {
+      pc.apply(c, r.p, z.p, n);
+      copy(c, z.p, p.p, n);
+      double rz = dot(c, r.p, z.p, n);
+      while (rep.iterations < cfg.max_iter && rep.history.back() > cfg.rtol) {
+        op.apply(p.p, ap.p);
+        const double pap = dot(c, p.p, ap.p, n);
+        if (!(pap > 0.0)) {
+          rep.failure = "cg: operator not positive definite (p^T A p <= 0 at iteration " +
+                        std::to_string(rep.iterations + 1) + ")";
+          break;
+        }
+        const double alpha = rz / pap;
+        axpy(c, alpha, p.p, x, n);
+        axpy(c, -alpha, ap.p, r.p, n);
+        ++rep.iterations;
+        rep.history.push_back(std::sqrt(dot(c, r.p, r.p, n)) / denom);
+        if (rep.history.back() <= cfg.rtol) break;
+        pc.apply(c, r.p, z.p, n);
+        const double rz_new = dot(c, r.p, z.p, n);
+        const double beta = rz_new / rz;
+        rz = rz_new;
+        launch(c, k_bicg_p, grid_for(n, 256, 148 * 16), 256, 0, z.p, p.p, z.p, beta, 0.0, n);  // p = z + beta p
+      }
+    }
+    const double true_rres = residual_norm(op, b, x, scratch.p, nullptr) / denom;
+    rep.history.back() = true_rres;
+    if (true_rres <= cfg.rtol) {
+      rep.converged = rep.failure.empty();
+      break;
+    }
+    if (!rep.failure.empty() || rep.iterations >= cfg.max_iter) break;
+    residual_norm(op, b, x, ap.p, r.p);  // krylov.hpp:402-404
+  }
+}
+
+void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const Pc& pc, SolveReport& rep) {
   Ctx& c = *op.sys->ctx;
   const int64_t n = op.n;
   const int restart = static_cast<int>(std::min<int64_t>(cfg.restart, n));
@@ -487,18 +542,18 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
   auto vec = [&](int k) { return V.p + static_cast<int64_t>(k) * n; };
   const double bnorm = std::sqrt(dot(c, b, b, n));
   const double denom = bnorm > 0.0 ? bnorm : 1.0;
-  launch(c, k_precond, eg, 256, 0, b, inv, tmp.p, n);
+  pc.apply(c, b, tmp.p, n);
   const double pnorm = std::sqrt(dot(c, tmp.p, tmp.p, n));
   const double pdenom = pnorm > 0.0 ? pnorm : 1.0;
   std::vector<double> h(static_cast<size_t>(restart + 1) * restart, 0.0), cs(restart), sn(restart), g(restart + 1);
   auto H = [&](int i, int j) -> double& { return h[static_cast<size_t>(i) * restart + j]; };
 
   double true_rres = residual_norm(op, b, x, tmp.p, r.p) / denom;
-  launch(c, k_precond, eg, 256, 0, r.p, inv, w.p, n);
+  pc.apply(c, r.p, w.p, n);
   rep.history.push_back(std::sqrt(dot(c, w.p, w.p, n)) / pdenom);
 
   while (true_rres > cfg.rtol && rep.iterations < cfg.max_iter && rep.failure.empty()) {
-    launch(c, k_precond, eg, 256, 0, r.p, inv, w.p, n);
+    pc.apply(c, r.p, w.p, n);
     const double beta = std::sqrt(dot(c, w.p, w.p, n));
     if (beta == 0.0) break;
     const double target_est = beta * std::min(1.0, 0.5 * cfg.rtol / true_rres);  // krylov.hpp:454
@@ -508,7 +563,7 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
     int j = 0, cols = 0;
     for (; j < restart && rep.iterations < cfg.max_iter; ++j) {
       op.apply(vec(j), tmp.p);
-      launch(c, k_precond, eg, 256, 0, tmp.p, inv, w.p, n);
+      pc.apply(c, tmp.p, w.p, n);
       for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, scalars stay on the device
         dot_dev(c, vec(i), w.p, n, hcol.p + i);
         add_scaled_dev(c, hcol.p + i, -1.0, vec(i), w.p, n);
@@ -569,7 +624,7 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
 
 // bicgstab (krylov.hpp:535-620): scalars on the host (one sync per dot); same breakdown messages,
 // early exit on a small s, true-residual re-verification and restart from the fresh residual.
-void bicgstab(Operator& op, const SolverCfg& cfg, const double* b, double* x, const double* inv, SolveReport& rep) {
+void bicgstab(Operator& op, const SolverCfg& cfg, const double* b, double* x, const Pc& pc, SolveReport& rep) {
   Ctx& c = *op.sys->ctx;
   const int64_t n = op.n;
   const unsigned eg = grid_for(n, 256, 148 * 16);
@@ -580,7 +635,7 @@ void bicgstab(Operator& op, const SolverCfg& cfg, const double* b, double* x, co
   const double denom = bnorm > 0.0 ? bnorm : 1.0;
   rep.history.push_back(residual_norm(op, b, x, t.p, r.p) / denom);
   copy(c, r.p, rhat.p, n);
-  auto precond = [&](const double* in, double* out) { launch(c, k_precond, eg, 256, 0, in, inv, out, n); };
+  auto precond = [&](const double* in, double* out) { pc.apply(c, in, out, n); };
   while (true) {
     double rho = 1.0, alpha = 1.0, omega = 1.0;
     while (rep.history.back() > cfg.rtol && rep.iterations < cfg.max_iter) {
@@ -651,12 +706,19 @@ void solve(Operator& op, const SolverCfg& cfg, const double* b, const double* x0
   validate_cfg(cfg);
   if (cfg.method < 0 || cfg.method > 2)
     throw CapabilityError("run_solver: CG, GMRES and BiCGStab are provided on the device");
-  if (cfg.precond != 0 && cfg.precond != 1) throw CapabilityError("run_solver: ILU0 is not provided on the device");
+  if (cfg.precond < 0 || cfg.precond > 2) throw std::invalid_argument("run_solver: unknown preconditioner");
+  if (cfg.precond == 2 && !op.csr_values())  // backend.hpp:151-156, 282
+    throw CapabilityError("assembled matrix required, but the operator is matrix-free");
   op.validate();
   Timer timer;
   Ctx& c = *op.sys->ctx;
   DevArray<double> inv;
   if (cfg.precond == 1) jacobi_inverse(op, inv);
+  Ilu0 ilu;
+  if (cfg.precond == 2) ilu.setup(*op.sys, op.csr_values());  // ilu0_setup(op.csr()), krylov.hpp:192
+  Pc pc;
+  pc.inv = inv.p;
+  pc.ilu = cfg.precond == 2 ? &ilu : nullptr;
   // the vector kernels use 16-byte accesses: iterate in an aligned buffer if the caller's is not
   DevArray<double> xa;
   double* xw = x;
@@ -666,9 +728,10 @@ void solve(Operator& op, const SolverCfg& cfg, const double* b, const double* x0
   }
   if (x0) copy(c, x0, xw, op.n);
   else fill(c, 0.0, xw, op.n);
-  if (cfg.method == 0) cg(op, cfg, b, xw, inv.p, rep);
-  else if (cfg.method == 1) gmres(op, cfg, b, xw, inv.p, rep);
-  else bicgstab(op, cfg, b, xw, inv.p, rep);
+  if (cfg.method == 0 && pc.ilu) cg_generic(op, cfg, b, xw, pc, rep);
+  else if (cfg.method == 0) cg(op, cfg, b, xw, inv.p, rep);
+  else if (cfg.method == 1) gmres(op, cfg, b, xw, pc, rep);
+  else bicgstab(op, cfg, b, xw, pc, rep);
   if (xw != x) copy(c, xw, x, op.n);
   AFEM_CK(cudaStreamSynchronize(c.stream));
   rep.wall_time = timer.seconds();

@@ -178,6 +178,44 @@ void assembly_case(const std::string& tag, int n, const std::vector<Material>& m
   }
 }
 
+// ILU(0) (krylov.hpp:116-192) through the device CSR vs the reference on the same eliminated system.
+void ilu_case(const std::string& tag, int n, const std::vector<Material>& mats) {
+  const Mesh mesh = generate_two_phase_mesh(n, n, 1.0, 1.0, {0.5, 0.5}, 0.25);
+  const DirichletSpec bcs = benchmark_bcs(mesh, 0.01);
+  const auto batches = build_batches(mesh, mats);
+  const auto pattern = precompute_sparsity(batches, mesh.n_dof());
+  b200::System sys(mesh, mats);
+  sys.set_dirichlet(bcs);
+  const auto u = bc_state(mesh, bcs, rand_vec(mesh.n_dof(), 0.01, 77));
+  CooTriplets k_ref = assemble_jacobian(batches, u, *pattern);
+  std::vector<double> rhs = assemble_residual(batches, u);
+  apply_dirichlet(*pattern, k_ref.values, rhs, bcs, u);
+  for (double& v : rhs) v = -v;
+  HandoffBuffer buf(pattern);
+  buf.handoff(std::move(k_ref));
+  const LinearOperator op_ref = explicit_operator(buf);
+  b200::DeviceHandoff dh(sys);
+  dh.assemble(u);
+  dh.handoff();
+  const auto op_dev = dh.explicit_operator();
+  for (SolverMethod m : {SolverMethod::CG, SolverMethod::GMRES, SolverMethod::BICGSTAB}) {
+    SolverConfig c;
+    c.method = m;
+    c.preconditioner = PreconKind::ILU0;
+    c.rtol = 1e-12;
+    c.max_iter = 5 * mesh.n_dof();
+    auto [xd, rd] = b200::run_solver(op_dev, rhs, c);
+    auto [xr, rr] = run_solver(op_ref, rhs, c);
+    char msg[200];
+    std::snprintf(msg, sizeof msg, " %s+ILU0: converged %d/%d, iterations %d vs %d, x within 1e-8 (%.2e)",
+                  to_string(m), int(rd.converged), int(rr.converged), rd.iterations, rr.iterations, rel_err(xd, xr));
+    check(rd.converged && rr.converged && std::abs(rd.iterations - rr.iterations) <= std::max(2, rr.iterations / 20) &&
+              rel_err(xd, xr) <= 1e-8,
+          tag + msg);
+  }
+  buf.release();
+}
+
 void newton_case(const std::string& tag, int n, const std::vector<Material>& mats) {
   const Mesh mesh = generate_two_phase_mesh(n, n, 1.0, 1.0, {0.5, 0.5}, 0.25);
   const DirichletSpec bcs = benchmark_bcs(mesh, 0.02);
@@ -244,7 +282,9 @@ void semantics() {
         "banded direct LU on the device path -> CapabilityError (out of scope, SURVEY §8f)");
   SolverConfig ilu;
   ilu.preconditioner = PreconKind::ILU0;
-  check(throws<CapabilityError>([&] { b200::run_solver(op, x, ilu); }), "ILU0 on the device path -> CapabilityError");
+  auto mfo = b200::matrix_free_operator(sys, u0);
+  check(throws<CapabilityError>([&] { b200::run_solver(mfo, x, ilu); }),
+        "ILU0 on a matrix-free operator -> CapabilityError (backend.hpp:282)");
   // non-convergence is reported, not thrown (krylov.hpp:66-72)
   SolverConfig tiny;
   tiny.max_iter = 2;
@@ -267,6 +307,8 @@ int main() {
   std::printf("libafem_b200 C++ overlay vs the reference (ABI %d)\n", afem_abi_version());
   assembly_case("config1 64x64 linear", 64, linear_mats());
   assembly_case("16x16 SVK+linear", 16, svk_mats());
+  ilu_case("24x24 linear", 24, linear_mats());
+  ilu_case("16x16 SVK+linear", 16, svk_mats());
   newton_case("12x12 SVK+linear", 12, svk_mats());
   newton_case("16x16 linear", 16, linear_mats());
   semantics();

@@ -43,8 +43,8 @@ def test_csv_schema_and_rows():
     lines = p.stdout.splitlines()
     assert lines[0].startswith("# afem_bench") and lines[1] == HEADER
     rows = [ln.split(",") for ln in lines[2:]]
-    assert len(rows) == 2 * 6  # 2 meshes x {CG, GMRES, BICGSTAB} x {NONE, JACOBI}
-    assert {r[2] for r in rows} == {"CG", "GMRES", "BICGSTAB"} and {r[3] for r in rows} == {"NONE", "JACOBI"}
+    assert len(rows) == 2 * 9  # 2 meshes x {CG, GMRES, BICGSTAB} x {NONE, JACOBI, ILU0}
+    assert {r[2] for r in rows} == {"CG", "GMRES", "BICGSTAB"} and {r[3] for r in rows} == {"NONE", "JACOBI", "ILU0"}
     cg_jacobi = [r for r in rows if r[2] == "CG" and r[3] == "JACOBI"]
     assert all(r[5] == "1" and float(r[8]) <= 1e-10 for r in cg_jacobi)
     p = run("newton", "--levels", "1", "--reps", "1")

@@ -204,3 +204,22 @@ def test_restatement_bicgstab_bitwise_vs_reference(precond):
     (xa, ra), (xb, rb) = out
     assert ra["converged"] and rb["converged"] and ra["iterations"] == rb["iterations"]
     assert np.array_equal(xa, xb) and np.array_equal(ra["residual_history"], rb["residual_history"])
+
+
+@pytest.mark.skipif(not available("ref"), reason="oracle/_ref not built")
+@pytest.mark.parametrize("method", [0, 1, 2], ids=["cg", "gmres", "bicgstab"])
+def test_restatement_ilu0_bitwise_vs_reference(method):
+    """ILU(0) (krylov.hpp:116-192), restated for the device path's parity: identical bits."""
+    R, O = Oracle("ref"), Oracle("restate")
+    mesh = R.mesh2d(12, 12)
+    bc = R.bcs(2, 12, 12, 0, 1.0, 0.01)
+    out = []
+    for lib in (R, O):
+        s = lib.system(2, *mesh, SVK_MIX, grid=(12, 12, 0, 1.0, 1.0, 1.0))
+        s.set_dirichlet(*bc)
+        u = bc_state(s.n, 2, *bc, u=random_vector(s.n, 0.01, 5))
+        v, r = s.eliminate(s.jacobian(u), s.residual(u), u)
+        out.append(s.solve(0, v, -r, method=method, precond=2, rtol=1e-12, max_iter=5000))
+    (xa, ra), (xb, rb) = out
+    assert ra["converged"] and rb["converged"] and ra["iterations"] == rb["iterations"]
+    assert np.array_equal(xa, xb)

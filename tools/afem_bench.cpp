@@ -215,7 +215,7 @@ std::vector<Record> cmd_apply(afem_ctx ctx, const Opts& o, bool mf) {
 }
 
 const char* mname(int m) { return m == 0 ? "CG" : (m == 1 ? "GMRES" : "BICGSTAB"); }
-const char* pname(int p) { return p == 0 ? "NONE" : "JACOBI"; }
+const char* pname(int p) { return p == 0 ? "NONE" : (p == 1 ? "JACOBI" : "ILU0"); }
 
 std::vector<Record> cmd_solvers(afem_ctx ctx, const Opts& o) {
   std::vector<Record> rs;
@@ -227,7 +227,7 @@ std::vector<Record> cmd_solvers(afem_ctx ctx, const Opts& o) {
     bench_system(o, s, b);
     std::vector<double> x(s.info.n_dof), hist(o.max_iter + 2);
     for (int m : {0, 1, 2})
-      for (int p : {0, 1})
+      for (int p : {0, 1, 2})
         for (int r = 0; r < o.reps; ++r) {
           afem_solver_cfg cfg{m, p, o.rtol, o.max_iter, o.restart};
           afem_solve_report rep{};
