@@ -72,11 +72,14 @@ inline afem_material to_afem(const Material& m) {
 }
 
 inline afem_solver_cfg to_afem(const SolverConfig& c) {
-  if (c.method != SolverMethod::CG && c.method != SolverMethod::GMRES && c.method != SolverMethod::BICGSTAB)
-    throw CapabilityError(std::string("b200 backend: solver method ") + to_string(c.method) +
-                          " is not on the device path (CG, GMRES, BICGSTAB)");
   afem_solver_cfg a{};
-  a.method = c.method == SolverMethod::GMRES ? 1 : (c.method == SolverMethod::BICGSTAB ? 2 : 0);
+  switch (c.method) {  // krylov.hpp:20 order
+    case SolverMethod::CG: a.method = 0; break;
+    case SolverMethod::GMRES: a.method = 1; break;
+    case SolverMethod::BICGSTAB: a.method = 2; break;
+    case SolverMethod::DIRECT_CHOL: a.method = 3; break;
+    case SolverMethod::DIRECT_LU: a.method = 4; break;
+  }
   a.precond = c.preconditioner == PreconKind::JACOBI ? 1 : (c.preconditioner == PreconKind::ILU0 ? 2 : 0);
   a.rtol = c.rtol;
   a.max_iter = c.max_iter;

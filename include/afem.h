@@ -68,9 +68,10 @@ typedef struct {
   double hardening;
 } afem_material;
 
-/* SolverConfig (krylov.hpp:43-55). method: 0 CG, 1 GMRES, 2 BICGSTAB; precond: 0 NONE, 1 JACOBI,
- * 2 ILU0 (assembled operators only: AFEM_E_CAPABILITY on a matrix-free one, like backend.hpp:282).
- * The banded direct methods are not on the device path. */
+/* SolverConfig (krylov.hpp:43-55). method: 0 CG, 1 GMRES, 2 BICGSTAB, 3 DIRECT_CHOL, 4 DIRECT_LU
+ * (banded, backend.hpp:245-269: iterations 1, converged iff the true residual <= 1e-10, breakdown
+ * reported in `failure`); precond: 0 NONE, 1 JACOBI, 2 ILU0. ILU0 and the direct methods need an
+ * assembled operator (AFEM_E_CAPABILITY on a matrix-free one, like backend.hpp:151-156, 282). */
 typedef struct {
   int32_t method;
   int32_t precond;

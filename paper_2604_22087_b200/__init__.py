@@ -19,7 +19,7 @@ __all__ = [
     "StaleEpochError", "CapabilityError", "FactorizationError", "InvertedElementError", "CudaError",
     "Context", "System", "Values", "HandoffBuffer", "LinearOperator", "explicit_operator",
     "matrix_free_operator", "run_solver", "fibres", "LINEAR", "SVK", "NEOHOOKE", "J2", "EXPLICIT", "MATRIX_FREE",
-    "CG", "GMRES", "BICGSTAB", "NONE", "JACOBI", "ILU0", "lib_path", "load",
+    "CG", "GMRES", "BICGSTAB", "DIRECT_CHOL", "DIRECT_LU", "NONE", "JACOBI", "ILU0", "lib_path", "load",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -28,7 +28,7 @@ LIB_PATH = os.path.join(HERE, "libafem_b200.so")
 LINEAR, SVK = 0, 1                 # MaterialModel (material.hpp:13)
 NEOHOOKE, J2 = 2, 3                # north-star laws beyond the reference (configs 3 and 4)
 EXPLICIT, MATRIX_FREE = 0, 1       # OperatorKind (backend.hpp:20)
-CG, GMRES, BICGSTAB = 0, 1, 2      # SolverMethod (krylov.hpp:20)
+CG, GMRES, BICGSTAB, DIRECT_CHOL, DIRECT_LU = 0, 1, 2, 3, 4  # SolverMethod (krylov.hpp:20)
 NONE, JACOBI, ILU0 = 0, 1, 2       # PreconKind (krylov.hpp:21)
 
 

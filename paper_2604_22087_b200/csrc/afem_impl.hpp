@@ -206,6 +206,9 @@ struct Ilu0 {
   void apply(const double* r, double* z) const;   // z = U^-1 L^-1 r
 };
 
+// ---- direct.cu (BandedFactorization, krylov.hpp:196-307): false + failure text on breakdown
+bool direct_solve(System& s, const double* vals, bool chol, const double* b, double* x, std::string& failure);
+
 // ---- stencil.cu
 StencilPlan* make_stencil_plan(System& s, const MfOp& op);  // nullptr when not applicable
 void stencil_apply(StencilPlan& p, const MfOp& op, const double* x, double* y, double* dot_out = nullptr);

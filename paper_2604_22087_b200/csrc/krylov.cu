@@ -704,8 +704,28 @@ void validate_cfg(const SolverCfg& c) {  // SolverConfig::validate (krylov.hpp:5
 // run_solver (backend.hpp:241-286), iterative methods. x0 may alias x.
 void solve(Operator& op, const SolverCfg& cfg, const double* b, const double* x0, double* x, SolveReport& rep) {
   validate_cfg(cfg);
-  if (cfg.method < 0 || cfg.method > 2)
-    throw CapabilityError("run_solver: CG, GMRES and BiCGStab are provided on the device");
+  if (cfg.method < 0 || cfg.method > 4) throw std::invalid_argument("run_solver: unknown method");
+  if (cfg.method >= 3) {  // DIRECT_CHOL / DIRECT_LU (backend.hpp:245-269)
+    if (!op.csr_values()) throw CapabilityError("assembled matrix required, but the operator is matrix-free");
+    op.validate();
+    Timer timer;
+    Ctx& c = *op.sys->ctx;
+    const double bnorm = std::sqrt(dot(c, b, b, op.n));
+    const double denom = bnorm > 0.0 ? bnorm : 1.0;
+    rep.history.push_back(bnorm / denom);
+    if (direct_solve(*op.sys, op.csr_values(), cfg.method == 3, b, x, rep.failure)) {
+      rep.iterations = 1;
+      DevArray<double> scratch(op.n);
+      const double rres = residual_norm(op, b, x, scratch.p, nullptr) / denom;
+      rep.history.push_back(rres);
+      rep.converged = rres <= 1e-10;  // kDirectResidualContract (krylov.hpp:59)
+    } else {
+      fill(c, 0.0, x, op.n);
+    }
+    AFEM_CK(cudaStreamSynchronize(c.stream));
+    rep.wall_time = timer.seconds();
+    return;
+  }
   if (cfg.precond < 0 || cfg.precond > 2) throw std::invalid_argument("run_solver: unknown preconditioner");
   if (cfg.precond == 2 && !op.csr_values())  // backend.hpp:151-156, 282
     throw CapabilityError("assembled matrix required, but the operator is matrix-free");

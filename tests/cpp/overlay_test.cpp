@@ -216,6 +216,42 @@ void ilu_case(const std::string& tag, int n, const std::vector<Material>& mats) 
   buf.release();
 }
 
+// Banded direct solvers (krylov.hpp:196-307, backend.hpp:245-269) vs the reference.
+void direct_case(const std::string& tag, int n, const std::vector<Material>& mats) {
+  const Mesh mesh = generate_two_phase_mesh(n, n, 1.0, 1.0, {0.5, 0.5}, 0.25);
+  const DirichletSpec bcs = benchmark_bcs(mesh, 0.01);
+  const auto batches = build_batches(mesh, mats);
+  const auto pattern = precompute_sparsity(batches, mesh.n_dof());
+  b200::System sys(mesh, mats);
+  sys.set_dirichlet(bcs);
+  const auto u = bc_state(mesh, bcs, rand_vec(mesh.n_dof(), 0.01, 91));
+  CooTriplets k_ref = assemble_jacobian(batches, u, *pattern);
+  std::vector<double> rhs = assemble_residual(batches, u);
+  apply_dirichlet(*pattern, k_ref.values, rhs, bcs, u);
+  for (double& v : rhs) v = -v;
+  HandoffBuffer buf(pattern);
+  buf.handoff(std::move(k_ref));
+  const LinearOperator op_ref = explicit_operator(buf);
+  b200::DeviceHandoff dh(sys);
+  dh.assemble(u);
+  dh.handoff();
+  const auto op_dev = dh.explicit_operator();
+  for (SolverMethod m : {SolverMethod::DIRECT_CHOL, SolverMethod::DIRECT_LU}) {
+    SolverConfig c;
+    c.method = m;
+    auto [xd, rd] = b200::run_solver(op_dev, rhs, c);
+    auto [xr, rr] = run_solver(op_ref, rhs, c);
+    char msg[200];
+    std::snprintf(msg, sizeof msg, " %s: converged %d/%d, iterations %d/%d, true rres %.2e, x within 1e-10 (%.2e)",
+                  to_string(m), int(rd.converged), int(rr.converged), rd.iterations, rr.iterations,
+                  rd.residual_history.back(), rel_err(xd, xr));
+    check(rd.converged && rr.converged && rd.iterations == 1 && rd.residual_history.size() == 2 &&
+              rel_err(xd, xr) <= 1e-10,
+          tag + msg);
+  }
+  buf.release();
+}
+
 void newton_case(const std::string& tag, int n, const std::vector<Material>& mats) {
   const Mesh mesh = generate_two_phase_mesh(n, n, 1.0, 1.0, {0.5, 0.5}, 0.25);
   const DirichletSpec bcs = benchmark_bcs(mesh, 0.02);
@@ -275,11 +311,12 @@ void semantics() {
   h.assemble(u0);
   h.handoff();
   check(throws<StaleEpochError>([&] { op.apply(x, y); }), "apply with a stale epoch -> StaleEpochError");
-  // device path capability gates
+  // capability gates (backend.hpp:151-156, 282)
   SolverConfig lu;
   lu.method = SolverMethod::DIRECT_LU;
-  check(throws<CapabilityError>([&] { b200::run_solver(op, x, lu); }),
-        "banded direct LU on the device path -> CapabilityError (out of scope, SURVEY §8f)");
+  auto mfd = b200::matrix_free_operator(sys, u0);
+  check(throws<CapabilityError>([&] { b200::run_solver(mfd, x, lu); }),
+        "direct LU on a matrix-free operator -> CapabilityError");
   SolverConfig ilu;
   ilu.preconditioner = PreconKind::ILU0;
   auto mfo = b200::matrix_free_operator(sys, u0);
@@ -308,6 +345,8 @@ int main() {
   assembly_case("config1 64x64 linear", 64, linear_mats());
   assembly_case("16x16 SVK+linear", 16, svk_mats());
   ilu_case("24x24 linear", 24, linear_mats());
+  direct_case("config1 64x64 linear", 64, linear_mats());
+  direct_case("16x16 SVK+linear", 16, svk_mats());
   ilu_case("16x16 SVK+linear", 16, svk_mats());
   newton_case("12x12 SVK+linear", 12, svk_mats());
   newton_case("16x16 linear", 16, linear_mats());

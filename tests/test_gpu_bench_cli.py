@@ -51,6 +51,10 @@ def test_csv_schema_and_rows():
     rows = [ln.split(",") for ln in p.stdout.splitlines()[2:]]
     assert p.returncode == 0 and [r[4] for r in rows] == ["EXPLICIT", "MATRIX_FREE"]
     assert all(r[5] == "1" for r in rows) and rows[0][6] == rows[1][6]  # same Newton count both kinds
+    p = run("direct", "--levels", "2", "--reps", "1")
+    rows = [ln.split(",") for ln in p.stdout.splitlines()[2:]]
+    assert p.returncode == 0 and [r[2] for r in rows] == ["DIRECT_CHOL", "DIRECT_LU"] * 2
+    assert all(r[5] == "1" and r[6] == "1" and float(r[8]) <= 1e-10 for r in rows)
     for cmd in ("spmv", "mfapply"):
         p = run(cmd, "--levels", "1", "--reps", "2")
         rows = [ln.split(",") for ln in p.stdout.splitlines()[2:]]

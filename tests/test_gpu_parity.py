@@ -343,3 +343,29 @@ def test_ilu0_hex8_against_restatement(afem, ctx, orc, method):
     buf.release()
     with pytest.raises(afem.CapabilityError):  # ILU0 needs the assembled matrix (backend.hpp:282)
         afem.run_solver(afem.matrix_free_operator(s, u), rhs, method=method, precond=afem.ILU0)
+
+
+def test_direct_solvers_semantics(afem, ctx):
+    """DIRECT_CHOL / DIRECT_LU (backend.hpp:245-269): one iteration, history [|b|/|b|, true rres],
+    converged iff rres <= 1e-10; a breakdown is reported (x = 0, failure text), never raised."""
+    s = afem.System.grid(ctx, 2, 12, 12, materials=LINEAR)
+    s.set_benchmark_dirichlet(0.01)
+    u = s.impose_dirichlet(random_vector(s.n, 0.01, 6))
+    vals = afem.Values(s).assemble(u)
+    rhs = -vals.eliminate(s.residual(u), u)
+    K = vals.numpy()
+    buf = afem.HandoffBuffer(s)
+    buf.handoff(vals)
+    op = afem.explicit_operator(buf)
+    xc, rc = afem.run_solver(op, rhs, method=afem.CG, precond=afem.JACOBI, rtol=1e-13)
+    for m in (afem.DIRECT_CHOL, afem.DIRECT_LU):
+        x, rep = afem.run_solver(op, rhs, method=m)
+        assert rep["converged"] and rep["iterations"] == 1 and len(rep["residual_history"]) == 2
+        assert rep["residual_history"][-1] <= 1e-10 and rel_err(x, xc) <= 1e-9
+    buf.release()
+    neg = afem.Values(s).set(-K)  # negative definite: Cholesky fails at the first pivot
+    buf2 = afem.HandoffBuffer(s)
+    buf2.handoff(neg)
+    x, rep = afem.run_solver(afem.explicit_operator(buf2), rhs, method=afem.DIRECT_CHOL)
+    assert not rep["converged"] and rep["failure"].startswith("cholesky: matrix not positive definite at pivot row 0")
+    assert not x.any()

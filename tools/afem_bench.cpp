@@ -4,6 +4,7 @@
 //   afem_bench spmv     [opts]   100 CSR applies of the eliminated benchmark tangent per rep (cmd_spmv)
 //   afem_bench mfapply  [opts]   100 matrix-free applies per rep (the bench.py metric, any mesh)
 //   afem_bench solvers  [opts]   method x preconditioner grid on the benchmark system (cmd_solvers)
+//   afem_bench direct   [opts]   banded Cholesky and LU on the benchmark system (cmd_direct)
 //   afem_bench newton   [opts]   solve_bvp under EXPLICIT and MATRIX_FREE (cmd_newton)
 //   afem_bench verify   [opts]   the five oracle checks of verify.hpp:62-308 through the ABI
 //
@@ -56,7 +57,7 @@ double now() {
 }
 
 Opts parse(int argc, char** argv) {
-  if (argc < 2) throw UsageError("missing subcommand (spmv | mfapply | solvers | newton | verify)");
+  if (argc < 2) throw UsageError("missing subcommand (spmv | mfapply | solvers | direct | newton | verify)");
   Opts o;
   o.cmd = argv[1];
   for (int i = 2; i < argc; ++i) {
@@ -214,7 +215,10 @@ std::vector<Record> cmd_apply(afem_ctx ctx, const Opts& o, bool mf) {
   return rs;
 }
 
-const char* mname(int m) { return m == 0 ? "CG" : (m == 1 ? "GMRES" : "BICGSTAB"); }
+const char* mname(int m) {
+  static const char* names[] = {"CG", "GMRES", "BICGSTAB", "DIRECT_CHOL", "DIRECT_LU"};
+  return names[m];
+}
 const char* pname(int p) { return p == 0 ? "NONE" : (p == 1 ? "JACOBI" : "ILU0"); }
 
 std::vector<Record> cmd_solvers(afem_ctx ctx, const Opts& o) {
@@ -236,6 +240,29 @@ std::vector<Record> cmd_solvers(afem_ctx ctx, const Opts& o) {
           rs.push_back({"solvers", mname(m), pname(p), "EXPLICIT", s.info.n_dof, rep.converged != 0, rep.iterations,
                         rep.wall_time, nh > 0 ? hist[nh - 1] : NAN});
         }
+  }
+  return rs;
+}
+
+// cmd_direct (bench.hpp:321-342): failures recorded with final_rres = NaN, never dropped.
+std::vector<Record> cmd_direct(afem_ctx ctx, const Opts& o) {
+  std::vector<Record> rs;
+  const auto mats = materials(o.materials);
+  for (int k = 0; k < o.levels; ++k) {
+    Sys s;
+    make_sys(ctx, o, level_n(o, k), mats, s);
+    Bench b;
+    bench_system(o, s, b);
+    std::vector<double> x(s.info.n_dof), hist(4);
+    for (int m : {3, 4})
+      for (int r = 0; r < o.reps; ++r) {
+        afem_solver_cfg cfg{m, 0, o.rtol, 1, o.restart};
+        afem_solve_report rep{};
+        ck(afem_solve(b.op, &cfg, b.rhs.data(), nullptr, x.data(), &rep, hist.data(), (int32_t)hist.size()));
+        const int nh = std::min<int>(rep.n_history, (int)hist.size());
+        rs.push_back({"direct", mname(m), "NONE", "EXPLICIT", s.info.n_dof, rep.converged != 0, rep.iterations,
+                      rep.wall_time, rep.failure[0] ? NAN : hist[nh - 1]});
+      }
   }
   return rs;
 }
@@ -484,7 +511,8 @@ int main(int argc, char** argv) {
   Opts o;
   try {
     o = parse(argc, argv);
-    if (o.cmd != "spmv" && o.cmd != "mfapply" && o.cmd != "solvers" && o.cmd != "newton" && o.cmd != "verify")
+    if (o.cmd != "spmv" && o.cmd != "mfapply" && o.cmd != "solvers" && o.cmd != "direct" && o.cmd != "newton" &&
+        o.cmd != "verify")
       throw UsageError("unknown subcommand " + o.cmd);
     materials(o.materials);
   } catch (const std::exception& e) {
@@ -512,6 +540,7 @@ int main(int argc, char** argv) {
       if (o.cmd == "spmv") rs = cmd_apply(ctx, o, false);
       else if (o.cmd == "mfapply") rs = cmd_apply(ctx, o, true);
       else if (o.cmd == "solvers") rs = cmd_solvers(ctx, o);
+      else if (o.cmd == "direct") rs = cmd_direct(ctx, o);
       else rs = cmd_newton(ctx, o, log);
       write_csv(os, rs, o);
       if (!log.str().empty()) std::cerr << log.str();
