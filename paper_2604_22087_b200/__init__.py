@@ -175,6 +175,8 @@ def load():
         "afem_dist_solve": ([vp, vp, vp, vp, vp, vp, vp, vp, i32], i32),
         "afem_dist_dot": ([vp, vp, vp, vp, vp], i32),
         "afem_dist_assemble": ([vp, vp, vp], i32),
+        "afem_dist_solve_bvp": ([vp, vp, vp, vp, vp, vp, vp, i32], i32),
+        "afem_dist_load_stepping": ([vp, vp, f64, i32, f64, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sigs.items():
         f = getattr(L, name)
@@ -678,6 +680,31 @@ class Dist:
         return x, dict(converged=bool(rep.converged), iterations=rep.iterations,
                        residual_history=hist[:min(rep.n_history, cap)].copy(), wall_time=rep.wall_time,
                        failure=rep.failure.decode())
+
+    def solve_bvp(self, sys: System, rtol=1e-10, atol=1e-14, max_iter=25, lin_rtol=1e-13, lin_max_iter=10000,
+                  precond=JACOBI, x0=None):
+        """Distributed solve_bvp (collective): MATRIX_FREE operator, CG."""
+        cfg = afem_newton_cfg(rtol, atol, max_iter, MATRIX_FREE, afem_solver_cfg(CG, precond, lin_rtol, lin_max_iter, 30))
+        rep = afem_newton_report()
+        norms = np.zeros(max_iter + 2)
+        u = np.zeros(sys.n)
+        x0 = None if x0 is None else _f64(x0)
+        _check(_lib.afem_dist_solve_bvp(self.h, sys.h, C.byref(cfg), _ptr(x0), _ptr(u), C.byref(rep), _ptr(norms),
+                                        len(norms)))
+        return u, dict(converged=bool(rep.converged), iterations=rep.iterations,
+                       total_linear_iterations=rep.total_linear_iterations,
+                       residual_norms=norms[:rep.n_norms].copy(), failure=rep.failure.decode())
+
+    def load_stepping(self, sys: System, total_strain, n_steps, lx_global=1.0, rtol=1e-10, atol=1e-14, max_iter=25,
+                      lin_rtol=1e-13, lin_max_iter=10000, precond=JACOBI):
+        """Distributed load_stepping (collective) with per-rank J2 history commits."""
+        cfg = afem_newton_cfg(rtol, atol, max_iter, MATRIX_FREE, afem_solver_cfg(CG, precond, lin_rtol, lin_max_iter, 30))
+        u = np.zeros(sys.n)
+        failed, conv = C.c_int32(), C.c_int32()
+        its = np.zeros(n_steps, np.int32)
+        _check(_lib.afem_dist_load_stepping(self.h, sys.h, total_strain, n_steps, lx_global, C.byref(cfg), _ptr(u),
+                                            C.byref(failed), C.byref(conv), _ptr(its)))
+        return u, dict(converged=bool(conv.value), failed_step=failed.value, step_iterations=its)
 
     def assemble(self, op: LinearOperator, v):
         """Sum the shared planes of a slab-partial vector with the neighbours' partials."""

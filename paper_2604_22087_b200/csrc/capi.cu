@@ -330,6 +330,74 @@ void newton(System& s, const afem_newton_cfg* cfg, double* u, NewtonReport& rep)
   rep.total_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+__global__ void k_zero_masked(const uint8_t* mask, const double* v, double* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = mask[i] ? 0.0 : v[i];
+}
+
+// solve_bvp (newton.hpp:59-152) over a z-slab decomposition: each rank holds its slab's u (shared
+// node planes duplicated and kept identical); the residual's shared planes are summed over the
+// neighbours, the free norm is a global dot over owned dofs, and each Newton step solves the
+// distributed matrix-free system with the distributed Jacobi-PCG (the assembled tangent is not
+// distributed: operator_kind must be MATRIX_FREE). Collective: every rank calls it.
+void dist_newton(System& s, Comm* comm, const afem_newton_cfg* cfg, double* u, NewtonReport& rep) {
+  validate_newton(cfg);
+  if (cfg->operator_kind != 1)
+    throw CapabilityError("distributed solve_bvp: MATRIX_FREE only (the assembled tangent is not distributed)");
+  Ctx& c = *s.ctx;
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t n = s.n_dof;
+  const unsigned eg = grid_for(n, 256, 148 * 16);
+  impose_dirichlet(s, u);
+  DevArray<double> R(n), rhs(n), du(n), Rm(n);
+  std::unique_ptr<DistMfOp> op = make_dist_mf_op(s, comm, make_mf_op(s, u));
+  auto global_residual = [&]() -> double {
+    residual(s, u, R.p);
+    op->halo_add(R.p, nullptr, false);  // sum the shared planes' partial sums
+    launch(c, k_zero_masked, eg, 256, 0, s.mask.p, R.p, Rm.p, n);
+    return std::sqrt(dist_dot(*op, Rm.p, Rm.p));  // free_norm (newton.hpp:46-51), owned dofs
+  };
+  double rnorm = global_residual();
+  const double r0 = rnorm;
+  rep.norms.push_back(rnorm);
+  const double target = std::max(cfg->rtol * r0, cfg->atol);
+  const SolverCfg lcfg = to_cfg(&cfg->linear);
+  while (true) {
+    if (!std::isfinite(rnorm)) {
+      rep.failure = "newton: non-finite residual norm at iteration " + std::to_string(rep.iterations);
+      break;
+    }
+    if (rnorm <= target) {
+      rep.converged = true;
+      break;
+    }
+    if (rep.iterations >= cfg->max_iter) {
+      rep.failure = "newton: no convergence within " + std::to_string(cfg->max_iter) + " iterations (residual " +
+                    std::to_string(rnorm) + ")";
+      break;
+    }
+    copy(c, R.p, rhs.p, n);
+    constrain_residual(s, rhs.p, u);
+    scal(c, -1.0, rhs.p, n);
+    SolveReport lin;
+    dist_solve(*op, lcfg, rhs.p, nullptr, du.p, lin);
+    rep.linear.push_back(lin);
+    if (!lin.converged) {
+      rep.failure = "newton: linear solve failed at iteration " + std::to_string(rep.iterations + 1) +
+                    (lin.failure.empty() ? " (tolerance not reached)" : " (" + lin.failure + ")");
+      break;
+    }
+    axpy(c, 1.0, du.p, u, n);
+    impose_dirichlet(s, u);
+    op = make_dist_mf_op(s, comm, make_mf_op(s, u));
+    rnorm = global_residual();
+    ++rep.iterations;
+    rep.norms.push_back(rnorm);
+  }
+  AFEM_CK(cudaStreamSynchronize(c.stream));
+  rep.total_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 void fill_newton(const NewtonReport& r, afem_newton_report* out, double* norms, int32_t cap) {
   if (!out) return;
   out->converged = r.converged;
@@ -1160,6 +1228,60 @@ afem_status afem_dist_assemble(afem_dist d, afem_op op, double* v) {
     Out<double> dv(c, v, dop->n, true);
     dop->halo_add(dv.d, nullptr, false);
     dv.finish();
+  });
+}
+
+afem_status afem_dist_solve_bvp(afem_dist d, afem_system slab, const afem_newton_cfg* cfg, const double* x0, double* u,
+                                afem_newton_report* rep, double* norms, int32_t norms_cap) {
+  return guarded([&] {
+    need(d, "dist");
+    need(cfg, "cfg");
+    need(u, "u");
+    System& s = SYS(slab);
+    Ctx& c = *s.ctx;
+    Out<double> du(c, u, s.n_dof, false);
+    if (x0) {
+      In<double> dx0(c, x0, s.n_dof);
+      copy(c, dx0.d, du.d, s.n_dof);
+    } else {
+      fill(c, 0.0, du.d, s.n_dof);
+    }
+    NewtonReport r;
+    dist_newton(s, d->comm.get(), cfg, du.d, r);
+    du.finish();
+    fill_newton(r, rep, norms, norms_cap);
+  });
+}
+
+afem_status afem_dist_load_stepping(afem_dist d, afem_system slab, double total_strain, int32_t n_steps,
+                                    double lx_global, const afem_newton_cfg* cfg, double* u, int32_t* failed_step,
+                                    int32_t* converged, int32_t* step_iterations) {
+  return guarded([&] {
+    need(d, "dist");
+    need(cfg, "cfg");
+    need(u, "u");
+    if (n_steps < 1) throw std::invalid_argument("load_stepping: n_steps must be >= 1");
+    System& s = SYS(slab);
+    Ctx& c = *s.ctx;
+    Out<double> du(c, u, s.n_dof, false);
+    fill(c, 0.0, du.d, s.n_dof);
+    if (failed_step) *failed_step = -1;
+    if (converged) *converged = 0;
+    for (int st = 1; st <= n_steps; ++st) {
+      const double strain = total_strain * st / n_steps;  // newton.hpp:171
+      set_dirichlet(s, slab_benchmark_bcs(s, d->comm->rank, d->comm->size, strain, lx_global));
+      NewtonReport r;
+      dist_newton(s, d->comm.get(), cfg, du.d, r);
+      if (step_iterations) step_iterations[st - 1] = r.iterations;
+      if (!r.converged) {
+        if (failed_step) *failed_step = st;
+        du.finish();
+        return;
+      }
+      history_commit(s, du.d);  // J2 history is element-local: each rank commits its own slab
+    }
+    if (converged) *converged = 1;
+    du.finish();
   });
 }
 

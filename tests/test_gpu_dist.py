@@ -102,3 +102,47 @@ def test_nccl_backend_single_rank(afem):
     xs, rep = d.run_solver(dop, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
     assert rep["converged"] and abs(rep["iterations"] - rg["iterations"]) <= max(2, rg["iterations"] // 100), (rep, rg)
     assert rel_err(xs, xg) <= 1e-8
+
+
+J2_MIX = [(3, 1.0, 0.3, 0.002, 0.1), (0, 10.0, 0.3)]
+
+
+@pytest.mark.parametrize("size", [2, 3])
+def test_distributed_j2_load_stepping_matches_single_domain(afem, size):
+    """Config 4 in miniature, slab-sharded: per-rank J2 history, distributed Newton (MF, CG+Jacobi)
+    with shared-plane residual assembly and a global free norm; vs the single-domain load path."""
+    nx, ny, nz = 8, 8, 12
+    ctx = afem.Context(0)
+    fib = afem.fibres(12345, 4)
+    g = afem.System.grid(ctx, 3, nx, ny, nz, inclusions=fib, radius=0.2, materials=J2_MIX)
+    ug, rg = g.load_stepping(0.01, 3, operator_kind=afem.MATRIX_FREE, lin_rtol=1e-12)
+    assert rg["converged"]
+    hg = g.history().reshape(nz, ny * nx * 8 * 8)
+    group = afem.ThreadGroup(size)
+    plane = 3 * (nx + 1) * (ny + 1)
+    results = {}
+
+    def work(rank):
+        try:
+            c = afem.Context(0)
+            s, (z0, z1) = afem.slab_system(c, nx, ny, nz, rank, size, inclusions=fib, radius=0.2, materials=J2_MIX)
+            d = afem.Dist(c, rank, size, backend="threads", group=group)
+            u, rep = d.load_stepping(s, 0.01, 3, lx_global=1.0, lin_rtol=1e-12)
+            results[rank] = dict(z=(z0, z1), u=u, rep=rep, hist=s.history())
+        except Exception as e:  # surfaced below
+            results[rank] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(size)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for r in range(size):
+        assert not isinstance(results[r], Exception), results[r]
+        res = results[r]
+        z0, z1 = res["z"]
+        assert res["rep"]["converged"]
+        assert list(res["rep"]["step_iterations"]) == list(rg["step_iterations"])
+        assert rel_err(res["u"], ug[plane * z0: plane * (z1 + 1)]) <= 1e-8
+        # the rank's committed history is the single-domain history of its element layers
+        assert rel_err(res["hist"], hg[z0:z1].ravel()) <= 1e-8
