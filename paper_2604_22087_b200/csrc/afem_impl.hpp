@@ -117,6 +117,9 @@ struct Operator {
   virtual bool uses_stencil() const { return false; }
   // pattern-ordered CSR values when the operator is the assembled matrix (persistent small-n CG)
   virtual const double* csr_values() const { return nullptr; }
+  // device flag: while *flag != 0 the apply returns at once (the CG loop's speculative chunk after
+  // convergence); false when the operator cannot skip
+  virtual bool set_skip(const int*) { return false; }
 };
 
 struct ExplicitOp : Operator {
@@ -137,6 +140,11 @@ struct MfOp : Operator {
   bool apply_dot(const double* x, double* y, double* dot_out) override;
   void diagonal(double* d) override;
   bool uses_stencil() const override { return stencil != nullptr; }
+  const int* skip = nullptr;
+  bool set_skip(const int* flag) override {
+    skip = flag;
+    return stencil != nullptr;
+  }
 };
 
 // ---- system.cu
@@ -211,7 +219,8 @@ bool direct_solve(System& s, const double* vals, bool chol, const double* b, dou
 
 // ---- stencil.cu
 StencilPlan* make_stencil_plan(System& s, const MfOp& op);  // nullptr when not applicable
-void stencil_apply(StencilPlan& p, const MfOp& op, const double* x, double* y, double* dot_out = nullptr);
+void stencil_apply(StencilPlan& p, const MfOp& op, const double* x, double* y, double* dot_out = nullptr,
+                   const int* skip = nullptr);
 int stencil_pieces(const StencilPlan& p);
 int stencil_piece_planes(const StencilPlan& p);
 void stencil_apply_pieces(StencilPlan& p, const MfOp& op, const double* x, double* y, int pa, int pb);

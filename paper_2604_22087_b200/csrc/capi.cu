@@ -51,13 +51,13 @@ void ExplicitOp::diagonal(double* d) { csr_diagonal(*sys, buf->store.p, d); }
 
 MfOp::~MfOp() { destroy_stencil_plan(stencil); }
 void MfOp::apply(const double* x, double* y) {
-  if (stencil) stencil_apply(*stencil, *this, x, y);
+  if (stencil) stencil_apply(*stencil, *this, x, y, nullptr, skip);
   else mf_apply_general(*sys, state.p, mask.p, x, y);
 }
 bool MfOp::apply_dot(const double* x, double* y, double* dot_out) {
   static const bool disabled = std::getenv("AFEM_NO_FUSED_DOT") != nullptr;
   if (!stencil || disabled) return false;
-  stencil_apply(*stencil, *this, x, y, dot_out);
+  stencil_apply(*stencil, *this, x, y, dot_out, skip);
   return true;
 }
 void MfOp::diagonal(double* d) { copy(*sys->ctx, diag.p, d, n); }

@@ -433,21 +433,76 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
       int chunk = 4;
       if (cg_persistent(op, x, r.p, p.p, ap.p, inv, st.p, hist.p)) {
         hs = fetch(c, st.p);
-      } else while (true) {
-        for (int k = 0; k < chunk; ++k) {
-          // fused operators write p^T A p straight into st->pap; others get the reduction kernel
-          double* pap_dev = reinterpret_cast<double*>(reinterpret_cast<char*>(st.p) + offsetof(CgDev, pap));
-          if (!op.apply_dot(p.p, ap.p, pap_dev)) {
-            op.apply(p.p, ap.p);
-            launch(c, k_cg_pap, rg, kRedThreads, 0, p.p, ap.p, n, c.red_partials.p, c.red_counter.p, st.p);
+      } else {
+        auto enqueue = [&](int cnt) {
+          for (int k = 0; k < cnt; ++k) {
+            // fused operators write p^T A p straight into st->pap; others get the reduction kernel
+            double* pap_dev = reinterpret_cast<double*>(reinterpret_cast<char*>(st.p) + offsetof(CgDev, pap));
+            if (!op.apply_dot(p.p, ap.p, pap_dev)) {
+              op.apply(p.p, ap.p);
+              launch(c, k_cg_pap, rg, kRedThreads, 0, p.p, ap.p, n, c.red_partials.p, c.red_counter.p, st.p);
+            }
+            launch(c, k_cg_update, rg, kRedThreads, 0, x, p.p, r.p, ap.p, inv, n, c.red_partials.p,
+                   c.red_counter.p, st.p, hist.p);
+            launch(c, k_cg_p, eg, 256, 0, r.p, inv, p.p, n, st.p);
           }
-          launch(c, k_cg_update, rg, kRedThreads, 0, x, p.p, r.p, ap.p, inv, n, c.red_partials.p, c.red_counter.p,
-                 st.p, hist.p);
-          launch(c, k_cg_p, eg, 256, 0, r.p, inv, p.p, n, st.p);
+        };
+        // Operators that can skip on the device-side done flag get one chunk enqueued ahead of the
+        // host's check of the previous one, so the GPU never drains at a chunk boundary; the
+        // speculative iterations after convergence are no-ops (every kernel tests the flag).
+        const int* done_dev = reinterpret_cast<const int*>(reinterpret_cast<const char*>(st.p) + offsetof(CgDev, done));
+        const bool spec = op.set_skip(done_dev);
+        if (!spec) {
+          while (true) {
+            enqueue(chunk);
+            hs = fetch(c, st.p);
+            if (hs.done) break;
+            chunk = std::min(chunk * 2, 64);
+          }
+        } else {
+          // the iteration loop as a CUDA graph of kGraphIters iterations (captured once per solve):
+          // one launch per chunk instead of four per iteration, so host hiccups cannot drain the GPU
+          constexpr int kGraphIters = 16;
+          static thread_local CgDev* hst = nullptr;
+          static thread_local cudaEvent_t ev = nullptr;
+          if (!hst) AFEM_CK(cudaMallocHost(reinterpret_cast<void**>(&hst), sizeof(CgDev)));
+          if (!ev) AFEM_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          cudaGraph_t graph = nullptr;
+          cudaGraphExec_t exec = nullptr;
+          const int64_t l0 = c.launches;
+          // capture on a private stream (the context stream may be the legacy default stream, which
+          // cannot capture); the instantiated graph is launched on the context stream
+          static thread_local cudaStream_t cap = nullptr;
+          if (!cap) AFEM_CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+          cudaStream_t home = c.stream;
+          c.stream = cap;
+          AFEM_CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+          enqueue(kGraphIters);
+          const cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+          c.stream = home;
+          AFEM_CK(ce);
+          const int64_t per_graph = c.launches - l0;
+          c.launches = l0;
+          AFEM_CK(cudaGraphInstantiate(&exec, graph, 0));
+          auto run = [&] {
+            AFEM_CK(cudaGraphLaunch(exec, c.stream));
+            c.launches += per_graph;
+          };
+          run();
+          while (true) {
+            AFEM_CK(cudaMemcpyAsync(hst, st.p, sizeof(CgDev), cudaMemcpyDeviceToHost, c.stream));
+            AFEM_CK(cudaEventRecord(ev, c.stream));
+            run();  // speculative: no-ops once done
+            AFEM_CK(cudaEventSynchronize(ev));
+            hs = *hst;
+            if (hs.done) break;
+          }
+          AFEM_CK(cudaStreamSynchronize(c.stream));
+          hs = fetch(c, st.p);
+          cudaGraphExecDestroy(exec);
+          cudaGraphDestroy(graph);
+          op.set_skip(nullptr);
         }
-        hs = fetch(c, st.p);
-        if (hs.done) break;
-        chunk = std::min(chunk * 2, 64);
       }
       const int it0 = rep.iterations;
       rep.iterations = hs.it;

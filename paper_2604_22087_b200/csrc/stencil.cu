@@ -211,6 +211,7 @@ struct DotArgs {
   double* out;
   int finish;
   int n_main;  // number of main-kernel partials (read by the items kernel's last block)
+  const int* skip;  // CG speculation: the apply is a no-op while *skip != 0
 };
 
 constexpr int RING = 4;  // plane slots: p (computing), p+1 (landed), p+2 (in flight), one spare
@@ -222,6 +223,7 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm) k_stencil_main(const __g
                                                         const double* __restrict__ x,
                                                         const uint8_t* __restrict__ info, double* __restrict__ y,
                                                         int kchunk, int kbeg, int kend, DotArgs dot) {
+  if (dot.skip && *dot.skip) return;
   double dsum = 0.0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double (*sm)[TY + 2][RS] = reinterpret_cast<double (*)[TY + 2][RS]>(smem_raw);
@@ -406,6 +408,7 @@ __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, 
                                                                  const double* __restrict__ x,
                                                                  const uint8_t* __restrict__ info, Items it,
                                                                  double* __restrict__ y, DotArgs dot) {
+  if (dot.skip && *dot.skip) return;
   __shared__ double Ks[24][3][8];
   __shared__ double Es[32];
   for (int t = threadIdx.x; t < 576; t += blockDim.x) {  // Ks[q][a][ln] = Khat[3 ln + a][q]
@@ -871,12 +874,12 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   return plan.release();
 }
 
-void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, double* dot_out) {
+void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, double* dot_out, const int* skip) {
   Ctx& c = *op.sys->ctx;
   const StencilParams& P = pl.p;
   const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TY - 1) / TY, pl.nchunks);
   const int nb_main = P.NXm > 0 ? static_cast<int>(grid.x * grid.y * grid.z) : 0;
-  const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main};
+  const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main, skip};
   if (P.NXm > 0) {
     if (dot_out) launch(c, k_stencil_main<true>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, 0, P.NZ, dot);
     else launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, 0, P.NZ, dot);
@@ -902,7 +905,7 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
   const StencilParams& P = pl.p;
   const int kb = pa * pl.zpiece, ke = std::min(pb * pl.zpiece, P.NZ);
   if (kb >= ke) return;
-  const DotArgs dot{nullptr, nullptr, nullptr, nullptr, 0, 0};
+  const DotArgs dot{nullptr, nullptr, nullptr, nullptr, 0, 0, nullptr};
   if (P.NXm > 0) {  // a piece is a few planes: smaller z chunks so the launch still fills the GPU
     const int tiles = ((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY);
     const int want = std::max(1, kMainBlocksPerSm * c.num_sms / std::max(tiles, 1));
