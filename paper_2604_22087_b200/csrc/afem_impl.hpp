@@ -133,6 +133,7 @@ struct ExplicitOp : Operator {
 
 struct MfOp : Operator {
   DevArray<double> state, diag;
+  DevArray<double> qpt;  // cached Gauss-point tangents (J2 grids), elemgrid.cu
   DevArray<uint8_t> mask;
   StencilPlan* stencil = nullptr;  // owned; released by destroy_stencil_plan
   ~MfOp() override;
@@ -180,6 +181,9 @@ bool grid_elem_path(const System& s);
 void grid_residual(System& s, const double* u, double* r);
 void grid_diagonal(System& s, const double* u, double* d);
 void grid_mf_apply(System& s, const double* state, const uint8_t* mask, const double* x, double* y);
+bool grid_tangent_cacheable(const System& s);
+void grid_tangent_cache(System& s, const double* u, DevArray<double>& qpt);
+void grid_mf_apply_cached(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y);
 
 // ---- blas.cu (deterministic reductions; results in device scalars or host)
 double dot(Ctx& c, const double* x, const double* y, int64_t n);

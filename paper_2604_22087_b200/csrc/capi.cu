@@ -52,6 +52,7 @@ void ExplicitOp::diagonal(double* d) { csr_diagonal(*sys, buf->store.p, d); }
 MfOp::~MfOp() { destroy_stencil_plan(stencil); }
 void MfOp::apply(const double* x, double* y) {
   if (stencil) stencil_apply(*stencil, *this, x, y, nullptr, skip);
+  else if (qpt.p) grid_mf_apply_cached(*sys, qpt.p, mask.p, x, y);
   else mf_apply_general(*sys, state.p, mask.p, x, y);
 }
 bool MfOp::apply_dot(const double* x, double* y, double* dot_out) {
@@ -123,6 +124,7 @@ std::unique_ptr<MfOp> make_mf_op(System& s, const double* d_u) {
   diagonal(s, op->state.p, op->diag.p);  // validates the state (detJ, det F) like the reference's AD pass
   launch(*s.ctx, k_unit_on_mask, grid_for(s.n_dof, 256, 148 * 16), 256, 0, op->mask.p, op->diag.p, s.n_dof);
   op->stencil = make_stencil_plan(s, *op);
+  if (!op->stencil && grid_tangent_cacheable(s)) grid_tangent_cache(s, op->state.p, op->qpt);
   return op;
 }
 

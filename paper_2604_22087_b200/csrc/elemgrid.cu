@@ -169,6 +169,132 @@ __global__ void __launch_bounds__(256) k_gather(SysView s, const double* __restr
   }
 }
 
+
+// ---- cached consistent tangents (J2 + linear grids): the matrix-free operator's state is fixed, so
+// the return map of every J2 Gauss point is evaluated once at operator creation and its consistent
+// tangent stored as (lam_eff, mu_eff, g2, n[6]) (kQpt doubles per Gauss point, structure of arrays
+// [q][k][element] so a warp's loads are coalesced); each apply then costs
+// one gather, dH, the cached isotropic-plus-rank-one tangent and the projection per Gauss point.
+constexpr int kQpt = 9;
+
+template <int D>
+__global__ void __launch_bounds__(128) k_grid_qp_tangent(const __grid_constant__ GeoT<D> G, SysView s, int nx, int ny,
+                                                         const double* __restrict__ u, double* __restrict__ qpt) {
+  constexpr int npe = EL<D>::npe, nq = EL<D>::nq, nd = EL<D>::nd;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s.n_elem; e += (int64_t)gridDim.x * blockDim.x) {
+    const DMat m = s.mats[s.phase[e]];
+    if (m.model != MODEL_J2) continue;
+    int64_t nodes[npe];
+    elem_nodes<D>(e, nx, ny, nodes);
+    double ue[nd];
+#pragma unroll
+    for (int k = 0; k < npe; ++k)
+#pragma unroll
+      for (int c = 0; c < D; ++c) ue[k * D + c] = __ldg(&u[nodes[k] * D + c]);
+    for (int q = 0; q < nq; ++q) {
+      double H[D][D];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          double t = 0.0;
+#pragma unroll
+          for (int i = 0; i < npe; ++i) t += ue[D * i + a] * G.g[q][i][b];
+          H[a][b] = t;
+        }
+      J2QP j;
+      j2_state<D>(m, H, s.hist + (e * nq + q) * kHist, j);
+      const int64_t ne = s.n_elem;
+      double* o = qpt + (int64_t)q * kQpt * ne + e;
+      const double mu_eff = m.mu * j.beta;
+      o[0 * ne] = m.kappa - 2.0 * mu_eff / 3.0;
+      o[1 * ne] = mu_eff;
+      o[2 * ne] = 2.0 * m.mu * j.gbar;
+      o[3 * ne] = j.n[0][0]; o[4 * ne] = j.n[1][1]; o[5 * ne] = j.n[2][2];
+      o[6 * ne] = j.n[1][2]; o[7 * ne] = j.n[0][2]; o[8 * ne] = j.n[0][1];
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) k_grid_jvp_cached(const __grid_constant__ GeoT<D> G, SysView s, int nx, int ny,
+                                                         const double* __restrict__ qpt,
+                                                         const uint8_t* __restrict__ mask,
+                                                         const double* __restrict__ x, double* __restrict__ ev) {
+  constexpr int npe = EL<D>::npe, nq = EL<D>::nq, nd = EL<D>::nd;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s.n_elem; e += (int64_t)gridDim.x * blockDim.x) {
+    const DMat m = s.mats[s.phase[e]];
+    const bool j2 = m.model == MODEL_J2;
+    int64_t nodes[npe];
+    elem_nodes<D>(e, nx, ny, nodes);
+    double xe[nd];
+#pragma unroll
+    for (int k = 0; k < npe; ++k)
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const int64_t d = nodes[k] * D + c;
+        xe[k * D + c] = mask[d] ? 0.0 : __ldg(&x[d]);
+      }
+    double f[nd];
+#pragma unroll
+    for (int k = 0; k < nd; ++k) f[k] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < nq; ++q) {
+      double dH[D][D];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          double t = 0.0;
+#pragma unroll
+          for (int i = 0; i < npe; ++i) t += xe[D * i + a] * G.g[q][i][b];
+          dH[a][b] = t;
+        }
+      double P[D][D];
+      if (j2) {  // lam tr(de) I + 2 mu de - g2 (n : de) n with the cached tangent
+        const int64_t ne = s.n_elem;
+        const double* t = qpt + (int64_t)q * kQpt * ne + e;
+        const double lam = __ldg(t), mu = __ldg(t + ne), g2 = __ldg(t + 2 * ne);
+        const double n00 = __ldg(t + 3 * ne), n11 = __ldg(t + 4 * ne), n22 = __ldg(t + 5 * ne);
+        const double n12 = __ldg(t + 6 * ne), n02 = __ldg(t + 7 * ne), n01 = __ldg(t + 8 * ne);
+        const double n3[3][3] = {{n00, n01, n02}, {n01, n11, n12}, {n02, n12, n22}};
+        double tr = 0.0, nde = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          tr += dH[a][a];
+#pragma unroll
+          for (int b = 0; b < D; ++b) nde += n3[a][b] * 0.5 * (dH[a][b] + dH[b][a]);
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b < D; ++b)
+            P[a][b] = (a == b ? lam * tr : 0.0) + mu * (dH[a][b] + dH[b][a]) - g2 * nde * n3[a][b];
+      } else {
+        stress_linear<D>(m, dH, P);
+      }
+      const double wdet = G.wdet[q];
+#pragma unroll
+      for (int i = 0; i < npe; ++i)
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          double t = 0.0;
+#pragma unroll
+          for (int b = 0; b < D; ++b) t += P[a][b] * G.g[q][i][b];
+          f[D * i + a] += wdet * t;
+        }
+    }
+    double2* o = reinterpret_cast<double2*>(ev + e * nd);
+#pragma unroll
+    for (int k = 0; k < nd / 2; ++k) o[k] = make_double2(f[2 * k], f[2 * k + 1]);
+  }
+}
+
+template <int D>
+void geo(const System& s, GeoT<D>& G) {
+  std::memcpy(&G, s.grid_geo.data(), sizeof G);
+}
+
 template <int D, int MODE>
 void run(System& s, const double* u, const uint8_t* mask, const double* x, double* y) {
   GeoT<D> G;
@@ -181,7 +307,44 @@ void run(System& s, const double* u, const uint8_t* mask, const double* x, doubl
          MODE == EV_JVP ? mask : nullptr, x, y);
 }
 
+template <int D>
+void cached_tangent(System& s, const double* u, DevArray<double>& qpt) {
+  GeoT<D> G;
+  geo<D>(s, G);
+  qpt.alloc((size_t)s.n_elem * EL<D>::nq * kQpt);
+  launch(*s.ctx, k_grid_qp_tangent<D>, grid_for(s.n_elem, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, u, qpt.p);
+}
+
+template <int D>
+void cached_apply(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y) {
+  GeoT<D> G;
+  geo<D>(s, G);
+  if (!s.ev.p) s.ev.alloc((size_t)s.n_elem * EL<D>::nd);
+  launch(*s.ctx, k_grid_jvp_cached<D>, grid_for(s.n_elem, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, qpt, mask,
+         x, s.ev.p);
+  launch(*s.ctx, k_gather<D>, grid_for(s.n_nodes, 256, 148 * 32), 256, 0, s.view(), s.ev.p, mask, x, y);
+}
+
 }  // namespace
+
+// J2 (+ linear) grid systems: the operator's Gauss-point tangents can be cached.
+bool grid_tangent_cacheable(const System& s) {
+  static const bool off = std::getenv("AFEM_NO_TANGENT_CACHE") != nullptr;
+  if (off || !grid_elem_path(s) || !s.has_history()) return false;
+  for (const DMat& m : s.mats)
+    if (m.model != MODEL_LINEAR && m.model != MODEL_J2) return false;
+  return true;
+}
+
+void grid_tangent_cache(System& s, const double* u, DevArray<double>& qpt) {
+  if (s.dim == 2) cached_tangent<2>(s, u, qpt);
+  else cached_tangent<3>(s, u, qpt);
+}
+
+void grid_mf_apply_cached(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y) {
+  if (s.dim == 2) cached_apply<2>(s, qpt, mask, x, y);
+  else cached_apply<3>(s, qpt, mask, x, y);
+}
 
 void grid_geometry(System& s) {
   const size_t n = s.dim == 2 ? (4 * 4 * 2 + 4) : (8 * 8 * 3 + 8);
