@@ -79,10 +79,13 @@ __global__ void k_cg_pap(const double* p, const double* ap, int64_t n, double* p
 // rz / pAp, where pAp was produced by k_cg_pap or fused into the operator apply.
 __global__ void k_cg_update(double* x, const double* p, double* r, const double* ap, const double* inv, int64_t n,
                             double* partials, unsigned int* counter, CgDev* st, double* hist) {
+  // r -= alpha Ap and (r.r, r.z) with z = M r on the fly; x += alpha p is deferred to k_cg_p, which
+  // reads p anyway (the converging iteration's x update is applied by the host loop's epilogue)
   if (st->done) return;
   const double pap = st->pap;
   if (!(pap > 0.0)) {  // krylov.hpp:377-381
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->alpha = 0.0;
       st->fail = 1;
       st->done = 1;
     }
@@ -92,20 +95,15 @@ __global__ void k_cg_update(double* x, const double* p, double* r, const double*
   double rr = 0.0, rz = 0.0;
   // 16-byte vector body (device allocations are 256-byte aligned) + scalar tail
   const int64_t n2 = n / 2;
-  double2* x2 = reinterpret_cast<double2*>(x);
   double2* r2 = reinterpret_cast<double2*>(r);
-  const double2* p2 = reinterpret_cast<const double2*>(p);
   const double2* ap2 = reinterpret_cast<const double2*>(ap);
   const double2* inv2 = reinterpret_cast<const double2*>(inv);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
-    const double2 pv = __ldcs(&p2[i]), av = __ldcs(&ap2[i]);
-    double2 xv = __ldcs(&x2[i]), rv = __ldcs(&r2[i]);
-    xv.x += a * pv.x;
-    xv.y += a * pv.y;
+    const double2 av = __ldcs(&ap2[i]);
+    double2 rv = r2[i];
     rv.x -= a * av.x;
     rv.y -= a * av.y;
-    __stcs(&x2[i], xv);
-    __stcs(&r2[i], rv);
+    r2[i] = rv;
     double zx = rv.x, zy = rv.y;
     if (inv) {
       const double2 iv = __ldg(&inv2[i]);
@@ -117,7 +115,6 @@ __global__ void k_cg_update(double* x, const double* p, double* r, const double*
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
     const int64_t i = n - 1;
-    x[i] += a * p[i];
     const double ri = r[i] - a * ap[i];
     r[i] = ri;
     const double zi = inv ? ri * inv[i] : ri;
@@ -129,6 +126,7 @@ __global__ void k_cg_update(double* x, const double* p, double* r, const double*
     if (threadIdx.x == 0) {
       const int it = st->it + 1;
       st->it = it;
+      st->alpha = a;
       const double h = sqrt(v[0]) / st->denom;
       hist[it] = h;
       if (h <= st->rtol) {
@@ -140,33 +138,48 @@ __global__ void k_cg_update(double* x, const double* p, double* r, const double*
         if (it >= st->max_iter) st->done = 1;
       }
     }
+  (void)x;
+  (void)p;
 }
 
-// p = M r + beta p
-__global__ void k_cg_p(const double* __restrict__ r, const double* __restrict__ inv, double* __restrict__ p, int64_t n,
-                       const CgDev* st) {
+// x += alpha p (the deferred update of k_cg_update), then p = M r + beta p
+__global__ void k_cg_p(const double* __restrict__ r, const double* __restrict__ inv, double* __restrict__ p,
+                       double* __restrict__ x, int64_t n, const CgDev* st) {
   if (st->done) return;
-  const double b = st->beta;
+  const double a = st->alpha, b = st->beta;
   const int64_t n2 = n / 2;
   const double2* r2 = reinterpret_cast<const double2*>(r);
   const double2* inv2 = reinterpret_cast<const double2*>(inv);
   double2* p2 = reinterpret_cast<double2*>(p);
+  double2* x2 = reinterpret_cast<double2*>(x);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
-    double2 z = __ldg(&r2[i]);
+    double2 z = __ldcs(&r2[i]);
     if (inv) {
       const double2 iv = __ldg(&inv2[i]);
       z.x *= iv.x;
       z.y *= iv.y;
     }
     double2 pv = p2[i];
+    double2 xv = __ldcs(&x2[i]);
+    xv.x += a * pv.x;
+    xv.y += a * pv.y;
+    __stcs(&x2[i], xv);
     pv.x = z.x + b * pv.x;
     pv.y = z.y + b * pv.y;
     p2[i] = pv;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
     const int64_t i = n - 1;
+    x[i] += a * p[i];
     p[i] = (inv ? r[i] * inv[i] : r[i]) + b * p[i];
   }
+}
+
+// the converging (or last) iteration's deferred x += alpha p (alpha = 0 after a pAp failure)
+__global__ void k_cg_x_epilogue(double* __restrict__ x, const double* __restrict__ p, int64_t n, const CgDev* st) {
+  const double a = st->alpha;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] += a * p[i];
 }
 
 __global__ void k_inv_diag(const double* d, double* inv, int64_t n, unsigned long long* first_zero) {
@@ -431,7 +444,8 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
     if (rep.history.back() > cfg.rtol && rep.iterations < cfg.max_iter) {
       launch(c, k_cg_start, rg, kRedThreads, 0, r.p, inv, p.p, n, c.red_partials.p, c.red_counter.p, st.p);
       int chunk = 4;
-      if (cg_persistent(op, x, r.p, p.p, ap.p, inv, st.p, hist.p)) {
+      const bool persistent = cg_persistent(op, x, r.p, p.p, ap.p, inv, st.p, hist.p);
+      if (persistent) {
         hs = fetch(c, st.p);
       } else {
         auto enqueue = [&](int cnt) {
@@ -444,7 +458,7 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
             }
             launch(c, k_cg_update, rg, kRedThreads, 0, x, p.p, r.p, ap.p, inv, n, c.red_partials.p,
                    c.red_counter.p, st.p, hist.p);
-            launch(c, k_cg_p, eg, 256, 0, r.p, inv, p.p, n, st.p);
+            launch(c, k_cg_p, eg, 256, 0, r.p, inv, p.p, x, n, st.p);
           }
         };
         // Operators that can skip on the device-side done flag get one chunk enqueued ahead of the
@@ -504,6 +518,7 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
           op.set_skip(nullptr);
         }
       }
+      if (!persistent) launch(c, k_cg_x_epilogue, eg, 256, 0, x, p.p, n, st.p);
       const int it0 = rep.iterations;
       rep.iterations = hs.it;
       if (hs.it > it0) {
