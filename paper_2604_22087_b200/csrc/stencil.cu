@@ -52,6 +52,15 @@ struct StencilParams {
   int NXm;                     // node columns the main kernel covers (tiles of 64; the last may be partial)
 };
 
+// Rows of Khat for the element corner at bit position 0 (hex node local_node(0, 0, 0)), columns in
+// bit-corner order: k[a][3 b + c] = Khat(node 0, corner with bits b)[a][c]. The brick is symmetric
+// under the reflections of each axis, so every other corner's rows follow by reflecting the
+// element (permuted corners, sign flips of the reflected components): the coefficients are the
+// same for every lane and live in the constant bank.
+struct RowsK0 {
+  double k[3][24];
+};
+
 struct StencilPlan {
   StencilParams p;
   DevArray<uint8_t> info;       // per node: bits 0-2 Dirichlet mask, bits 3-7 base phase code
@@ -62,7 +71,8 @@ struct StencilPlan {
   int item_blocks = 1;
   DevArray<double> part_main, part_items;  // fused p.Ap partials (main kernel, item kernel)
   DevArray<unsigned int> counter;
-  DevArray<double> Kg;   // Khat (row-major 24 x 24) in global memory for the correction kernels
+  DevArray<double> Kg;   // Khat (row-major 24 x 24)
+  RowsK0 k0;             // the correction kernel's coefficients
   int64_t n_items = 0;   // tile correction items incl. padding
   int64_t n_fix_nodes = 0, n_edge_nodes = 0;
   int kchunk = 16;
@@ -403,19 +413,16 @@ struct Items {
 };
 
 template <bool DOT>
-__global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, const double* __restrict__ Kg,
+__global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, const __grid_constant__ RowsK0 K0,
                                                                  const double* __restrict__ Epar,
                                                                  const double* __restrict__ x,
                                                                  const uint8_t* __restrict__ info, Items it,
                                                                  double* __restrict__ y, DotArgs dot) {
   if (dot.skip && *dot.skip) return;
-  __shared__ double Ks[24][3][8];
   __shared__ double Es[32];
-  for (int t = threadIdx.x; t < 576; t += blockDim.x) {  // Ks[q][a][ln] = Khat[3 ln + a][q]
-    const int r = t / 24, q = t % 24;
-    Ks[q][r % 3][r / 3] = __ldg(&Kg[t]);
-  }
+  __shared__ __align__(16) double Ks[3][24];  // every lane reads the same word: broadcasts, 16-byte pairs
   if (threadIdx.x < 32) Es[threadIdx.x] = __ldg(&Epar[threadIdx.x]);
+  if (threadIdx.x < 72) Ks[threadIdx.x / 24][threadIdx.x % 24] = K0.k[threadIdx.x / 24][threadIdx.x % 24];
   __syncthreads();
   double dsum = 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -457,32 +464,35 @@ __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, 
       const int j = rr % NY, k = rr / NY;
       const int o = w & 7;
       const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
-      const int ln = local_node(1 - ox, 1 - oy, 1 - oz);
+      const int rm = (1 - ox) | ((1 - oy) << 1) | ((1 - oz) << 2);  // the node's bit corner in the element
       const int e0 = (i - 1 + ox) + NX * (j - 1 + oy) + NXY * (k - 1 + oz);  // may lie outside (masked)
-      double xv[24];
+      // reflected frame: the node sits at bit corner 0; frame corner b is element corner b ^ rm, and
+      // component c of x and row c of y flip sign with bit c of rm
+      const double s0 = (rm & 1) ? -1.0 : 1.0, s1 = (rm & 2) ? -1.0 : 1.0, s2 = (rm & 4) ? -1.0 : 1.0;
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {  // a node's 24-byte record in two requests: 16 B aligned + 8 B
-        const int nd = e0 + corner_x(m) + NX * corner_y(m) + NXY * (m >> 2);
-        const uint32_t zb = (zm >> (3 * m)) & 7;
+      for (int b = 0; b < 8; ++b) {
+        const int pb = b ^ rm;
+        const int nd = e0 + (pb & 1) + NX * ((pb >> 1) & 1) + NXY * (pb >> 2);
+        const uint32_t zb = (zm >> (3 * local_node(pb & 1, (pb >> 1) & 1, pb >> 2))) & 7;
         const int a0 = zb == 7 ? 0 : 3 * nd;  // all-zero corners (outside) read a safe address
         const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);  // 16 B-aligned pair
         const double2 pr = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
         const double sg = __ldg(x + (odd ? a0 : a0 + 2));
-        const double c0 = odd ? sg : pr.x, c1 = odd ? pr.x : pr.y, c2 = odd ? pr.y : sg;
-        xv[3 * m + 0] = (zb & 1) ? 0.0 : c0;
-        xv[3 * m + 1] = (zb & 2) ? 0.0 : c1;
-        xv[3 * m + 2] = (zb & 4) ? 0.0 : c2;
-      }
+        const double c0 = (zb & 1) ? 0.0 : s0 * (odd ? sg : pr.x);
+        const double c1 = (zb & 2) ? 0.0 : s1 * (odd ? pr.x : pr.y);
+        const double c2 = (zb & 4) ? 0.0 : s2 * (odd ? pr.y : sg);
+        const double cv[3] = {c0, c1, c2};
 #pragma unroll
-      for (int q = 0; q < 24; ++q) {
-        r0 = fma(Ks[q][0][ln], xv[q], r0);
-        r1 = fma(Ks[q][1][ln], xv[q], r1);
-        r2 = fma(Ks[q][2][ln], xv[q], r2);
+        for (int cc = 0; cc < 3; ++cc) {
+          r0 = fma(Ks[0][3 * b + cc], cv[cc], r0);
+          r1 = fma(Ks[1][3 * b + cc], cv[cc], r1);
+          r2 = fma(Ks[2][3 * b + cc], cv[cc], r2);
+        }
       }
       const double dE = Es[(w >> 8) & 31] - Es[(w >> 13) & 31];
-      r0 *= dE;
-      r1 *= dE;
-      r2 *= dE;
+      r0 *= s0 * dE;
+      r1 *= s1 * dE;
+      r2 *= s2 * dE;
     }
     // segmented tree sum: rem = items from this lane to its segment's end (<= 8, never crossing the
     // batch); after the step with offset d every lane holds the sum of [lane, min(lane + 2d, end))
@@ -664,6 +674,13 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   for (int r = 0; r < 24; ++r)
     for (int q = 0; q < 24; ++q) P.K[r][q] = K[r * 24 + q];
   plan->Kg = std::move(dK);
+  {
+    const int r0 = 3 * local_node(0, 0, 0);
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 8; ++b)
+        for (int cc = 0; cc < 3; ++cc)
+          plan->k0.k[a][3 * b + cc] = K[(r0 + a) * 24 + 3 * local_node(b & 1, (b >> 1) & 1, b >> 2) + cc];
+  }
   double fam[27][3][3];
   family_stencil(K, 0, 0, fam);
   if (!snap(fam, 0)) return nullptr;
@@ -887,10 +904,10 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, 
   if (pl.n_items > 0) {
     const Items it{pl.it_rec.p, pl.it_zm.p, pl.n_items};
     if (dot_out)
-      launch(c, k_stencil_items<true>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.Kg.p, pl.Ed.p, x, pl.info.p,
+      launch(c, k_stencil_items<true>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p,
              it, y, dot);
     else
-      launch(c, k_stencil_items<false>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.Kg.p, pl.Ed.p, x, pl.info.p,
+      launch(c, k_stencil_items<false>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p,
              it, y, dot);
   }
 }
@@ -917,7 +934,7 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
   if (i1 > i0) {
     const Items it{pl.it_rec.p + i0, pl.it_zm.p + i0, i1 - i0};
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((i1 - i0) / 256, (int64_t)pl.iocc * c.num_sms)));
-    launch(c, k_stencil_items<false>, blocks, kItemThreads, 0, P.NX, P.NY, pl.Kg.p, pl.Ed.p, x, pl.info.p, it, y, dot);
+    launch(c, k_stencil_items<false>, blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p, it, y, dot);
   }
 }
 
