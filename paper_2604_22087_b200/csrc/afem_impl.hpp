@@ -129,6 +129,11 @@ struct ExplicitOp : Operator {
   void apply(const double* x, double* y) override;
   void diagonal(double* d) override;
   const double* csr_values() const override { return buf->store.p; }
+  const int* skip = nullptr;
+  bool set_skip(const int* flag) override {
+    skip = flag;
+    return true;
+  }
 };
 
 struct MfOp : Operator {
@@ -144,7 +149,7 @@ struct MfOp : Operator {
   const int* skip = nullptr;
   bool set_skip(const int* flag) override {
     skip = flag;
-    return stencil != nullptr;
+    return stencil != nullptr || qpt.p != nullptr;
   }
 };
 
@@ -171,7 +176,7 @@ void diagonal(System& s, const double* u, double* d);
 void mf_apply_general(System& s, const double* state, const uint8_t* mask, const double* x, double* y);
 void eliminate(System& s, double* values, double* residual, const double* u);
 void constrain_residual(System& s, double* residual, const double* u);
-void csr_apply(System& s, const double* values, const double* x, double* y);
+void csr_apply(System& s, const double* values, const double* x, double* y, const int* skip = nullptr);
 void csr_diagonal(System& s, const double* values, double* d);
 void impose_dirichlet(System& s, double* u);
 
@@ -183,7 +188,8 @@ void grid_diagonal(System& s, const double* u, double* d);
 void grid_mf_apply(System& s, const double* state, const uint8_t* mask, const double* x, double* y);
 bool grid_tangent_cacheable(const System& s);
 void grid_tangent_cache(System& s, const double* u, DevArray<double>& qpt);
-void grid_mf_apply_cached(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y);
+void grid_mf_apply_cached(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y,
+                          const int* skip = nullptr);
 
 // ---- blas.cu (deterministic reductions; results in device scalars or host)
 double dot(Ctx& c, const double* x, const double* y, int64_t n);

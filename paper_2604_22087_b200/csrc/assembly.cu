@@ -314,7 +314,9 @@ __global__ void k_impose(const uint8_t* mask, const double* presc, double* u, in
 // y = A x over pattern-ordered values: one warp per node (its dim rows are contiguous).
 template <int D>
 __global__ void __launch_bounds__(256) k_csr_apply(SysView s, const double* __restrict__ values,
-                                                   const double* __restrict__ x, double* __restrict__ y) {
+                                                   const double* __restrict__ x, double* __restrict__ y,
+                                                   const int* skip) {
+  if (skip && *skip) return;  // the CG loop's speculative iterations after convergence
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t n = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; n < s.n_nodes; n += warps) {
@@ -423,10 +425,10 @@ void impose_dirichlet(System& s, double* u) {
   launch(*s.ctx, k_impose, grid_for(s.n_dof, 256, 148 * 64), 256, 0, s.mask.p, s.presc.p, u, s.n_dof);
 }
 
-void csr_apply(System& s, const double* values, const double* x, double* y) {
+void csr_apply(System& s, const double* values, const double* x, double* y, const int* skip) {
   const unsigned g = grid_for(s.n_nodes * 32, 256, 148 * 64);
-  if (s.dim == 2) launch(*s.ctx, k_csr_apply<2>, g, 256, 0, s.view(), values, x, y);
-  else launch(*s.ctx, k_csr_apply<3>, g, 256, 0, s.view(), values, x, y);
+  if (s.dim == 2) launch(*s.ctx, k_csr_apply<2>, g, 256, 0, s.view(), values, x, y, skip);
+  else launch(*s.ctx, k_csr_apply<3>, g, 256, 0, s.view(), values, x, y, skip);
 }
 
 void csr_diagonal(System& s, const double* values, double* d) {

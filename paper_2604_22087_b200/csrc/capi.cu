@@ -46,13 +46,13 @@ void ExplicitOp::validate() const {  // backend.hpp:176-181
   if (buf->state != 1) throw LeaseError("explicit operator used while the buffer lease is not held");
   if (buf->epoch != epoch) throw StaleEpochError("explicit operator built from a stale assembly epoch");
 }
-void ExplicitOp::apply(const double* x, double* y) { csr_apply(*sys, buf->store.p, x, y); }
+void ExplicitOp::apply(const double* x, double* y) { csr_apply(*sys, buf->store.p, x, y, skip); }
 void ExplicitOp::diagonal(double* d) { csr_diagonal(*sys, buf->store.p, d); }
 
 MfOp::~MfOp() { destroy_stencil_plan(stencil); }
 void MfOp::apply(const double* x, double* y) {
   if (stencil) stencil_apply(*stencil, *this, x, y, nullptr, skip);
-  else if (qpt.p) grid_mf_apply_cached(*sys, qpt.p, mask.p, x, y);
+  else if (qpt.p) grid_mf_apply_cached(*sys, qpt.p, mask.p, x, y, skip);
   else mf_apply_general(*sys, state.p, mask.p, x, y);
 }
 bool MfOp::apply_dot(const double* x, double* y, double* dot_out) {

@@ -149,7 +149,9 @@ __global__ void __launch_bounds__(128) k_grid_elem(const __grid_constant__ GeoT<
 // constrained dofs (backend.hpp:146-147).
 template <int D>
 __global__ void __launch_bounds__(256) k_gather(SysView s, const double* __restrict__ ev, const uint8_t* __restrict__ mask,
-                                                const double* __restrict__ x, double* __restrict__ y) {
+                                                const double* __restrict__ x, double* __restrict__ y,
+                                                const int* skip) {
+  if (skip && *skip) return;
   constexpr int npe = EL<D>::npe, nd = EL<D>::nd;
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < s.n_nodes; n += (int64_t)gridDim.x * blockDim.x) {
     double acc[D];
@@ -220,7 +222,9 @@ template <int D>
 __global__ void __launch_bounds__(128) k_grid_jvp_cached(const __grid_constant__ GeoT<D> G, SysView s, int nx, int ny,
                                                          const double* __restrict__ qpt,
                                                          const uint8_t* __restrict__ mask,
-                                                         const double* __restrict__ x, double* __restrict__ ev) {
+                                                         const double* __restrict__ x, double* __restrict__ ev,
+                                                         const int* skip) {
+  if (skip && *skip) return;
   constexpr int npe = EL<D>::npe, nq = EL<D>::nq, nd = EL<D>::nd;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s.n_elem; e += (int64_t)gridDim.x * blockDim.x) {
     const DMat m = s.mats[s.phase[e]];
@@ -304,7 +308,7 @@ void run(System& s, const double* u, const uint8_t* mask, const double* x, doubl
   launch(*s.ctx, k_grid_elem<D, MODE>, grid_for(s.n_elem, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, u, mask, x,
          s.ev.p);
   launch(*s.ctx, k_gather<D>, grid_for(s.n_nodes, 256, 148 * 32), 256, 0, s.view(), s.ev.p,
-         MODE == EV_JVP ? mask : nullptr, x, y);
+         MODE == EV_JVP ? mask : nullptr, x, y, nullptr);
 }
 
 template <int D>
@@ -316,13 +320,13 @@ void cached_tangent(System& s, const double* u, DevArray<double>& qpt) {
 }
 
 template <int D>
-void cached_apply(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y) {
+void cached_apply(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y, const int* skip) {
   GeoT<D> G;
   geo<D>(s, G);
   if (!s.ev.p) s.ev.alloc((size_t)s.n_elem * EL<D>::nd);
   launch(*s.ctx, k_grid_jvp_cached<D>, grid_for(s.n_elem, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, qpt, mask,
-         x, s.ev.p);
-  launch(*s.ctx, k_gather<D>, grid_for(s.n_nodes, 256, 148 * 32), 256, 0, s.view(), s.ev.p, mask, x, y);
+         x, s.ev.p, skip);
+  launch(*s.ctx, k_gather<D>, grid_for(s.n_nodes, 256, 148 * 32), 256, 0, s.view(), s.ev.p, mask, x, y, skip);
 }
 
 }  // namespace
@@ -341,9 +345,10 @@ void grid_tangent_cache(System& s, const double* u, DevArray<double>& qpt) {
   else cached_tangent<3>(s, u, qpt);
 }
 
-void grid_mf_apply_cached(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y) {
-  if (s.dim == 2) cached_apply<2>(s, qpt, mask, x, y);
-  else cached_apply<3>(s, qpt, mask, x, y);
+void grid_mf_apply_cached(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y,
+                          const int* skip) {
+  if (s.dim == 2) cached_apply<2>(s, qpt, mask, x, y, skip);
+  else cached_apply<3>(s, qpt, mask, x, y, skip);
 }
 
 void grid_geometry(System& s) {

@@ -340,7 +340,9 @@ bool cg_persistent(Operator& op, double* x, double* r, double* p, double* ap, co
   const double* vals = op.csr_values();
   System& s = *op.sys;
   Ctx& c = *s.ctx;
-  if (off || !vals || op.n > (int64_t)1 << 21) return false;
+  // grid-wide syncs beat kernel launches only while an iteration is short: measured crossover between
+  // 3.8 M nonzeros (22 vs 30 us per iteration) and 8.7 M (41 vs 38 us); 348 vs 146 us at 67 M
+  if (off || !vals || s.nnz > 6000000) return false;
   int coop = 0;
   AFEM_CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c.device));
   if (!coop) return false;
