@@ -479,10 +479,11 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
           // the iteration loop as a CUDA graph of kGraphIters iterations (captured once per solve):
           // one launch per chunk instead of four per iteration, so host hiccups cannot drain the GPU
           constexpr int kGraphIters = 16;
-          static thread_local CgDev* hst = nullptr;
-          static thread_local cudaEvent_t ev = nullptr;
-          if (!hst) AFEM_CK(cudaMallocHost(reinterpret_cast<void**>(&hst), sizeof(CgDev)));
-          if (!ev) AFEM_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          static thread_local CgDev* hst = nullptr;  // two status snapshots (chunks k and k + 1)
+          static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+          if (!hst) AFEM_CK(cudaMallocHost(reinterpret_cast<void**>(&hst), 2 * sizeof(CgDev)));
+          for (cudaEvent_t& e : ev)
+            if (!e) AFEM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
           cudaGraph_t graph = nullptr;
           cudaGraphExec_t exec = nullptr;
           const int64_t l0 = c.launches;
@@ -504,14 +505,20 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
             AFEM_CK(cudaGraphLaunch(exec, c.stream));
             c.launches += per_graph;
           };
-          run();
-          while (true) {
-            AFEM_CK(cudaMemcpyAsync(hst, st.p, sizeof(CgDev), cudaMemcpyDeviceToHost, c.stream));
-            AFEM_CK(cudaEventRecord(ev, c.stream));
-            run();  // speculative: no-ops once done
-            AFEM_CK(cudaEventSynchronize(ev));
-            hs = *hst;
+          // two chunks queued ahead of the host's check: a host stall shorter than two chunks
+          // (about 5 ms at 128^3) never drains the GPU; chunks past convergence are no-ops
+          auto run_snap = [&](int slot) {
+            run();
+            AFEM_CK(cudaMemcpyAsync(hst + slot, st.p, sizeof(CgDev), cudaMemcpyDeviceToHost, c.stream));
+            AFEM_CK(cudaEventRecord(ev[slot], c.stream));
+          };
+          run_snap(0);
+          run_snap(1);
+          for (int k = 0;; ++k) {
+            AFEM_CK(cudaEventSynchronize(ev[k & 1]));
+            hs = hst[k & 1];
             if (hs.done) break;
+            run_snap(k & 1);
           }
           AFEM_CK(cudaStreamSynchronize(c.stream));
           hs = fetch(c, st.p);
