@@ -46,6 +46,95 @@ __global__ void k_grid_geometry(const double* coords, const int32_t* conn, doubl
 
 enum : int { EV_RESIDUAL = 0, EV_JVP = 1, EV_DIAG = 2 };
 
+__device__ __forceinline__ int grid_find_pos(const int32_t* adj, int deg, int64_t m) {
+  int lo = 0, hi = deg;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (adj[mid] < m) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <int D>
+__device__ __forceinline__ void elem_nodes(int64_t e, int nx, int ny, int64_t (&nd)[EL<D>::npe]);
+
+// K(u) rows of node n into pattern-ordered CSR values: assembly.cu's k_jacobian (assembly.hpp:144-173)
+// with the uniform-brick gradients instead of a per-(node, element, qp) Jacobian inverse and
+// implicit connectivity. Same per-entry summation order (elements in (batch, element) order, Gauss
+// points in order), so the result is deterministic.
+template <int D>
+__global__ void __launch_bounds__(128) k_grid_jacobian(const __grid_constant__ GeoT<D> G, SysView s, int nx, int ny,
+                                                       const double* __restrict__ u, double* __restrict__ values) {
+  constexpr int npe = EL<D>::npe, nq = EL<D>::nq, nd = EL<D>::nd;
+  int err = 0;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < s.n_nodes; n += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a0 = s.adj_ptr[n];
+    const int deg = static_cast<int>(s.adj_ptr[n + 1] - a0);
+    const int64_t base = (int64_t)D * D * a0;
+    for (int j = 0; j < D * D * deg; ++j) values[base + j] = 0.0;
+    for (int64_t p = s.inc_ptr[n]; p < s.inc_ptr[n + 1]; ++p) {
+      const uint32_t v = s.inc[p];
+      const int64_t e = v / npe;
+      const int ln = v % npe;
+      int64_t nodes[npe];
+      elem_nodes<D>(e, nx, ny, nodes);
+      double ue[nd];
+#pragma unroll
+      for (int k = 0; k < npe; ++k)
+#pragma unroll
+        for (int c = 0; c < D; ++c) ue[k * D + c] = __ldg(&u[nodes[k] * D + c]);
+      const DMat m = s.mats[s.phase[e]];
+      int pos[npe];
+#pragma unroll
+      for (int k = 0; k < npe; ++k) pos[k] = grid_find_pos(s.adj + a0, deg, nodes[k]);
+      double K[D][nd];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int j = 0; j < nd; ++j) K[a][j] = 0.0;
+      for (int q = 0; q < nq; ++q) {
+        double H[D][D];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b < D; ++b) {
+            double h = 0.0;
+#pragma unroll
+            for (int k = 0; k < npe; ++k) h += ue[k * D + a] * G.g[q][k][b];
+            H[a][b] = h;
+          }
+        TangentQP<D> t;
+        tangent_qp<D>(m, H, t, err, s.hist ? s.hist + (e * nq + q) * kHist : nullptr);
+        double gn[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) gn[c] = G.g[q][ln][c];
+        const double wdet = G.wdet[q];
+#pragma unroll
+        for (int lm = 0; lm < npe; ++lm) {
+          double gm[D], blk[D][D];
+#pragma unroll
+          for (int c = 0; c < D; ++c) gm[c] = G.g[q][lm][c];
+          tangent_block<D>(t, gn, gm, blk);
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = 0; b < D; ++b) K[a][lm * D + b] += wdet * blk[a][b];
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const int64_t row = base + (int64_t)a * D * deg;
+#pragma unroll
+        for (int lm = 0; lm < npe; ++lm)
+#pragma unroll
+          for (int b = 0; b < D; ++b) values[row + pos[lm] * D + b] += K[a][lm * D + b];
+      }
+    }
+  }
+  if (err) atomicOr(s.err, err);
+}
+
+
 template <int D>
 __device__ __forceinline__ void elem_nodes(int64_t e, int nx, int ny, int64_t (&nd)[EL<D>::npe]) {
   const int ex = static_cast<int>(e % nx);
@@ -369,6 +458,18 @@ bool grid_elem_path(const System& s) {
 void grid_residual(System& s, const double* u, double* r) {
   if (s.dim == 2) run<2, EV_RESIDUAL>(s, u, nullptr, nullptr, r);
   else run<3, EV_RESIDUAL>(s, u, nullptr, nullptr, r);
+}
+
+void grid_jacobian(System& s, const double* u, double* values) {
+  if (s.dim == 2) {
+    GeoT<2> G;
+    geo<2>(s, G);
+    launch(*s.ctx, k_grid_jacobian<2>, grid_for(s.n_nodes, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, u, values);
+  } else {
+    GeoT<3> G;
+    geo<3>(s, G);
+    launch(*s.ctx, k_grid_jacobian<3>, grid_for(s.n_nodes, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, u, values);
+  }
 }
 
 void grid_diagonal(System& s, const double* u, double* d) {
