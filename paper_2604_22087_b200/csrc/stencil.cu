@@ -401,8 +401,8 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm) k_stencil_main(const __g
 // straddle a batch; the head sums them with fixed-order shuffles and updates y directly.
 // Deterministic (fixed batch -> CTA mapping, fixed shuffle order), no atomics, no barriers.
 // rec: node (low 32 bits, -1 = padding) | oct << 32 | seg << 35 | edge << 39 | pho << 40 |
-// phb << 45 | rem << 50 (items left in the segment, this one included); zm: bit 3m+b = input b of
-// element corner m is zero (Dirichlet or outside).
+// phb << 45 | rem << 50 (items left in the segment, this one included); zm: bit 3b+c = input c of
+// the element's bit corner b ^ rm (the item's reflected frame) is zero (Dirichlet or outside).
 constexpr int kItemThreads = 256;
 constexpr uint64_t kPadRec = 0xffffffffull;
 
@@ -460,20 +460,16 @@ __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, 
       }
     }
     if (node >= 0) {
-      const int i = node % NX, rr = node / NX;
-      const int j = rr % NY, k = rr / NY;
-      const int o = w & 7;
-      const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
-      const int rm = (1 - ox) | ((1 - oy) << 1) | ((1 - oz) << 2);  // the node's bit corner in the element
-      const int e0 = (i - 1 + ox) + NX * (j - 1 + oy) + NXY * (k - 1 + oz);  // may lie outside (masked)
+      const int rm = (w & 7) ^ 7;  // the node's bit corner in the element (octant o = its mirror)
+      // frame corner b lies at +-bit_c(b) along axis c from the node (minus where rm has bit c)
+      const int SX = (rm & 1) ? -1 : 1, SY = (rm & 2) ? -NX : NX, SZ = (rm & 4) ? -NXY : NXY;
       // reflected frame: the node sits at bit corner 0; frame corner b is element corner b ^ rm, and
       // component c of x and row c of y flip sign with bit c of rm
       const double s0 = (rm & 1) ? -1.0 : 1.0, s1 = (rm & 2) ? -1.0 : 1.0, s2 = (rm & 4) ? -1.0 : 1.0;
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
-        const int pb = b ^ rm;
-        const int nd = e0 + (pb & 1) + NX * ((pb >> 1) & 1) + NXY * (pb >> 2);
-        const uint32_t zb = (zm >> (3 * local_node(pb & 1, (pb >> 1) & 1, pb >> 2))) & 7;
+        const int nd = node + ((b & 1) ? SX : 0) + ((b & 2) ? SY : 0) + ((b & 4) ? SZ : 0);
+        const uint32_t zb = (zm >> (3 * b)) & 7;
         const int a0 = zb == 7 ? 0 : 3 * nd;  // all-zero corners (outside) read a safe address
         const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);  // 16 B-aligned pair
         const double2 pr = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
@@ -822,12 +818,16 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
         const uint64_t rec = static_cast<uint64_t>(static_cast<uint32_t>(nm.node)) |
                              (static_cast<uint64_t>(o) << 32) | ((nm.edge ? 1ull : 0ull) << 39) | (pho << 40) |
                              (phb << 45);
-        uint32_t zm = 0;  // zero inputs: Dirichlet, or outside the domain
+        // zero inputs (Dirichlet, or outside the domain) in the item kernel's reflected frame: bits
+        // 3b..3b+2 belong to frame corner b = element bit corner b ^ rm, rm = the node's bit corner
+        uint32_t zm = 0;
         const int ei = ni - 1 + (o & 1), ej = nj - 1 + ((o >> 1) & 1), ek = nk - 1 + (o >> 2);
-        for (int m = 0; m < 8; ++m) {
-          const int ii = ei + corner_x(m), jj = ej + corner_y(m), kk = ek + (m >> 2);
+        const int rm = o ^ 7;
+        for (int b = 0; b < 8; ++b) {
+          const int pb = b ^ rm;
+          const int ii = ei + (pb & 1), jj = ej + ((pb >> 1) & 1), kk = ek + (pb >> 2);
           const bool in = ii >= 0 && ii < P.NX && jj >= 0 && jj < P.NY && kk >= 0 && kk < P.NZ;
-          zm |= (in ? (hinfo[ii + (int64_t)P.NX * (jj + (int64_t)P.NY * kk)] & 7u) : 7u) << (3 * m);
+          zm |= (in ? (hinfo[ii + (int64_t)P.NX * (jj + (int64_t)P.NY * kk)] & 7u) : 7u) << (3 * b);
         }
         ti.push_back({static_cast<uint32_t>(nk / plan->zpiece),
                       (lid << 36) | ((uint64_t)(nj % TY) * TXN + ni % TXN) << 3 | static_cast<uint64_t>(o), rec, zm});
