@@ -208,3 +208,20 @@ def test_stencil_full_bench_size_properties(afem, ctx):
     assert rel_err(ax, opg.apply(x)) <= TOL
     assert rel_err(ops.apply(2.5 * x - 0.75 * z), 2.5 * ax - 0.75 * az) <= TOL
     assert abs(np.dot(x, az) - np.dot(z, ax)) <= 1e-12 * np.linalg.norm(x) * np.linalg.norm(az)
+
+
+def test_stencil_cg_full_bench_size(afem, ctx):
+    """Jacobi-PCG at the bench size (6.44 M dofs, rtol 1e-8, the CUDA-graph loop with speculative
+    chunks): converged, one history entry per iteration plus the initial residual, and the
+    true residual of the returned x (a fresh apply) meets the tolerance — the reference's
+    re-verification contract (krylov.hpp:331-342, 383-394)."""
+    n = 128
+    s = grid(afem, ctx, n, n_fibres=40, radius=0.05)
+    s.set_dirichlet(*Oracle("restate").bcs(3, n, n, n, 1.0, 0.01))
+    u0 = s.impose_dirichlet(np.zeros(s.n))
+    op = afem.matrix_free_operator(s, u0)
+    b = -s.constrain_residual(s.residual(u0), u0)
+    x, rep = afem.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
+    assert rep["converged"] and 3000 < rep["iterations"] < 4500
+    assert len(rep["residual_history"]) == rep["iterations"] + 1
+    assert np.linalg.norm(b - op.apply(x)) <= 1.0001e-8 * np.linalg.norm(b)
