@@ -76,6 +76,7 @@ struct System {
   // scratch of the element-centric kernels (elemgrid.cu), allocated on first use
   std::vector<double> grid_geo;
   DevArray<double> ev;
+  DevArray<double> kscr;  // element tangent blocks of one z slab (elemgrid.cu grid_jacobian)
   std::shared_ptr<IluLevels> ilu_levels;  // built on the first ILU(0) setup
   // structured grid metadata (afem_system_create_grid)
   bool grid = false;

@@ -12,6 +12,7 @@
 // The reduction order is the node-centric kernels' (and the reference's), so results stay
 // deterministic run to run with no atomics. Algorithmic traffic per element: u_e/x_e gathers
 // (L2-resident neighbours), J2 history (nq*64 B), 2*nd*8 B of scratch.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -57,6 +58,137 @@ __device__ __forceinline__ int grid_find_pos(const int32_t* adj, int deg, int64_
 
 template <int D>
 __device__ __forceinline__ void elem_nodes(int64_t e, int nx, int ny, int64_t (&nd)[EL<D>::npe]);
+
+// Element-centric tangent (3D grids), two passes per z slab of node planes:
+//   k_grid_kelem    warp per element: lanes 0-7 evaluate the 8 Gauss-point tangents once (shared
+//                   memory), lane (corner ln, corner pair g) accumulates the blocks (ln, 2g), (ln, 2g+1)
+//                   over the Gauss points in order -> scratch [e][ln][a][24]
+//   k_grid_kgather  warp per node: the node's 9 deg row entries accumulated in shared memory over its
+//                   incident elements in (batch, element) order, then written once, coalesced
+// Per entry the sums run in the node-centric kernel's order (Gauss points within an element, then
+// elements in incidence order), so the values are the same; each Gauss point's constitutive
+// tangent is evaluated once instead of once per incident node, and every CSR value is written once.
+constexpr int kKelemWarps = 4;
+constexpr int kKe = 8 * 3 * 24;  // doubles of one element's scratch block
+
+__global__ void __launch_bounds__(32 * kKelemWarps) k_grid_kelem(const __grid_constant__ GeoT<3> G, SysView s, int nx,
+                                                                 int ny, const double* __restrict__ u, int64_t e0,
+                                                                 int64_t e1, double* __restrict__ scr) {
+  __shared__ TangentQP<3> ts[kKelemWarps][8];
+  __shared__ double us[kKelemWarps][24];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int err = 0;
+  for (int64_t e = e0 + blockIdx.x * (int64_t)kKelemWarps + w; e < e1; e += (int64_t)gridDim.x * kKelemWarps) {
+    const DMat m = s.mats[s.phase[e]];
+    int64_t nodes[8];
+    elem_nodes<3>(e, nx, ny, nodes);
+    if (lane < 24) us[w][lane] = __ldg(&u[nodes[lane / 3] * 3 + lane % 3]);
+    __syncwarp();
+    if (lane < 8) {
+      const int q = lane;
+      double H[3][3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          double h = 0.0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) h += us[w][k * 3 + a] * G.g[q][k][b];
+          H[a][b] = h;
+        }
+      TangentQP<3> t;
+      tangent_qp<3>(m, H, t, err, s.hist ? s.hist + (e * 8 + q) * kHist : nullptr);
+      ts[w][q] = t;
+    }
+    __syncwarp();
+    {  // lane = (corner ln, corner pair g): blocks (ln, lm) for lm = 2g, 2g + 1, all three rows
+      const int ln = lane >> 2, g = lane & 3;
+      double K[2][3][3];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) K[h][a][b] = 0.0;
+      for (int q = 0; q < 8; ++q) {
+        const TangentQP<3>& t = ts[w][q];
+        double gn[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gn[c] = G.g[q][ln][c];
+        const double wdet = G.wdet[q];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int lm = 2 * g + h;
+          double gm[3], blk[3][3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) gm[c] = G.g[q][lm][c];
+          tangent_block<3>(t, gn, gm, blk);
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) K[h][a][b] += wdet * blk[a][b];
+        }
+      }
+      double* o = scr + (e - e0) * kKe + ln * 72 + 6 * g;  // [ln][a][lm * 3 + b]
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) o[a * 24 + h * 3 + b] = K[h][a][b];
+    }
+    __syncwarp();
+  }
+  if (err) atomicOr(s.err, err);
+}
+
+constexpr int kGatherWarps = 4;
+
+// hex8 corner m's position bits (element.hpp:22-23 ring, then z)
+__device__ __forceinline__ int corner_bit_x(int m) { return ((m & 3) == 1 || (m & 3) == 2) ? 1 : 0; }
+__device__ __forceinline__ int corner_bit_y(int m) { return (m & 3) >= 2 ? 1 : 0; }
+
+__global__ void __launch_bounds__(32 * kGatherWarps) k_grid_kgather(SysView s, int nx, int ny, int nz, int64_t n0, int64_t n1,
+                                                                    int64_t e0, const double* __restrict__ scr,
+                                                                    double* __restrict__ values) {
+  __shared__ double row[kGatherWarps][243];
+  __shared__ int pos[kGatherWarps][8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t n = n0 + blockIdx.x * (int64_t)kGatherWarps + w; n < n1; n += (int64_t)gridDim.x * kGatherWarps) {
+    const int64_t a0 = s.adj_ptr[n];
+    // the grid node's neighbours sorted by id = (dz, dy, dx) lexicographic over the offsets that
+    // stay inside the grid: slot of offset (dx, dy, dz) in closed form
+    const int NXn = nx + 1, NYn = ny + 1;
+    const int i = static_cast<int>(n % NXn);
+    const int64_t rr = n / NXn;
+    const int j = static_cast<int>(rr % NYn), kz = static_cast<int>(rr / NYn);
+    const int xlo = i > 0, ylo = j > 0, zlo = kz > 0;
+    const int cx = 1 + xlo + (i < nx), cy = 1 + ylo + (j < ny), cz = 1 + zlo + (kz < nz);
+    const int deg = cx * cy * cz;
+    const int len = 9 * deg;
+    for (int jj = lane; jj < len; jj += 32) row[w][jj] = 0.0;
+    for (int64_t p = s.inc_ptr[n]; p < s.inc_ptr[n + 1]; ++p) {
+      const uint32_t v = s.inc[p];
+      const int64_t e = v / 8;
+      const int ln = v % 8;
+      if (lane < 8) {  // corner lane relative to the node's corner ln
+        const int dx = corner_bit_x(lane) - corner_bit_x(ln), dy = corner_bit_y(lane) - corner_bit_y(ln);
+        const int dz = (lane >> 2) - (ln >> 2);
+        pos[w][lane] = ((dz + zlo) * cy + (dy + ylo)) * cx + (dx + xlo);
+      }
+      __syncwarp();
+      const double* src = scr + (e - e0) * kKe + ln * 72;
+      for (int k = lane; k < 72; k += 32) {  // k = a * 24 + lm * 3 + b: distinct targets
+        const int a = k / 24, r = k % 24;
+        row[w][a * 3 * deg + pos[w][r / 3] * 3 + r % 3] += __ldg(&src[k]);
+      }
+      __syncwarp();
+    }
+    double* out = values + 9 * a0;
+    for (int jj = lane; jj < len; jj += 32) out[jj] = row[w][jj];
+    __syncwarp();
+  }
+}
 
 // K(u) rows of node n into pattern-ordered CSR values: assembly.cu's k_jacobian (assembly.hpp:144-173)
 // with the uniform-brick gradients instead of a per-(node, element, qp) Jacobian inverse and
@@ -468,7 +600,29 @@ void grid_jacobian(System& s, const double* u, double* values) {
   } else {
     GeoT<3> G;
     geo<3>(s, G);
-    launch(*s.ctx, k_grid_jacobian<3>, grid_for(s.n_nodes, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, u, values);
+    static const bool node_centric = std::getenv("AFEM_NODE_JACOBIAN") != nullptr;
+    if (node_centric) {
+      launch(*s.ctx, k_grid_jacobian<3>, grid_for(s.n_nodes, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, u,
+             values);
+      return;
+    }
+    // z slabs of node planes; slab [k0, k1) needs element planes [k0 - 1, k1) (clamped)
+    const int64_t epp = (int64_t)s.nx * s.ny, npp = (int64_t)(s.nx + 1) * (s.ny + 1);
+    const int nzn = s.nz + 1;
+    const int64_t budget = (int64_t)1 << 31;  // scratch bytes
+    const int S = static_cast<int>(std::max<int64_t>(1, budget / (epp * kKe * 8) - 1));
+    if (!s.kscr.p || s.kscr.n < (size_t)std::min<int64_t>(S + 1, s.nz) * epp * kKe)
+      s.kscr.alloc((size_t)std::min<int64_t>(S + 1, s.nz) * epp * kKe);
+    for (int k0 = 0; k0 < nzn; k0 += S) {
+      const int k1 = std::min(nzn, k0 + S);
+      const int ea = std::max(0, k0 - 1), eb = std::min(s.nz, k1);
+      const int64_t e0 = ea * epp, e1 = eb * epp;
+      launch(*s.ctx, k_grid_kelem, grid_for((e1 - e0) * 32, 32 * kKelemWarps, 148 * 16), 32 * kKelemWarps, 0, G,
+             s.view(), s.nx, s.ny, u, e0, e1, s.kscr.p);
+      const int64_t n0 = k0 * npp, n1 = k1 * npp;
+      launch(*s.ctx, k_grid_kgather, grid_for((n1 - n0) * 32, 32 * kGatherWarps, 148 * 16), 32 * kGatherWarps, 0,
+             s.view(), s.nx, s.ny, s.nz, n0, n1, e0, s.kscr.p, values);
+    }
   }
 }
 
