@@ -610,7 +610,8 @@ void grid_jacobian(System& s, const double* u, double* values) {
     const int64_t epp = (int64_t)s.nx * s.ny, npp = (int64_t)(s.nx + 1) * (s.ny + 1);
     const int nzn = s.nz + 1;
     const int64_t budget = (int64_t)1 << 31;  // scratch bytes
-    const int S = static_cast<int>(std::max<int64_t>(1, budget / (epp * kKe * 8) - 1));
+    int S = static_cast<int>(std::max<int64_t>(1, budget / (epp * kKe * 8) - 1));
+    if (const char* e = std::getenv("AFEM_JAC_SLAB")) S = std::max(1, std::atoi(e));  // tests: force slabs
     if (!s.kscr.p || s.kscr.n < (size_t)std::min<int64_t>(S + 1, s.nz) * epp * kKe)
       s.kscr.alloc((size_t)std::min<int64_t>(S + 1, s.nz) * epp * kKe);
     for (int k0 = 0; k0 < nzn; k0 += S) {
