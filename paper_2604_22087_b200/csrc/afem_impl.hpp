@@ -187,6 +187,7 @@ bool grid_elem_path(const System& s);
 void grid_residual(System& s, const double* u, double* r);
 void grid_diagonal(System& s, const double* u, double* d);
 void grid_jacobian(System& s, const double* u, double* values);
+void grid_history_commit(System& s, const double* u);  // 3D grids
 void grid_mf_apply(System& s, const double* state, const uint8_t* mask, const double* x, double* y);
 bool grid_tangent_cacheable(const System& s);
 void grid_tangent_cache(System& s, const double* u, DevArray<double>& qpt);

@@ -410,6 +410,10 @@ void mf_apply_general(System& s, const double* state, const uint8_t* mask, const
 
 void history_commit(System& s, const double* u) {
   if (!s.has_history()) return;
+  if (s.dim == 3 && grid_elem_path(s)) {
+    grid_history_commit(s, u);
+    return;
+  }
   const unsigned g = grid_for(s.n_elem, 128, 148 * 64);
   if (s.dim == 2) launch(*s.ctx, k_history_commit<2>, g, 128, 0, s.view(), u, s.hist.p);
   else launch(*s.ctx, k_history_commit<3>, g, 128, 0, s.view(), u, s.hist.p);

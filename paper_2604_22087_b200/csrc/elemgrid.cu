@@ -59,6 +59,37 @@ __device__ __forceinline__ int grid_find_pos(const int32_t* adj, int deg, int64_
 template <int D>
 __device__ __forceinline__ void elem_nodes(int64_t e, int nx, int ny, int64_t (&nd)[EL<D>::npe]);
 
+// J2 history commit on grids: thread per (element, Gauss point) — consecutive threads own
+// consecutive 64-byte history slots (coalesced read-modify-write), uniform-brick gradients.
+template <int D>
+__global__ void __launch_bounds__(128) k_grid_history_commit(const __grid_constant__ GeoT<D> G, SysView s, int nx,
+                                                             int ny, const double* __restrict__ u, double* hist) {
+  constexpr int npe = EL<D>::npe, nq = EL<D>::nq;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < s.n_elem * nq; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / nq;
+    const int q = static_cast<int>(t % nq);
+    const DMat m = s.mats[s.phase[e]];
+    if (m.model != MODEL_J2) continue;
+    int64_t nodes[npe];
+    elem_nodes<D>(e, nx, ny, nodes);
+    double H[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) H[a][b] = 0.0;
+#pragma unroll
+    for (int k = 0; k < npe; ++k)
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double ua = __ldg(&u[nodes[k] * D + a]);
+#pragma unroll
+        for (int b = 0; b < D; ++b) H[a][b] += ua * G.g[q][k][b];
+      }
+    double* hq = hist + t * kHist;
+    j2_commit<D>(m, H, hq, hq);
+  }
+}
+
 // Element-centric tangent (3D grids), two passes per z slab of node planes:
 //   k_grid_kelem    warp per element: lanes 0-7 evaluate the 8 Gauss-point tangents once (shared
 //                   memory), lane (corner ln, corner pair g) accumulates the blocks (ln, 2g), (ln, 2g+1)
@@ -590,6 +621,13 @@ bool grid_elem_path(const System& s) {
 void grid_residual(System& s, const double* u, double* r) {
   if (s.dim == 2) run<2, EV_RESIDUAL>(s, u, nullptr, nullptr, r);
   else run<3, EV_RESIDUAL>(s, u, nullptr, nullptr, r);
+}
+
+void grid_history_commit(System& s, const double* u) {
+  GeoT<3> G;
+  geo<3>(s, G);
+  launch(*s.ctx, k_grid_history_commit<3>, grid_for(s.n_elem * 8, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, u,
+         s.hist.p);
 }
 
 void grid_jacobian(System& s, const double* u, double* values) {
