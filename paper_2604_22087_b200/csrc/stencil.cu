@@ -77,6 +77,7 @@ struct StencilPlan {
   int64_t n_fix_nodes = 0, n_edge_nodes = 0;
   int kchunk = 16;
   int nchunks = 1;
+  int main_blocks = 1;  // balanced main-kernel grid
   // z pieces for the pipelined host-buffer apply (afem_op_apply with host x / y): items are
   // ordered piece-major, piece_items[p] = first item of piece p (multiple of 32)
   int zpiece = 16;
@@ -232,7 +233,8 @@ template <bool DOT>
 __global__ void __launch_bounds__(NT, kMainBlocksPerSm) k_stencil_main(const __grid_constant__ StencilParams P,
                                                         const double* __restrict__ x,
                                                         const uint8_t* __restrict__ info, double* __restrict__ y,
-                                                        int kchunk, int kbeg, int kend, DotArgs dot) {
+                                                        int kchunk, int kbeg, int kend, DotArgs dot, int ntx,
+                                                        int nty) {
   if (dot.skip && *dot.skip) return;
   double dsum = 0.0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -241,8 +243,35 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm) k_stencil_main(const __g
       reinterpret_cast<uint32_t (*)[NT][NS]>(smem_raw + sizeof(double) * RING * (TY + 2) * RS);
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int NX = P.NX, NY = P.NY, NZ = P.NZ;
-  const int i0 = blockIdx.x * TXN, j0 = blockIdx.y * TY;
-  const int k0 = kbeg + blockIdx.z * kchunk, k1 = min(k0 + kchunk, kend);
+  // Segments (tile, plane range k0 .. k1-1). Fixed z chunks (kchunk > 0): grid = (x tiles, y tiles,
+  // chunks), one segment per CTA. Balanced (kchunk == 0): one resident wave, each CTA an equal
+  // contiguous range of tile-major (tile, plane) units; a range crossing a tile boundary restarts
+  // the plane pipeline.
+  const int nzr = kend - kbeg;
+  int64_t u = 0, ue = 1;
+  if (kchunk <= 0) {
+    const int64_t U = (int64_t)ntx * nty * nzr;
+    u = U * blockIdx.x / gridDim.x;
+    ue = U * (blockIdx.x + 1) / gridDim.x;
+  }
+  while (u < ue) {
+  int bx, by, k0, k1;
+  if (kchunk > 0) {
+    bx = blockIdx.x;
+    by = blockIdx.y;
+    k0 = kbeg + blockIdx.z * kchunk;
+    k1 = min(k0 + kchunk, kend);
+    u = ue;
+  } else {
+    const int tile = static_cast<int>(u / nzr), kk = static_cast<int>(u % nzr);
+    const int kl = static_cast<int>(min(static_cast<int64_t>(nzr), kk + (ue - u)));
+    bx = tile % ntx;
+    by = tile / ntx;
+    k0 = kbeg + kk;
+    k1 = kbeg + kl;
+    u += kl - kk;
+  }
+  const int i0 = bx * TXN, j0 = by * TY;
   const int i = i0 + 2 * tx, j = j0 + ty;
   const bool active = j < NY;
   const bool v0 = i < P.NXm, v1 = i + 1 < P.NXm;  // the lane's two nodes exist (ragged last tile)
@@ -379,6 +408,9 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm) k_stencil_main(const __g
     }
     __syncthreads();
     sel1 = sel2;
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
   }
   if constexpr (DOT) {
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -875,8 +907,11 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
     }
     AFEM_CK(cudaStreamSynchronize(c.stream));
   }
-  const int64_t nb_main = (int64_t)((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY) * plan->nchunks;
-  plan->part_main.alloc(std::max<int64_t>(nb_main, 1));
+  // balanced main grid: one resident wave, no more CTAs than (tile, plane) units
+  const int64_t units = (int64_t)((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY) * P.NZ;
+  plan->main_blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(slots, units)));
+  if (const char* e = std::getenv("AFEM_MAIN_BLOCKS")) plan->main_blocks = std::max(1, std::atoi(e));
+  plan->part_main.alloc(std::max<int64_t>(plan->main_blocks, 1));
   int iocc = 1;  // one wave of resident item CTAs, each walking one contiguous range
   AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&iocc, k_stencil_items<true>, kItemThreads, 0));
   plan->iocc = std::max(iocc, 1);
@@ -894,12 +929,14 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
 void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, double* dot_out, const int* skip) {
   Ctx& c = *op.sys->ctx;
   const StencilParams& P = pl.p;
-  const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TY - 1) / TY, pl.nchunks);
-  const int nb_main = P.NXm > 0 ? static_cast<int>(grid.x * grid.y * grid.z) : 0;
+  const int ntx = (P.NXm + TXN - 1) / TXN, nty = (P.NY + TY - 1) / TY;
+  const int nb_main = P.NXm > 0 ? pl.main_blocks : 0;
   const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main, skip};
-  if (P.NXm > 0) {
-    if (dot_out) launch(c, k_stencil_main<true>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, 0, P.NZ, dot);
-    else launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, pl.kchunk, 0, P.NZ, dot);
+  if (P.NXm > 0) {  // balanced single wave (kchunk 0)
+    if (dot_out)
+      launch(c, k_stencil_main<true>, nb_main, NT, kMainSmem, P, x, pl.info.p, y, 0, 0, P.NZ, dot, ntx, nty);
+    else
+      launch(c, k_stencil_main<false>, nb_main, NT, kMainSmem, P, x, pl.info.p, y, 0, 0, P.NZ, dot, ntx, nty);
   }
   if (pl.n_items > 0) {
     const Items it{pl.it_rec.p, pl.it_zm.p, pl.n_items};
@@ -928,7 +965,7 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
     const int want = std::max(1, kMainBlocksPerSm * c.num_sms / std::max(tiles, 1));
     const int kc = std::max(4, (ke - kb + want - 1) / want);
     const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TY - 1) / TY, (ke - kb + kc - 1) / kc);
-    launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, kc, kb, ke, dot);
+    launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, kc, kb, ke, dot, 0, 0);
   }
   const int64_t i0 = pl.piece_items[pa], i1 = pl.piece_items[pb];
   if (i1 > i0) {
