@@ -288,6 +288,10 @@ afem_status afem_dist_destroy(afem_dist d);
 afem_status afem_dist_set_benchmark_dirichlet(afem_dist d, afem_system slab, double strain, double lx_global);
 /* matrix_free_operator over the distributed system (local operator + plane halo). */
 afem_status afem_dist_op_create_mf(afem_dist d, afem_system slab, const double* u, afem_op* out);
+/* explicit_operator over the distributed system: the slab's own eliminated CSR values (pattern
+ * order, nnz of the slab system, host or device; copied) — the local SpMV yields partial sums on
+ * the shared node planes, completed by the same plane halo as the matrix-free operator. */
+afem_status afem_dist_op_create_explicit(afem_dist d, afem_system slab, const double* values, afem_op* out);
 /* run_solver, CG (+ Jacobi), every rank calling collectively; reports are identical on all ranks. */
 afem_status afem_dist_solve(afem_dist d, afem_op op, const afem_solver_cfg* cfg, const double* b, const double* x0,
                             double* x, afem_solve_report* rep, double* history, int32_t hist_cap);

@@ -172,6 +172,7 @@ def load():
         "afem_dist_destroy": ([vp], i32),
         "afem_dist_set_benchmark_dirichlet": ([vp, vp, f64, f64], i32),
         "afem_dist_op_create_mf": ([vp, vp, vp, vp], i32),
+        "afem_dist_op_create_explicit": ([vp, vp, vp, vp], i32),
         "afem_dist_solve": ([vp, vp, vp, vp, vp, vp, vp, vp, i32], i32),
         "afem_dist_dot": ([vp, vp, vp, vp, vp], i32),
         "afem_dist_assemble": ([vp, vp, vp], i32),
@@ -666,6 +667,12 @@ class Dist:
     def matrix_free_operator(self, sys: System, u) -> LinearOperator:
         h = C.c_void_p()
         _check(_lib.afem_dist_op_create_mf(self.h, sys.h, _ptr(_f64(u)), C.byref(h)))
+        return LinearOperator(h, sys, keep=self)
+
+    def explicit_operator(self, sys: System, values) -> LinearOperator:
+        """The slab's eliminated assembled values (pattern order): local SpMV + the plane halo."""
+        h = C.c_void_p()
+        _check(_lib.afem_dist_op_create_explicit(self.h, sys.h, _ptr(_f64(values)), C.byref(h)))
         return LinearOperator(h, sys, keep=self)
 
     def run_solver(self, op: LinearOperator, b, method=CG, precond=JACOBI, rtol=1e-13, max_iter=10000, x0=None):

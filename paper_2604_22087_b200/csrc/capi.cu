@@ -1199,6 +1199,19 @@ afem_status afem_dist_op_create_mf(afem_dist d, afem_system slab, const double* 
   });
 }
 
+afem_status afem_dist_op_create_explicit(afem_dist d, afem_system slab, const double* values, afem_op* out) {
+  return guarded([&] {
+    need(d, "dist");
+    need(values, "values");
+    need(out, "out");
+    System& s = SYS(slab);
+    In<double> dv(*s.ctx, values, s.nnz);
+    auto h = std::make_unique<afem_op_s>();
+    h->op = make_dist_csr_op(s, d->comm.get(), dv.d);
+    *out = h.release();
+  });
+}
+
 afem_status afem_dist_solve(afem_dist d, afem_op op, const afem_solver_cfg* cfg, const double* b, const double* x0,
                             double* x, afem_solve_report* rep, double* history, int32_t hist_cap) {
   return guarded([&] {

@@ -254,13 +254,13 @@ void DistMfOp::halo_finish(double* v, const double* x_for_mask, bool diag_mode) 
   const bool reset = diag_mode || x_for_mask;  // neither: plain assembly of partial sums
   if (lo) {
     launch(c, k_add, g, 256, 0, v, recv_lo.p, np);
-    if (reset) launch(c, k_reset_masked, g, 256, 0, v, x_for_mask, local->mask.p, 1.0, diag_mode ? 0 : 1, np);
+    if (reset) launch(c, k_reset_masked, g, 256, 0, v, x_for_mask, mask(), 1.0, diag_mode ? 0 : 1, np);
   }
   if (hi) {
     launch(c, k_add, g, 256, 0, top, recv_hi.p, np);
     if (reset)
       launch(c, k_reset_masked, g, 256, 0, top, x_for_mask ? x_for_mask + (n - np) : nullptr,
-             local->mask.p + (n - np), 1.0, diag_mode ? 0 : 1, np);
+             mask() + (n - np), 1.0, diag_mode ? 0 : 1, np);
   }
 }
 
@@ -269,6 +269,11 @@ void DistMfOp::halo_finish(double* v, const double* x_for_mask, bool diag_mode) 
 // send/recv), the interior pieces run meanwhile on the context stream, which then waits for the
 // exchange and adds the received partial sums. Same arithmetic as apply + halo_add.
 void DistMfOp::apply(const double* x, double* y) {
+  if (!local) {  // assembled: local SpMV (partial sums on the shared planes) + halo
+    csr_apply(*sys, vals.p, x, y);
+    halo_add(y, x, false);
+    return;
+  }
   StencilPlan* pl = local->stencil;
   const int P = pl ? stencil_pieces(*pl) : 0;
   if (comm->size == 1 || P < 3) {
@@ -310,6 +315,28 @@ std::unique_ptr<DistMfOp> make_dist_mf_op(System& s, Comm* comm, std::unique_ptr
   op->local = std::move(local);
   op->diag.alloc(s.n_dof);
   op->local->diagonal(op->diag.p);
+  op->halo_add(op->diag.p, nullptr, true);  // Jacobi diagonal of the global operator, unit on constraints
+  AFEM_CK(cudaStreamSynchronize(s.ctx->stream));
+  return op;
+}
+
+std::unique_ptr<DistMfOp> make_dist_csr_op(System& s, Comm* comm, const double* d_values) {
+  if (!s.grid || s.dim != 3) throw std::invalid_argument("dist operator: 3D grid (slab) system required");
+  auto op = std::make_unique<DistMfOp>();
+  op->sys = &s;
+  op->kind = 0;
+  op->n = s.n_dof;
+  op->comm = comm;
+  op->plane = static_cast<int64_t>(s.nx + 1) * (s.ny + 1) * 3;
+  op->owned_offset = comm->rank > 0 ? op->plane : 0;
+  op->send_lo.alloc(op->plane);
+  op->recv_lo.alloc(op->plane);
+  op->send_hi.alloc(op->plane);
+  op->recv_hi.alloc(op->plane);
+  op->vals.alloc(s.nnz);
+  copy(*s.ctx, d_values, op->vals.p, s.nnz);
+  op->diag.alloc(s.n_dof);
+  csr_diagonal(s, op->vals.p, op->diag.p);
   op->halo_add(op->diag.p, nullptr, true);  // Jacobi diagonal of the global operator, unit on constraints
   AFEM_CK(cudaStreamSynchronize(s.ctx->stream));
   return op;

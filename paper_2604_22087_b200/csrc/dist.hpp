@@ -31,9 +31,12 @@ void nccl_unique_id(void* out);
 void slab_range(int nz, int size, int rank, int* z0, int* z1);
 std::vector<Constraint> slab_benchmark_bcs(const System& s, int rank, int size, double strain, double lx_global);
 
-// Matrix-free operator of one slab: local stencil/general apply + plane halo add.
+// Operator of one slab: local apply + plane halo add. Matrix-free (local = the slab's MfOp) or
+// assembled (vals = the slab's eliminated CSR values: the local SpMV gives partial sums on the two
+// shared planes exactly like the matrix-free apply).
 struct DistMfOp : Operator {
   std::unique_ptr<MfOp> local;
+  DevArray<double> vals;  // assembled variant (local == nullptr)
   Comm* comm = nullptr;
   int64_t plane = 0;         // dofs per z node plane
   int64_t owned_offset = 0;  // first owned dof (the bottom plane belongs to rank-1 when rank > 0)
@@ -42,12 +45,14 @@ struct DistMfOp : Operator {
   void apply(const double* x, double* y) override;
   void diagonal(double* d) override;
   bool uses_stencil() const override { return local && local->uses_stencil(); }
+  const uint8_t* mask() const { return local ? local->mask.p : sys->mask.p; }
   void halo_add(double* v, const double* x_for_mask, bool diag_mode);
   // the received neighbour partials added into v's shared planes (+ unit Dirichlet rows)
   void halo_finish(double* v, const double* x_for_mask, bool diag_mode);
 };
 
 std::unique_ptr<DistMfOp> make_dist_mf_op(System& s, Comm* comm, std::unique_ptr<MfOp> local);
+std::unique_ptr<DistMfOp> make_dist_csr_op(System& s, Comm* comm, const double* d_values);
 void dist_solve(DistMfOp& op, const SolverCfg& cfg, const double* b, const double* x0, double* x, SolveReport& rep);
 double dist_dot(DistMfOp& op, const double* a, const double* b);
 
