@@ -292,7 +292,8 @@ afem_status afem_dist_op_create_mf(afem_dist d, afem_system slab, const double* 
  * order, nnz of the slab system, host or device; copied) — the local SpMV yields partial sums on
  * the shared node planes, completed by the same plane halo as the matrix-free operator. */
 afem_status afem_dist_op_create_explicit(afem_dist d, afem_system slab, const double* values, afem_op* out);
-/* run_solver, CG (+ Jacobi), every rank calling collectively; reports are identical on all ranks. */
+/* run_solver, every rank calling collectively: CG (device-scalar loop), GMRES(restart) or BiCGStab
+ * (owned-dof inner products + allreduce), NONE or JACOBI; reports are identical on all ranks. */
 afem_status afem_dist_solve(afem_dist d, afem_op op, const afem_solver_cfg* cfg, const double* b, const double* x0,
                             double* x, afem_solve_report* rep, double* history, int32_t hist_cap);
 /* Sum the shared planes of a slab-partial vector (e.g. a local residual) with the neighbours'

@@ -121,6 +121,12 @@ struct Operator {
   // device flag: while *flag != 0 the apply returns at once (the CG loop's speculative chunk after
   // convergence); false when the operator cannot skip
   virtual bool set_skip(const int*) { return false; }
+  // Inner products of the Krylov methods (GMRES, BiCGStab): the whole vector here; a distributed
+  // operator sums its owned dofs and allreduces (dist.cu).
+  virtual double inner(const double* a, const double* b);
+  virtual void inner_dev(const double* a, const double* b, double* out_dev);
+  // ||b - A x||; keeps r = b - A x when r is given
+  virtual double resid(const double* b, const double* x, double* scratch, double* r);
 };
 
 struct ExplicitOp : Operator {

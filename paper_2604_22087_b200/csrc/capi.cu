@@ -1226,7 +1226,13 @@ afem_status afem_dist_solve(afem_dist d, afem_op op, const afem_solver_cfg* cfg,
     In<double> db(c, b, dop->n), dx0(c, x0, dop->n);
     Out<double> dx(c, x, dop->n, false);
     SolveReport r;
-    dist_solve(*dop, to_cfg(cfg), db.d, dx0.d, dx.d, r);
+    const SolverCfg sc = to_cfg(cfg);
+    if (sc.method == 1 || sc.method == 2) {  // GMRES / BiCGStab through the operator's owned inner products
+      if (sc.precond != 0 && sc.precond != 1) throw CapabilityError("distributed run_solver: NONE or JACOBI");
+      solve(*dop, sc, db.d, dx0.d, dx.d, r);
+    } else {
+      dist_solve(*dop, sc, db.d, dx0.d, dx.d, r);
+    }
     dx.finish();
     fill_report(r, rep, history, hist_cap);
   });

@@ -484,7 +484,7 @@ static double dist_residual_norm(DistMfOp& op, const double* b, const double* x,
 
 void dist_solve(DistMfOp& op, const SolverCfg& cfg, const double* b, const double* x0, double* x, SolveReport& rep) {
   validate_cfg(cfg);
-  if (cfg.method != 0) throw CapabilityError("distributed run_solver: CG only");
+  if (cfg.method != 0) throw CapabilityError("distributed run_solver: CG, GMRES or BiCGStab");
   if (cfg.precond != 0 && cfg.precond != 1) throw CapabilityError("distributed run_solver: NONE or JACOBI");
   const auto t0 = std::chrono::steady_clock::now();
   Ctx& c = *op.sys->ctx;
@@ -572,6 +572,25 @@ double dist_dot(DistMfOp& op, const double* a, const double* b) {
          c.red_counter.p, s.p);
   op.comm->allreduce_sum(s.p, 1, c.stream);
   return fetch_dev(c, s.p);
+}
+
+double DistMfOp::inner(const double* a, const double* b) { return dist_dot(*this, a, b); }
+
+void DistMfOp::inner_dev(const double* a, const double* b, double* out_dev) {
+  Ctx& c = *sys->ctx;
+  launch(c, k_owned_dot, red_grid(n - owned_offset), kRedThreads, 0, a + owned_offset, b + owned_offset,
+         n - owned_offset, c.red_partials.p, c.red_counter.p, out_dev);
+  comm->allreduce_sum(out_dev, 1, c.stream);
+}
+
+double DistMfOp::resid(const double* b, const double* x, double* scratch, double* r) {
+  Ctx& c = *sys->ctx;
+  apply(x, scratch);
+  DevArray<double> s(1);
+  launch(c, k_dres, red_grid(n), kRedThreads, 0, b, scratch, r, n, owned_offset, c.red_partials.p, c.red_counter.p,
+         s.p);
+  comm->allreduce_sum(s.p, 1, c.stream);
+  return std::sqrt(fetch_dev(c, s.p));
 }
 
 }  // namespace afem

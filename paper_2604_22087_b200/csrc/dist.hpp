@@ -46,6 +46,10 @@ struct DistMfOp : Operator {
   void diagonal(double* d) override;
   bool uses_stencil() const override { return local && local->uses_stencil(); }
   const uint8_t* mask() const { return local ? local->mask.p : sys->mask.p; }
+  // owned-dof inner products + allreduce (the GMRES / BiCGStab scalars, identical on every rank)
+  double inner(const double* a, const double* b) override;
+  void inner_dev(const double* a, const double* b, double* out_dev) override;
+  double resid(const double* b, const double* x, double* scratch, double* r) override;
   void halo_add(double* v, const double* x_for_mask, bool diag_mode);
   // the received neighbour partials added into v's shared planes (+ unit Dirichlet rows)
   void halo_finish(double* v, const double* x_for_mask, bool diag_mode);

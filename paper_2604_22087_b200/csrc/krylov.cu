@@ -412,6 +412,16 @@ double residual_norm(Operator& op, const double* b, const double* x, double* scr
   return fetch(c, c.red_out.p);
 }
 
+}  // namespace
+
+double Operator::inner(const double* a, const double* b) { return dot(*sys->ctx, a, b, n); }
+void Operator::inner_dev(const double* a, const double* b, double* out_dev) { dot_dev(*sys->ctx, a, b, n, out_dev); }
+double Operator::resid(const double* b, const double* x, double* scratch, double* r) {
+  return residual_norm(*this, b, x, scratch, r);
+}
+
+namespace {
+
 // JacobiPreconditioner::from_diagonal (krylov.hpp:83-92).
 void jacobi_inverse(Operator& op, DevArray<double>& inv) {
   Ctx& c = *op.sys->ctx;
@@ -619,21 +629,21 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
   DevArray<double> tmp(n), r(n), w(n), scratch(n), V(static_cast<size_t>(restart + 1) * n);
   DevArray<double> hcol(restart + 2);
   auto vec = [&](int k) { return V.p + static_cast<int64_t>(k) * n; };
-  const double bnorm = std::sqrt(dot(c, b, b, n));
+  const double bnorm = std::sqrt(op.inner(b, b));
   const double denom = bnorm > 0.0 ? bnorm : 1.0;
   pc.apply(c, b, tmp.p, n);
-  const double pnorm = std::sqrt(dot(c, tmp.p, tmp.p, n));
+  const double pnorm = std::sqrt(op.inner(tmp.p, tmp.p));
   const double pdenom = pnorm > 0.0 ? pnorm : 1.0;
   std::vector<double> h(static_cast<size_t>(restart + 1) * restart, 0.0), cs(restart), sn(restart), g(restart + 1);
   auto H = [&](int i, int j) -> double& { return h[static_cast<size_t>(i) * restart + j]; };
 
-  double true_rres = residual_norm(op, b, x, tmp.p, r.p) / denom;
+  double true_rres = op.resid(b, x, tmp.p, r.p) / denom;
   pc.apply(c, r.p, w.p, n);
-  rep.history.push_back(std::sqrt(dot(c, w.p, w.p, n)) / pdenom);
+  rep.history.push_back(std::sqrt(op.inner(w.p, w.p)) / pdenom);
 
   while (true_rres > cfg.rtol && rep.iterations < cfg.max_iter && rep.failure.empty()) {
     pc.apply(c, r.p, w.p, n);
-    const double beta = std::sqrt(dot(c, w.p, w.p, n));
+    const double beta = std::sqrt(op.inner(w.p, w.p));
     if (beta == 0.0) break;
     const double target_est = beta * std::min(1.0, 0.5 * cfg.rtol / true_rres);  // krylov.hpp:454
     launch(c, k_scale_into, eg, 256, 0, w.p, beta, vec(0), n);
@@ -644,10 +654,10 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
       op.apply(vec(j), tmp.p);
       pc.apply(c, tmp.p, w.p, n);
       for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, scalars stay on the device
-        dot_dev(c, vec(i), w.p, n, hcol.p + i);
+        op.inner_dev(vec(i), w.p, hcol.p + i);
         add_scaled_dev(c, hcol.p + i, -1.0, vec(i), w.p, n);
       }
-      dot_dev(c, w.p, w.p, n, hcol.p + j + 1);
+      op.inner_dev(w.p, w.p, hcol.p + j + 1);
       std::vector<double> hc(j + 2);
       AFEM_CK(cudaMemcpyAsync(hc.data(), hcol.p, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
       AFEM_CK(cudaStreamSynchronize(c.stream));
@@ -694,9 +704,9 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
     }
     if (!rep.failure.empty()) break;
     for (int k = 0; k < cols; ++k) axpy(c, y[k], vec(k), x, n);
-    true_rres = residual_norm(op, b, x, tmp.p, r.p) / denom;
+    true_rres = op.resid(b, x, tmp.p, r.p) / denom;
   }
-  true_rres = residual_norm(op, b, x, scratch.p, nullptr) / denom;
+  true_rres = op.resid(b, x, scratch.p, nullptr) / denom;
   rep.history.push_back(true_rres);
   rep.converged = rep.failure.empty() && true_rres <= cfg.rtol;
 }
@@ -710,15 +720,15 @@ void bicgstab(Operator& op, const SolverCfg& cfg, const double* b, double* x, co
   DevArray<double> r(n), rhat(n), p(n), v(n), sv(n), t(n), phat(n), shat(n);
   fill(c, 0.0, p.p, n);
   fill(c, 0.0, v.p, n);
-  const double bnorm = std::sqrt(dot(c, b, b, n));
+  const double bnorm = std::sqrt(op.inner(b, b));
   const double denom = bnorm > 0.0 ? bnorm : 1.0;
-  rep.history.push_back(residual_norm(op, b, x, t.p, r.p) / denom);
+  rep.history.push_back(op.resid(b, x, t.p, r.p) / denom);
   copy(c, r.p, rhat.p, n);
   auto precond = [&](const double* in, double* out) { pc.apply(c, in, out, n); };
   while (true) {
     double rho = 1.0, alpha = 1.0, omega = 1.0;
     while (rep.history.back() > cfg.rtol && rep.iterations < cfg.max_iter) {
-      const double rho_new = dot(c, rhat.p, r.p, n);
+      const double rho_new = op.inner(rhat.p, r.p);
       if (rho_new == 0.0) {
         rep.failure = "bicgstab: rho breakdown at iteration " + std::to_string(rep.iterations + 1);
         break;
@@ -728,44 +738,44 @@ void bicgstab(Operator& op, const SolverCfg& cfg, const double* b, double* x, co
       launch(c, k_bicg_p, eg, 256, 0, r.p, p.p, v.p, beta, omega, n);
       precond(p.p, phat.p);
       op.apply(phat.p, v.p);
-      const double rhat_v = dot(c, rhat.p, v.p, n);
+      const double rhat_v = op.inner(rhat.p, v.p);
       if (rhat_v == 0.0) {
         rep.failure = "bicgstab: rhat^T v breakdown at iteration " + std::to_string(rep.iterations + 1);
         break;
       }
       alpha = rho / rhat_v;
       launch(c, k_bicg_s, eg, 256, 0, r.p, v.p, alpha, sv.p, n);
-      if (std::sqrt(dot(c, sv.p, sv.p, n)) / denom <= cfg.rtol) {
+      if (std::sqrt(op.inner(sv.p, sv.p)) / denom <= cfg.rtol) {
         axpy(c, alpha, phat.p, x, n);
         copy(c, sv.p, r.p, n);
         ++rep.iterations;
-        rep.history.push_back(std::sqrt(dot(c, r.p, r.p, n)) / denom);
+        rep.history.push_back(std::sqrt(op.inner(r.p, r.p)) / denom);
         break;
       }
       precond(sv.p, shat.p);
       op.apply(shat.p, t.p);
-      const double tt = dot(c, t.p, t.p, n);
+      const double tt = op.inner(t.p, t.p);
       if (tt == 0.0) {
         rep.failure = "bicgstab: omega breakdown (t = 0) at iteration " + std::to_string(rep.iterations + 1);
         break;
       }
-      omega = dot(c, t.p, sv.p, n) / tt;
+      omega = op.inner(t.p, sv.p) / tt;
       if (omega == 0.0) {
         rep.failure = "bicgstab: omega breakdown at iteration " + std::to_string(rep.iterations + 1);
         break;
       }
       launch(c, k_bicg_xr, eg, 256, 0, x, r.p, phat.p, shat.p, sv.p, t.p, alpha, omega, n);
       ++rep.iterations;
-      rep.history.push_back(std::sqrt(dot(c, r.p, r.p, n)) / denom);
+      rep.history.push_back(std::sqrt(op.inner(r.p, r.p)) / denom);
     }
-    const double true_rres = residual_norm(op, b, x, t.p, nullptr) / denom;
+    const double true_rres = op.resid(b, x, t.p, nullptr) / denom;
     rep.history.back() = true_rres;
     if (true_rres <= cfg.rtol) {
       rep.converged = rep.failure.empty();
       break;
     }
     if (!rep.failure.empty() || rep.iterations >= cfg.max_iter) break;
-    residual_norm(op, b, x, t.p, r.p);  // restart from the fresh residual (krylov.hpp:611-616)
+    op.resid(b, x, t.p, r.p);  // restart from the fresh residual (krylov.hpp:611-616)
     copy(c, r.p, rhat.p, n);
     fill(c, 0.0, p.p, n);
     fill(c, 0.0, v.p, n);
