@@ -299,8 +299,9 @@ afem_status afem_dist_solve(afem_dist d, afem_op op, const afem_solver_cfg* cfg,
 /* Sum the shared planes of a slab-partial vector (e.g. a local residual) with the neighbours'
  * partials, in place (collective). */
 afem_status afem_dist_assemble(afem_dist d, afem_op op, double* v);
-/* solve_bvp (newton.hpp:59-152) over the slab decomposition (collective; MATRIX_FREE operator, CG
- * + Jacobi): residual shared planes summed across neighbours, global free norm over owned dofs. */
+/* solve_bvp (newton.hpp:59-152) over the slab decomposition (collective; MATRIX_FREE tangent, or
+ * EXPLICIT = each slab's assembled + eliminated tangent; CG + Jacobi): residual shared planes summed
+ * across neighbours, global free norm over owned dofs. */
 afem_status afem_dist_solve_bvp(afem_dist d, afem_system slab, const afem_newton_cfg* cfg, const double* x0,
                                 double* u, afem_newton_report* rep, double* norms, int32_t norms_cap);
 /* load_stepping (newton.hpp:163-186) over the slab decomposition with the global benchmark BCs,

@@ -344,15 +344,28 @@ __global__ void k_zero_masked(const uint8_t* mask, const double* v, double* out,
 // distributed: operator_kind must be MATRIX_FREE). Collective: every rank calls it.
 void dist_newton(System& s, Comm* comm, const afem_newton_cfg* cfg, double* u, NewtonReport& rep) {
   validate_newton(cfg);
-  if (cfg->operator_kind != 1)
-    throw CapabilityError("distributed solve_bvp: MATRIX_FREE only (the assembled tangent is not distributed)");
   Ctx& c = *s.ctx;
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t n = s.n_dof;
   const unsigned eg = grid_for(n, 256, 148 * 16);
   impose_dirichlet(s, u);
   DevArray<double> R(n), rhs(n), du(n), Rm(n);
-  std::unique_ptr<DistMfOp> op = make_dist_mf_op(s, comm, make_mf_op(s, u));
+  // tangent operator at u: matrix-free, or (EXPLICIT) each slab's assembled tangent eliminated on
+  // the slab (assemble_jacobian + apply_dirichlet, newton.hpp:93-104) with the plane halo
+  const bool explicit_op = cfg->operator_kind == 0;
+  DevArray<double> vals, scratch;
+  if (explicit_op) {
+    vals.alloc(s.nnz);
+    scratch.alloc(n);
+  }
+  auto tangent = [&]() -> std::unique_ptr<DistMfOp> {
+    if (!explicit_op) return make_dist_mf_op(s, comm, make_mf_op(s, u));
+    jacobian(s, u, vals.p);
+    fill(c, 0.0, scratch.p, n);
+    eliminate(s, vals.p, scratch.p, u);  // u satisfies the constraints: only the matrix changes
+    return make_dist_csr_op(s, comm, vals.p);
+  };
+  std::unique_ptr<DistMfOp> op = tangent();
   auto global_residual = [&]() -> double {
     residual(s, u, R.p);
     op->halo_add(R.p, nullptr, false);  // sum the shared planes' partial sums
@@ -391,7 +404,7 @@ void dist_newton(System& s, Comm* comm, const afem_newton_cfg* cfg, double* u, N
     }
     axpy(c, 1.0, du.p, u, n);
     impose_dirichlet(s, u);
-    op = make_dist_mf_op(s, comm, make_mf_op(s, u));
+    op = tangent();
     rnorm = global_residual();
     ++rep.iterations;
     rep.norms.push_back(rnorm);
