@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(32 * kGatherWarps) k_grid_kgather(SysView s, i
                                                                     int64_t e0, const double* __restrict__ scr,
                                                                     double* __restrict__ values) {
   __shared__ double row[kGatherWarps][243];
-  __shared__ int pos[kGatherWarps][8];
+  __shared__ int pos[kGatherWarps][64];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t n = n0 + blockIdx.x * (int64_t)kGatherWarps + w; n < n1; n += (int64_t)gridDim.x * kGatherWarps) {
     const int64_t a0 = s.adj_ptr[n];
@@ -198,20 +198,41 @@ __global__ void __launch_bounds__(32 * kGatherWarps) k_grid_kgather(SysView s, i
     const int deg = cx * cy * cz;
     const int len = 9 * deg;
     for (int jj = lane; jj < len; jj += 32) row[w][jj] = 0.0;
-    for (int64_t p = s.inc_ptr[n]; p < s.inc_ptr[n + 1]; ++p) {
-      const uint32_t v = s.inc[p];
-      const int64_t e = v / 8;
-      const int ln = v % 8;
-      if (lane < 8) {  // corner lane relative to the node's corner ln
-        const int dx = corner_bit_x(lane) - corner_bit_x(ln), dy = corner_bit_y(lane) - corner_bit_y(ln);
-        const int dz = (lane >> 2) - (ln >> 2);
-        pos[w][lane] = ((dz + zlo) * cy + (dy + ylo)) * cx + (dx + xlo);
+    // all (<= 8) incident elements' 72-value rows are loaded up front (24 independent loads per
+    // lane), then added element by element in incidence order
+    const int64_t p0 = s.inc_ptr[n];
+    const int cnt = static_cast<int>(s.inc_ptr[n + 1] - p0);
+    double vals[8][3];
+#pragma unroll
+    for (int pe = 0; pe < 8; ++pe) {
+      if (pe < cnt) {
+        const uint32_t v = s.inc[p0 + pe];
+        const double* src = scr + (static_cast<int64_t>(v / 8) - e0) * kKe + (v % 8) * 72;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const int k = lane + 32 * r;
+          vals[pe][r] = k < 72 ? __ldg(&src[k]) : 0.0;
+        }
       }
-      __syncwarp();
-      const double* src = scr + (e - e0) * kKe + ln * 72;
-      for (int k = lane; k < 72; k += 32) {  // k = a * 24 + lm * 3 + b: distinct targets
-        const int a = k / 24, r = k % 24;
-        row[w][a * 3 * deg + pos[w][r / 3] * 3 + r % 3] += __ldg(&src[k]);
+    }
+    for (int h = lane; h < 8 * cnt; h += 32) {  // slot of corner (h % 8) of incident element h / 8
+      const int ln = static_cast<int>(s.inc[p0 + h / 8] % 8), cm = h % 8;
+      const int dx = corner_bit_x(cm) - corner_bit_x(ln), dy = corner_bit_y(cm) - corner_bit_y(ln);
+      const int dz = (cm >> 2) - (ln >> 2);
+      pos[w][h] = ((dz + zlo) * cy + (dy + ylo)) * cx + (dx + xlo);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int pe = 0; pe < 8; ++pe) {
+      if (pe < cnt) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {  // k = a * 24 + lm * 3 + b: distinct targets within an element
+          const int k = lane + 32 * r;
+          if (k < 72) {
+            const int a = k / 24, q = k % 24;
+            row[w][a * 3 * deg + pos[w][pe * 8 + q / 3] * 3 + q % 3] += vals[pe][r];
+          }
+        }
       }
       __syncwarp();
     }
