@@ -298,3 +298,19 @@ def test_distributed_newton_assembled_tangent_matches_single_domain(afem, size):
         assert res["rep"]["converged"]
         assert res["rep"]["iterations"] == rg["iterations"]
         assert rel_err(res["u"], ug[plane * z0: plane * (z1 + 1)]) <= 1e-8
+
+
+def test_distributed_capability_errors(afem):
+    """The distributed run_solver keeps the reference's error contract: ILU(0) and the direct
+    methods need the whole assembled matrix (CapabilityError, backend.hpp:151-156 / 245-269), an
+    unknown method is invalid; a non-distributed operator is rejected."""
+    ctx, fib, s, u, x, op, b = _global(afem)
+    d = afem.Dist(ctx, 0, 1, backend="nccl", uid=afem.nccl_unique_id())
+    sys_, _ = afem.slab_system(ctx, NX, NY, NZ, 0, 1, inclusions=fib, radius=0.15, materials=LINEAR)
+    d.set_benchmark_dirichlet(sys_, STRAIN)
+    dop = d.matrix_free_operator(sys_, sys_.impose_dirichlet(np.zeros(sys_.n)))
+    for method, precond in ((afem.CG, afem.ILU0), (afem.GMRES, afem.ILU0), (afem.DIRECT_CHOL, afem.NONE)):
+        with pytest.raises(afem.CapabilityError):
+            d.run_solver(dop, b, method=method, precond=precond, rtol=1e-8, max_iter=10)
+    with pytest.raises(afem.AfemError):
+        d.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=10)
