@@ -78,6 +78,13 @@ struct StencilPlan {
   int kchunk = 16;
   int nchunks = 1;
   int main_blocks = 1;  // balanced main-kernel grid
+  // the plain apply (no fused dot, no skip flag) as an instantiated two-kernel graph, keyed on (x, y)
+  const double* gx = nullptr;
+  double* gy = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  ~StencilPlan() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+  }
   // z pieces for the pipelined host-buffer apply (afem_op_apply with host x / y): items are
   // ordered piece-major, piece_items[p] = first item of piece p (multiple of 32)
   int zpiece = 16;
@@ -926,7 +933,44 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   return plan.release();
 }
 
+static void stencil_apply_launch(StencilPlan& pl, const MfOp& op, const double* x, double* y, double* dot_out,
+                                 const int* skip);
+
 void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, double* dot_out, const int* skip) {
+  Ctx& c = *op.sys->ctx;
+  static const bool no_graph = std::getenv("AFEM_NO_APPLY_GRAPH") != nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (!dot_out && !skip && !no_graph) AFEM_CK(cudaStreamIsCapturing(c.stream, &cs));
+  if (dot_out || skip || no_graph || cs != cudaStreamCaptureStatusNone) {
+    stencil_apply_launch(pl, op, x, y, dot_out, skip);
+    return;
+  }
+  if (!pl.gexec || pl.gx != x || pl.gy != y) {  // (re)capture on a private stream (the context
+    static thread_local cudaStream_t cap = nullptr;  // stream may be the legacy default stream)
+    if (!cap) AFEM_CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    cudaStream_t home = c.stream;
+    const int64_t l0 = c.launches;
+    c.stream = cap;
+    AFEM_CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    stencil_apply_launch(pl, op, x, y, nullptr, nullptr);
+    const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+    c.stream = home;
+    c.launches = l0;
+    AFEM_CK(ce);
+    if (pl.gexec) cudaGraphExecDestroy(pl.gexec);
+    pl.gexec = nullptr;
+    AFEM_CK(cudaGraphInstantiate(&pl.gexec, g, 0));
+    cudaGraphDestroy(g);
+    pl.gx = x;
+    pl.gy = y;
+  }
+  AFEM_CK(cudaGraphLaunch(pl.gexec, c.stream));
+  c.launches += (pl.p.NXm > 0 ? 1 : 0) + (pl.n_items > 0 ? 1 : 0);
+}
+
+static void stencil_apply_launch(StencilPlan& pl, const MfOp& op, const double* x, double* y, double* dot_out,
+                                 const int* skip) {
   Ctx& c = *op.sys->ctx;
   const StencilParams& P = pl.p;
   const int ntx = (P.NXm + TXN - 1) / TXN, nty = (P.NY + TY - 1) / TY;
