@@ -105,34 +105,43 @@ constexpr int kKe = 8 * 3 * 24;  // doubles of one element's scratch block
 __global__ void __launch_bounds__(32 * kKelemWarps) k_grid_kelem(const __grid_constant__ GeoT<3> G, SysView s, int nx,
                                                                  int ny, const double* __restrict__ u, int64_t e0,
                                                                  int64_t e1, double* __restrict__ scr) {
-  __shared__ TangentQP<3> ts[kKelemWarps][8];
-  __shared__ double us[kKelemWarps][24];
+  __shared__ TangentQP<3> ts[kKelemWarps][2][8];
+  __shared__ double us[kKelemWarps][2][24];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int err = 0;
-  for (int64_t e = e0 + blockIdx.x * (int64_t)kKelemWarps + w; e < e1; e += (int64_t)gridDim.x * kKelemWarps) {
-    const DMat m = s.mats[s.phase[e]];
-    int64_t nodes[8];
-    elem_nodes<3>(e, nx, ny, nodes);
-    if (lane < 24) us[w][lane] = __ldg(&u[nodes[lane / 3] * 3 + lane % 3]);
+  // two elements per warp trip: lanes 0-15 evaluate both elements' 16 Gauss-point tangents at once
+  for (int64_t ep = e0 + 2 * (blockIdx.x * (int64_t)kKelemWarps + w); ep < e1;
+       ep += 2 * (int64_t)gridDim.x * kKelemWarps) {
+    const int ne = ep + 1 < e1 ? 2 : 1;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (h < ne && lane < 24) {
+        int64_t nodes[8];
+        elem_nodes<3>(ep + h, nx, ny, nodes);
+        us[w][h][lane] = __ldg(&u[nodes[lane / 3] * 3 + lane % 3]);
+      }
     __syncwarp();
-    if (lane < 8) {
-      const int q = lane;
+    if (lane < 8 * ne) {
+      const int h = lane >> 3, q = lane & 7;
+      const int64_t e = ep + h;
+      const DMat m = s.mats[s.phase[e]];
       double H[3][3];
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
-          double h = 0.0;
+          double hh = 0.0;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) h += us[w][k * 3 + a] * G.g[q][k][b];
-          H[a][b] = h;
+          for (int k = 0; k < 8; ++k) hh += us[w][h][k * 3 + a] * G.g[q][k][b];
+          H[a][b] = hh;
         }
       TangentQP<3> t;
       tangent_qp<3>(m, H, t, err, s.hist ? s.hist + (e * 8 + q) * kHist : nullptr);
-      ts[w][q] = t;
+      ts[w][h][q] = t;
     }
     __syncwarp();
-    {  // lane = (corner ln, corner pair g): blocks (ln, lm) for lm = 2g, 2g + 1, all three rows
+    for (int he = 0; he < ne; ++he) {  // lane = (corner ln, corner pair g): blocks (ln, 2g), (ln, 2g + 1)
+      const int64_t e = ep + he;
       const int ln = lane >> 2, g = lane & 3;
       double K[2][3][3];
 #pragma unroll
@@ -142,7 +151,7 @@ __global__ void __launch_bounds__(32 * kKelemWarps) k_grid_kelem(const __grid_co
 #pragma unroll
           for (int b = 0; b < 3; ++b) K[h][a][b] = 0.0;
       for (int q = 0; q < 8; ++q) {
-        const TangentQP<3>& t = ts[w][q];
+        const TangentQP<3>& t = ts[w][he][q];
         double gn[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) gn[c] = G.g[q][ln][c];
