@@ -261,6 +261,18 @@ int32_t orc_mf_diagonal(void* sys, const double* u, double* d) {
   });
 }
 
+int32_t orc_mf_diagonal_mt(void* sys, const double* u, double* d, int32_t nthreads) {
+  return guarded([&] {
+    auto* s = S(sys);
+    std::vector<double> v;
+    by_dim(s, [&] { v = orc::assemble_diagonal_mt<2>(s->batches, u, s->n_dof(), nthreads); },
+           [&] { v = orc::assemble_diagonal_mt<3>(s->batches, u, s->n_dof(), nthreads); });
+    for (int64_t k = 0; k < s->n_dof(); ++k)
+      if (s->table.constrained[k]) v[k] = 1.0;
+    std::memcpy(d, v.data(), v.size() * 8);
+  });
+}
+
 int32_t orc_csr_apply(void* sys, const double* values, const double* x, double* y) {
   return guarded([&] {
     auto* s = S(sys);

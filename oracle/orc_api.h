@@ -128,6 +128,7 @@ int32_t orc_constrain_residual(void* sys, double* residual, const double* u);
 int32_t orc_mf_apply(void* sys, const double* u, const double* x, double* y);
 int32_t orc_mf_apply_mt(void* sys, const double* u, const double* x, double* y, int32_t nthreads);
 int32_t orc_mf_diagonal(void* sys, const double* u, double* d);
+int32_t orc_mf_diagonal_mt(void* sys, const double* u, double* d, int32_t nthreads);  // threaded, same values
 int32_t orc_csr_apply(void* sys, const double* values, const double* x, double* y);
 
 /* op_kind 0: EXPLICIT over values (eliminated CSR values, pattern order); 1: MATRIX_FREE at state u */

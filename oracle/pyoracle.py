@@ -122,6 +122,7 @@ class Oracle:
             "orc_mf_apply": [vp, vp, vp, vp],
             "orc_mf_apply_mt": [vp, vp, vp, vp, C.c_int32],
             "orc_mf_diagonal": [vp, vp, vp],
+            "orc_mf_diagonal_mt": [vp, vp, vp, C.c_int32],
             "orc_csr_apply": [vp, vp, vp, vp],
             "orc_solve": [vp, C.c_int32, vp, vp, vp, vp, vp, vp, vp, C.c_int32],
             "orc_solve_bvp": [vp, vp, vp, vp, vp, vp, C.c_int32],
@@ -284,8 +285,13 @@ class OracleSystem:
         self._c(self.o.lib.orc_mf_apply_mt(self.h, _p(u), _p(x), _p(out), nthreads))
         return out
 
-    def mf_diagonal(self, u):
-        return self._vec(self.o.lib.orc_mf_diagonal, u)
+    def mf_diagonal(self, u, nthreads=1):
+        if nthreads <= 1:
+            return self._vec(self.o.lib.orc_mf_diagonal, u)
+        out = np.zeros(self.n)
+        u = np.ascontiguousarray(u, np.float64)
+        self._c(self.o.lib.orc_mf_diagonal_mt(self.h, _p(u), _p(out), nthreads))
+        return out
 
     def csr_apply(self, values, x):
         out = np.zeros(self.n)

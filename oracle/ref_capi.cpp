@@ -283,6 +283,10 @@ int32_t orc_mf_diagonal(void* sys, const double* u, double* d) {
   });
 }
 
+int32_t orc_mf_diagonal_mt(void* sys, const double* u, double* d, int32_t) {
+  return orc_mf_diagonal(sys, u, d);  // the reference is single-threaded
+}
+
 int32_t orc_csr_apply(void* sys, const double* values, const double* x, double* y) {
   return guarded([&] {
     auto* s = S(sys);

@@ -714,6 +714,35 @@ std::vector<double> assemble_diagonal(const std::vector<Batch>& batches, const d
   return diag;
 }
 
+// assemble_diagonal on host threads (bench/test sizing only): per-thread partial vectors over
+// contiguous element ranges of each batch, summed in thread order afterwards.
+template <int D>
+std::vector<double> assemble_diagonal_mt(const std::vector<Batch>& batches, const double* u, int64_t n,
+                                         int nthreads) {
+  if (nthreads <= 1) return assemble_diagonal<D>(batches, u, n);
+  constexpr int nd = ET<D>::ndpe;
+  std::vector<std::vector<double>> part(nthreads, std::vector<double>(n, 0.0));
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; ++t)
+    th.emplace_back([&, t] {
+      std::vector<double> K(nd * nd), ue(nd);
+      for (const auto& b : batches) {
+        const std::size_t lo = b.size() * t / nthreads, hi = b.size() * (t + 1) / nthreads;
+        for (std::size_t e = lo; e < hi; ++e) {
+          const int* dofs = &b.dof_map[e * nd];
+          for (int k = 0; k < nd; ++k) ue[k] = u[dofs[k]];
+          element_jacobian<D>(b, e, ue.data(), K.data());
+          for (int k = 0; k < nd; ++k) part[t][dofs[k]] += K[k * nd + k];
+        }
+      }
+    });
+  for (auto& x : th) x.join();
+  std::vector<double> diag(n, 0.0);
+  for (int t = 0; t < nthreads; ++t)
+    for (int64_t i = 0; i < n; ++i) diag[i] += part[t][i];
+  return diag;
+}
+
 // constraint_table (assembly.hpp:197-211)
 inline ConstraintTable constraint_table(const std::vector<Constraint>& cs, int64_t n_dof, int D) {
   ConstraintTable t;

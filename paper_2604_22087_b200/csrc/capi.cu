@@ -337,11 +337,25 @@ __global__ void k_zero_masked(const uint8_t* mask, const double* v, double* out,
     out[i] = mask[i] ? 0.0 : v[i];
 }
 
+// run_solver (backend.hpp:241-286) over a slab operator: CG runs the distributed device-scalar PCG
+// loop; GMRES and BiCGStab run the single-GPU methods over the operator's owned-dof inner products
+// (one allreduce each). Preconditioners: NONE or JACOBI. Collective.
+void dist_run_solver(DistMfOp& op, const SolverCfg& sc, const double* b, const double* x0, double* x,
+                     SolveReport& r) {
+  if (sc.method == 1 || sc.method == 2) {
+    if (sc.precond != 0 && sc.precond != 1) throw CapabilityError("distributed run_solver: NONE or JACOBI");
+    solve(op, sc, b, x0, x, r);
+  } else {
+    dist_solve(op, sc, b, x0, x, r);
+  }
+}
+
 // solve_bvp (newton.hpp:59-152) over a z-slab decomposition: each rank holds its slab's u (shared
 // node planes duplicated and kept identical); the residual's shared planes are summed over the
 // neighbours, the free norm is a global dot over owned dofs, and each Newton step solves the
-// distributed matrix-free system with the distributed Jacobi-PCG (the assembled tangent is not
-// distributed: operator_kind must be MATRIX_FREE). Collective: every rank calls it.
+// distributed tangent system — matrix-free, or (EXPLICIT) every slab's own assembled and eliminated
+// tangent with the same plane halo — with the configured Krylov method (dist_run_solver).
+// Collective: every rank calls it.
 void dist_newton(System& s, Comm* comm, const afem_newton_cfg* cfg, double* u, NewtonReport& rep) {
   validate_newton(cfg);
   Ctx& c = *s.ctx;
@@ -395,7 +409,7 @@ void dist_newton(System& s, Comm* comm, const afem_newton_cfg* cfg, double* u, N
     constrain_residual(s, rhs.p, u);
     scal(c, -1.0, rhs.p, n);
     SolveReport lin;
-    dist_solve(*op, lcfg, rhs.p, nullptr, du.p, lin);
+    dist_run_solver(*op, lcfg, rhs.p, nullptr, du.p, lin);
     rep.linear.push_back(lin);
     if (!lin.converged) {
       rep.failure = "newton: linear solve failed at iteration " + std::to_string(rep.iterations + 1) +
@@ -458,6 +472,7 @@ afem_status afem_ctx_destroy(afem_ctx ctx) {
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
     ctx->c.release_copy_streams();
+    ctx->c.release_graph_resources();
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
   });
@@ -1240,12 +1255,7 @@ afem_status afem_dist_solve(afem_dist d, afem_op op, const afem_solver_cfg* cfg,
     Out<double> dx(c, x, dop->n, false);
     SolveReport r;
     const SolverCfg sc = to_cfg(cfg);
-    if (sc.method == 1 || sc.method == 2) {  // GMRES / BiCGStab through the operator's owned inner products
-      if (sc.precond != 0 && sc.precond != 1) throw CapabilityError("distributed run_solver: NONE or JACOBI");
-      solve(*dop, sc, db.d, dx0.d, dx.d, r);
-    } else {
-      dist_solve(*dop, sc, db.d, dx0.d, dx.d, r);
-    }
+    dist_run_solver(*dop, sc, db.d, dx0.d, dx.d, r);
     dx.finish();
     fill_report(r, rep, history, hist_cap);
   });

@@ -100,12 +100,99 @@ struct Ctx {
     if (s_out) cudaStreamDestroy(s_out);
     s_in = s_out = nullptr;
   }
+  // Per-context resources of the graph paths (created lazily on this context's device, so two
+  // contexts on different devices driven from one host thread never share them):
+  //   cap        private capture stream (the context stream may be the legacy default stream)
+  //   snap/snap_ev  pinned host slots + events for the CG loop's status snapshots
+  //   pcg_parts  block partials of the persistent cooperative CG
+  cudaStream_t cap = nullptr;
+  void* snap = nullptr;
+  size_t snap_bytes = 0;
+  cudaEvent_t snap_ev[2] = {nullptr, nullptr};
+  DevArray<double> pcg_parts;
+  cudaStream_t capture_stream() {
+    if (!cap) AFEM_CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    return cap;
+  }
+  void* pinned_snap(size_t bytes) {
+    if (snap_bytes < bytes) {
+      if (snap) cudaFreeHost(snap);
+      snap = nullptr;
+      snap_bytes = 0;
+      AFEM_CK(cudaMallocHost(&snap, bytes));
+      snap_bytes = bytes;
+    }
+    for (cudaEvent_t& e : snap_ev)
+      if (!e) AFEM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return snap;
+  }
+  void release_graph_resources() {
+    for (cudaEvent_t& e : snap_ev)
+      if (e) cudaEventDestroy(e), e = nullptr;
+    if (snap) cudaFreeHost(snap);
+    snap = nullptr;
+    snap_bytes = 0;
+    if (cap) cudaStreamDestroy(cap);
+    cap = nullptr;
+    pcg_parts.release();
+  }
   void* stage(size_t bytes) {
     if (staging_next >= (int)staging.size()) staging.emplace_back();
     DevArray<uint8_t>& b = staging[staging_next++];
     if (b.n < bytes) b.alloc(bytes);
     return b.p;
   }
+};
+
+// Stream capture of library launches into a graph, exception-safe: the context's stream is
+// redirected to its private capture stream for the guard's lifetime. end() returns the captured
+// graph; if the guard dies without end() (a launch threw), the capture is ended and discarded and
+// the context's stream and launch counter are restored, so the context stays usable.
+struct CaptureGuard {
+  Ctx& c;
+  cudaStream_t home;
+  int64_t l0;
+  bool open = true;
+  explicit CaptureGuard(Ctx& ctx) : c(ctx), home(ctx.stream), l0(ctx.launches) {
+    cudaStream_t s = c.capture_stream();
+    AFEM_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    c.stream = s;
+  }
+  // ends the capture; returns the graph (caller owns it) and the number of launches captured
+  cudaGraph_t end(int64_t* captured = nullptr) {
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c.stream, &g);
+    open = false;
+    if (captured) *captured = c.launches - l0;
+    c.stream = home;
+    c.launches = l0;
+    AFEM_CK(e);
+    return g;
+  }
+  ~CaptureGuard() {
+    if (!open) return;
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(c.stream, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();  // clear the capture-invalidation error
+    c.stream = home;
+    c.launches = l0;
+  }
+  CaptureGuard(const CaptureGuard&) = delete;
+  CaptureGuard& operator=(const CaptureGuard&) = delete;
+};
+
+// Runs a callable on scope exit (cleanup on every path, exceptions included).
+template <class F>
+struct ScopeExit {
+  F f;
+  bool armed = true;
+  explicit ScopeExit(F fn) : f(std::move(fn)) {}
+  ~ScopeExit() {
+    if (armed) f();
+  }
+  ScopeExit(const ScopeExit&) = delete;
+  ScopeExit& operator=(const ScopeExit&) = delete;
 };
 
 constexpr int kRedBlocks = 1184;  // 8 x 148 SMs: partial-sum slots for the deterministic reductions

@@ -669,7 +669,12 @@ void grid_jacobian(System& s, const double* u, double* values) {
     GeoT<3> G;
     geo<3>(s, G);
     static const bool node_centric = std::getenv("AFEM_NODE_JACOBIAN") != nullptr;
-    if (node_centric) {
+    const int64_t budget = (int64_t)1 << 31;  // element-block scratch bytes of the slab path
+    const int64_t plane_bytes = (int64_t)s.nx * s.ny * kKe * 8;
+    // the slab path holds at least two element planes of blocks (a slab plus its lower halo
+    // plane); when that exceeds the budget (very wide xy grids) the node-centric kernel, which
+    // needs no scratch, assembles instead
+    if (node_centric || budget / plane_bytes < 2) {
       launch(*s.ctx, k_grid_jacobian<3>, grid_for(s.n_nodes, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, u,
              values);
       return;
@@ -677,8 +682,7 @@ void grid_jacobian(System& s, const double* u, double* values) {
     // z slabs of node planes; slab [k0, k1) needs element planes [k0 - 1, k1) (clamped)
     const int64_t epp = (int64_t)s.nx * s.ny, npp = (int64_t)(s.nx + 1) * (s.ny + 1);
     const int nzn = s.nz + 1;
-    const int64_t budget = (int64_t)1 << 31;  // scratch bytes
-    int S = static_cast<int>(std::max<int64_t>(1, budget / (epp * kKe * 8) - 1));
+    int S = static_cast<int>(std::max<int64_t>(1, budget / plane_bytes - 1));
     if (const char* e = std::getenv("AFEM_JAC_SLAB")) S = std::max(1, std::atoi(e));  // tests: force slabs
     if (!s.kscr.p || s.kscr.n < (size_t)std::min<int64_t>(S + 1, s.nz) * epp * kKe)
       s.kscr.alloc((size_t)std::min<int64_t>(S + 1, s.nz) * epp * kKe);

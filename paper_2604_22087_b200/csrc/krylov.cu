@@ -355,7 +355,7 @@ bool cg_persistent(Operator& op, double* x, double* r, double* p, double* ap, co
   const int64_t want = (s.n_nodes * 32 + 255) / 256;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, cap),
                                                                                (int64_t)per_sm * c.num_sms)));
-  static thread_local DevArray<double> parts;
+  DevArray<double>& parts = c.pcg_parts;
   if (parts.n < (size_t)3 * blocks) parts.alloc(3 * (size_t)blocks);
   SysView v = s.view();
   int64_t n = op.n;
@@ -489,27 +489,23 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
           // the iteration loop as a CUDA graph of kGraphIters iterations (captured once per solve):
           // one launch per chunk instead of four per iteration, so host hiccups cannot drain the GPU
           constexpr int kGraphIters = 16;
-          static thread_local CgDev* hst = nullptr;  // two status snapshots (chunks k and k + 1)
-          static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
-          if (!hst) AFEM_CK(cudaMallocHost(reinterpret_cast<void**>(&hst), 2 * sizeof(CgDev)));
-          for (cudaEvent_t& e : ev)
-            if (!e) AFEM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          CgDev* hst = static_cast<CgDev*>(c.pinned_snap(2 * sizeof(CgDev)));  // snapshots of chunks k, k + 1
+          cudaEvent_t* ev = c.snap_ev;
           cudaGraph_t graph = nullptr;
           cudaGraphExec_t exec = nullptr;
-          const int64_t l0 = c.launches;
-          // capture on a private stream (the context stream may be the legacy default stream, which
-          // cannot capture); the instantiated graph is launched on the context stream
-          static thread_local cudaStream_t cap = nullptr;
-          if (!cap) AFEM_CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-          cudaStream_t home = c.stream;
-          c.stream = cap;
-          AFEM_CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-          enqueue(kGraphIters);
-          const cudaError_t ce = cudaStreamEndCapture(cap, &graph);
-          c.stream = home;
-          AFEM_CK(ce);
-          const int64_t per_graph = c.launches - l0;
-          c.launches = l0;
+          // on every exit (exceptions included): the speculative skip flag points into this solve's
+          // CgDev, so it is detached before st is freed; graph objects are released
+          ScopeExit cleanup([&] {
+            op.set_skip(nullptr);
+            if (exec) cudaGraphExecDestroy(exec);
+            if (graph) cudaGraphDestroy(graph);
+          });
+          int64_t per_graph = 0;
+          {
+            CaptureGuard cap(c);  // instantiated graph is launched on the context stream
+            enqueue(kGraphIters);
+            graph = cap.end(&per_graph);
+          }
           AFEM_CK(cudaGraphInstantiate(&exec, graph, 0));
           auto run = [&] {
             AFEM_CK(cudaGraphLaunch(exec, c.stream));
@@ -532,9 +528,6 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
           }
           AFEM_CK(cudaStreamSynchronize(c.stream));
           hs = fetch(c, st.p);
-          cudaGraphExecDestroy(exec);
-          cudaGraphDestroy(graph);
-          op.set_skip(nullptr);
         }
       }
       if (!persistent) launch(c, k_cg_x_epilogue, eg, 256, 0, x, p.p, n, st.p);

@@ -945,23 +945,17 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, 
     stencil_apply_launch(pl, op, x, y, dot_out, skip);
     return;
   }
-  if (!pl.gexec || pl.gx != x || pl.gy != y) {  // (re)capture on a private stream (the context
-    static thread_local cudaStream_t cap = nullptr;  // stream may be the legacy default stream)
-    if (!cap) AFEM_CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-    cudaGraph_t g = nullptr;
-    cudaStream_t home = c.stream;
-    const int64_t l0 = c.launches;
-    c.stream = cap;
-    AFEM_CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    stencil_apply_launch(pl, op, x, y, nullptr, nullptr);
-    const cudaError_t ce = cudaStreamEndCapture(cap, &g);
-    c.stream = home;
-    c.launches = l0;
-    AFEM_CK(ce);
+  if (!pl.gexec || pl.gx != x || pl.gy != y) {  // (re)capture on the context's private stream
     if (pl.gexec) cudaGraphExecDestroy(pl.gexec);
     pl.gexec = nullptr;
+    cudaGraph_t g = nullptr;
+    {
+      CaptureGuard cap(c);
+      stencil_apply_launch(pl, op, x, y, nullptr, nullptr);
+      g = cap.end();
+    }
+    ScopeExit free_graph([&] { cudaGraphDestroy(g); });
     AFEM_CK(cudaGraphInstantiate(&pl.gexec, g, 0));
-    cudaGraphDestroy(g);
     pl.gx = x;
     pl.gy = y;
   }

@@ -250,6 +250,7 @@ def test_graph_apply_recaptures_on_new_pointers(afem, ctx):
         torch.cuda.synchronize()
         assert np.array_equal(yk.cpu().numpy(), ref[k])
     dx[0].copy_(dx[2])  # same pointers, new contents
+    torch.cuda.synchronize()  # the copy runs on torch's stream, the apply on the context's own
     L.afem_op_apply_async(op.h, C.c_void_p(dx[0].data_ptr()), C.c_void_p(dy[0].data_ptr()))
     torch.cuda.synchronize()
     assert np.array_equal(dy[0].cpu().numpy(), ref[2])
