@@ -28,17 +28,18 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "afem_impl.hpp"
 #include "reduce.cuh"
+#include "tma.cuh"
 
 namespace afem {
 
 constexpr int kVoid = 31;  // phase code of an octant outside the domain (E = 0)
 
 struct StencilParams {
-  double S[27][3][3];          // full family, d = (dx+1) + 3(dy+1) + 9(dz+1)
   double HY[2][9][3][3];       // y face lo/hi, entries with dy = 0: index (dx+1) + 3(dz+1)
   double HZ[2][9][3][3];       // z face lo/hi, entries with dz = 0: index (dx+1) + 3(dy+1)
   double HYZ[2][2][3][3][3];   // y and z faces, entries with dy = dz = 0: index dx+1
@@ -46,7 +47,6 @@ struct StencilParams {
   // S(d)_ab = sgn(d_a) sgn(d_b) Og[pair(a,b)][|d_c|] (a != b, c the third axis; zero if d_a d_b = 0).
   double Dg[3][2][2][2];
   double Og[3][2];             // pairs xy, xz, yz
-  double K[24][24];            // uniform-brick element stiffness at E = 1
   double E[32];                // modulus per phase code (E[kVoid] = 0)
   int NX, NY, NZ;              // node counts per axis
   int NXm;                     // node columns the main kernel covers (tiles of 64; the last may be partial)
@@ -91,6 +91,13 @@ struct StencilPlan {
   int npieces = 1;
   std::vector<int64_t> piece_items;
   int iocc = 1;
+  // TMA staging of the main kernel (k_stencil_tma): info map once per plan, x map per x pointer
+  bool tma = true;
+  DevArray<uint8_t> info_pad;  // the TMA kernel's padded info rows (k_info_pad)
+  int ipx = 0;
+  CUtensorMap mi{}, mx{};
+  const double* mx_ptr = nullptr;
+  int xshift = 0;
 };
 
 namespace {
@@ -179,38 +186,60 @@ __device__ __forceinline__ void nb(const StencilParams& P, double x0, double x1,
   }
 }
 
-// One staged row DJ: 6 LDS.128 (conflict-free, 48 B lane stride) give the 12 interleaved dofs of
-// the lane's window: left neighbour, node 0, node 1, right neighbour.
-template <int DJ, int YF, int ZF>
-__device__ __forceinline__ void row_step(const StencilParams& P, const double* __restrict__ srow, int tx,
+// The 12 interleaved dofs of the lane's window in one staged row (left neighbour, node 0, node 1,
+// right neighbour). off = 0: 6 LDS.128 (conflict-free, 48 B lane stride). The TMA-staged rows land
+// 0 or 1 double in (boxes start on 16-byte boundaries), so that kernel reads 12 LDS.64 at the
+// row's offset (the same shared wavefronts: two-way conflicts per half-warp instead of per-quarter
+// 16-byte accesses) with no per-row code variants.
+template <bool ALIGNED>
+__device__ __forceinline__ void load_window(const double* __restrict__ srow, int tx, int off, double (&w)[12]) {
+  if constexpr (ALIGNED) {
+    const double2* r2 = reinterpret_cast<const double2*>(srow + 6 * tx);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const double2 v = r2[k];
+      w[2 * k] = v.x;
+      w[2 * k + 1] = v.y;
+    }
+  } else {
+    const double* r = srow + off + 6 * tx;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) w[k] = r[k];
+  }
+}
+
+template <int DJ, int YF, int ZF, bool ALIGNED>
+__device__ __forceinline__ void row_step(const StencilParams& P, const double* __restrict__ srow, int tx, int off,
                                          double (&acc)[2][3][3]) {
-  const double2* r2 = reinterpret_cast<const double2*>(srow + 6 * tx);
-  const double2 w0 = r2[0], w1 = r2[1], w2 = r2[2], w3 = r2[3], w4 = r2[4], w5 = r2[5];
-  nb<-1, DJ, YF, ZF, 0>(P, w0.x, w1.y, acc);
-  nb<-1, DJ, YF, ZF, 1>(P, w0.y, w2.x, acc);
-  nb<-1, DJ, YF, ZF, 2>(P, w1.x, w2.y, acc);
-  nb<0, DJ, YF, ZF, 0>(P, w1.y, w3.x, acc);
-  nb<0, DJ, YF, ZF, 1>(P, w2.x, w3.y, acc);
-  nb<0, DJ, YF, ZF, 2>(P, w2.y, w4.x, acc);
-  nb<1, DJ, YF, ZF, 0>(P, w3.x, w4.y, acc);
-  nb<1, DJ, YF, ZF, 1>(P, w3.y, w5.x, acc);
-  nb<1, DJ, YF, ZF, 2>(P, w4.x, w5.y, acc);
+  double w[12];
+  load_window<ALIGNED>(srow, tx, off, w);
+  nb<-1, DJ, YF, ZF, 0>(P, w[0], w[3], acc);
+  nb<-1, DJ, YF, ZF, 1>(P, w[1], w[4], acc);
+  nb<-1, DJ, YF, ZF, 2>(P, w[2], w[5], acc);
+  nb<0, DJ, YF, ZF, 0>(P, w[3], w[6], acc);
+  nb<0, DJ, YF, ZF, 1>(P, w[4], w[7], acc);
+  nb<0, DJ, YF, ZF, 2>(P, w[5], w[8], acc);
+  nb<1, DJ, YF, ZF, 0>(P, w[6], w[9], acc);
+  nb<1, DJ, YF, ZF, 1>(P, w[7], w[10], acc);
+  nb<1, DJ, YF, ZF, 2>(P, w[8], w[11], acc);
 }
 
-template <int YF, int ZF>
+template <int YF, int ZF, int STRIDE>
 __device__ __forceinline__ void plane_step(const StencilParams& P, const double* __restrict__ s, int tx, int ty,
-                                           double (&acc)[2][3][3]) {
-  row_step<-1, YF, ZF>(P, s + (ty + 0) * RS, tx, acc);
-  row_step<0, YF, ZF>(P, s + (ty + 1) * RS, tx, acc);
-  row_step<1, YF, ZF>(P, s + (ty + 2) * RS, tx, acc);
+                                           int offs, double (&acc)[2][3][3]) {
+  constexpr bool AL = STRIDE == RS;  // the cp.async-staged kernel's rows are 16-byte aligned
+  row_step<-1, YF, ZF, AL>(P, s + (ty + 0) * STRIDE, tx, offs & 1, acc);
+  row_step<0, YF, ZF, AL>(P, s + (ty + 1) * STRIDE, tx, (offs >> 1) & 1, acc);
+  row_step<1, YF, ZF, AL>(P, s + (ty + 2) * STRIDE, tx, (offs >> 2) & 1, acc);
 }
 
-template <int YF>
+// offs: bit r = the window offset of staged row ty + r (0 for the cp.async-staged kernel)
+template <int YF, int STRIDE = RS>
 __device__ __forceinline__ void plane_dispatch(const StencilParams& P, const double* s, int tx, int ty, int zc,
-                                               double (&acc)[2][3][3]) {
-  if (zc == 0) plane_step<YF, 0>(P, s, tx, ty, acc);
-  else if (zc == 1) plane_step<YF, 1>(P, s, tx, ty, acc);
-  else plane_step<YF, 2>(P, s, tx, ty, acc);
+                                               double (&acc)[2][3][3], int offs = 0) {
+  if (zc == 0) plane_step<YF, 0, STRIDE>(P, s, tx, ty, offs, acc);
+  else if (zc == 1) plane_step<YF, 1, STRIDE>(P, s, tx, ty, offs, acc);
+  else plane_step<YF, 2, STRIDE>(P, s, tx, ty, offs, acc);
 }
 
 __host__ __device__ __forceinline__ int local_node(int lx, int ly, int lz) {
@@ -429,6 +458,246 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm) k_stencil_main(const __g
       block_reduce<1>(a);
       if (threadIdx.x == 0) dot.part_main[bid] = a[0];
     }
+  }
+}
+
+// k_stencil_tma: the main kernel with Blackwell bulk-async staging. Per CTA plane the (TY + 2)
+// rows of the 64 + 2 node window (interleaved dofs) and their info bytes arrive by TMA: rank-1
+// tensor copies (cp.async.bulk.tensor.1d; boxes start on 16-byte boundaries, zero fill outside
+// [0, n)) issued by one thread and completed on one mbarrier per ring slot — no per-thread address
+// arithmetic and no registers spent on staging. x rows: the box starts at the even element at or
+// below the row's first dof, so a row lands 0 or 1 double in (its parity, known to every thread;
+// load_window reads either). Info rows come from a padded copy of the info bytes (row pitch ipx, a
+// multiple of 16, >= 16 pad bytes of value 7 = "all components masked" before every row start and
+// after every tile's last column), so a row's box always starts 16-byte aligned, 15 bytes before
+// the window. Rows outside the y range are never copied (their slot rows are zeroed once per
+// segment); columns outside [0, NX) and Dirichlet dofs are zeroed by one masking pass per plane
+// from the staged info bytes (one 4-byte word per thread, an early out when it holds no constrained
+// dof). Ring of 4 slots: plane p is computed, p + 1 is landed and masked, p + 2 is in flight, and
+// p + 3 is issued into p - 1's slot after the plane barrier (a proxy fence orders the threads'
+// generic writes before the async-proxy overwrite). Arithmetic, output order and the fused dot are
+// those of k_stencil_main, so the two kernels are bitwise identical.
+constexpr int RSP = 208;             // staged row pitch (doubles): 200 landed, rows 128-byte aligned for TMA
+constexpr int IRP = 128;             // staged info row pitch (bytes)
+constexpr int XBOX = 3 * (TXN + 2) + 2;  // doubles per x box (the 198-dof window + alignment slack)
+constexpr int IBOX = 96;             // info bytes per box (15 pad + 66 window, rounded to 16)
+constexpr int IOFF = 15;             // window byte offset inside an info box
+constexpr int IW0 = IOFF / 4, IW1 = (IOFF + TXN + 2 + 3) / 4;  // info words touching the window
+constexpr int IWORDS = IW1 - IW0;
+constexpr size_t kTmaSmem = 128 + sizeof(double) * RING * (TY + 2) * RSP + RING * (TY + 2) * IRP +
+                            8 * RING + 8 * 32;
+static_assert((TY + 2) * IWORDS <= NT, "one info word per thread");
+static_assert(XBOX <= RSP && IBOX <= IRP && XBOX <= 256, "TMA box sizes");
+
+template <bool DOT>
+__global__ void __launch_bounds__(NT, kMainBlocksPerSm)
+    k_stencil_tma(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mi,
+                  const __grid_constant__ StencilParams P, int xshift, int ipx, const double* __restrict__ x,
+                  double* __restrict__ y, int kchunk, int kbeg, int kend, DotArgs dot, int ntx, int nty) {
+  if (dot.skip && *dot.skip) return;
+  double dsum = 0.0;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // 128-byte aligned base, derived from smem_raw itself so the compiler keeps shared-space
+  // accesses (LDS / STS, not generic loads)
+  unsigned char* const base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  double (*xs)[TY + 2][RSP] = reinterpret_cast<double (*)[TY + 2][RSP]>(base);
+  uint8_t (*is)[TY + 2][IRP] =
+      reinterpret_cast<uint8_t (*)[TY + 2][IRP]>(base + sizeof(double) * RING * (TY + 2) * RSP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + sizeof(double) * RING * (TY + 2) * RSP + RING * (TY + 2) * IRP);
+  double* Es = reinterpret_cast<double*>(bars + RING);
+  const int tid = threadIdx.x;
+  const int tx = tid % TX, ty = tid / TX;
+  const int NX = P.NX, NY = P.NY, NZ = P.NZ;
+  if (tid < 32) Es[tid] = P.E[tid];
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < RING; ++q) mbar_init(smem_u32(&bars[q]), 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  uint32_t phase = 0;  // bit s: parity of slot s's next completion
+  auto ring = [](int p) { return (p + 1) & (RING - 1); };
+  const int nzr = kend - kbeg;
+  int64_t u = 0, ue = 1;
+  if (kchunk <= 0) {
+    const int64_t U = (int64_t)ntx * nty * nzr;
+    u = U * blockIdx.x / gridDim.x;
+    ue = U * (blockIdx.x + 1) / gridDim.x;
+  }
+  while (u < ue) {
+    int bx, by, k0, k1;
+    if (kchunk > 0) {
+      bx = blockIdx.x;
+      by = blockIdx.y;
+      k0 = kbeg + blockIdx.z * kchunk;
+      k1 = min(k0 + kchunk, kend);
+      u = ue;
+    } else {
+      const int tile = static_cast<int>(u / nzr), kk = static_cast<int>(u % nzr);
+      const int kl = static_cast<int>(min(static_cast<int64_t>(nzr), kk + (ue - u)));
+      bx = tile % ntx;
+      by = tile / ntx;
+      k0 = kbeg + kk;
+      k1 = kbeg + kl;
+      u += kl - kk;
+    }
+    const int i0 = bx * TXN, j0 = by * TY;
+    const int i = i0 + 2 * tx, j = j0 + ty;
+    const bool active = j < NY;
+    const bool v0 = i < P.NXm, v1 = i + 1 < P.NXm;
+    const int yf = j == 0 ? 1 : (j == NY - 1 ? 2 : 0);
+    // window offset (0 / 1 double) of staged row r of plane p: parity of its first dof's element
+    auto roff = [&](int r, int p) -> int {
+      return (1 + NX * ((j0 - 1 + r) + NY * p) + xshift) & 1;  // 3 (i0 - 1 + ...) = i0 - 1 + ... mod 2
+    };
+
+    // rows outside [0, NY) are never copied: zero them in every slot for this segment
+    __syncthreads();
+    for (int r = 0; r < TY + 2; ++r) {
+      const int jj = j0 - 1 + r;
+      if (jj >= 0 && jj < NY) continue;
+      for (int q = tid; q < RING * RSP; q += NT) xs[q / RSP][r][q % RSP] = 0.0;
+    }
+    __syncthreads();
+    auto issue = [&](int p) {  // one thread: plane p into its slot
+      const int sl = ring(p);
+      const uint32_t bar = smem_u32(&bars[sl]);
+      if (p < 0 || p >= NZ) {
+        mbar_arrive(bar);
+        return;
+      }
+      int rows = 0;
+#pragma unroll
+      for (int r = 0; r < TY + 2; ++r) rows += (j0 - 1 + r >= 0 && j0 - 1 + r < NY) ? 1 : 0;
+      mbar_arrive_expect_tx(bar, static_cast<uint32_t>(rows * (XBOX * 8 + IBOX)));
+#pragma unroll
+      for (int r = 0; r < TY + 2; ++r) {
+        const int jj = j0 - 1 + r;
+        if (jj < 0 || jj >= NY) continue;
+        const int row = jj + NY * p;
+        const int c = 3 * (i0 - 1 + NX * row) + xshift;  // < 2^31 (make_stencil_plan)
+        tma_load_1d(smem_u32(&xs[sl][r][0]), &mx, c & ~1, bar);
+        tma_load_1d(smem_u32(&is[sl][r][0]), &mi, i0 + ipx * row, bar);
+      }
+    };
+    auto wait = [&](int p) {
+      const int sl = ring(p);
+      mbar_wait(smem_u32(&bars[sl]), (phase >> sl) & 1u);
+      phase ^= 1u << sl;
+    };
+    auto mask = [&](int p) {  // zero out-of-range columns and Dirichlet dofs of landed plane p
+      if (p < 0 || p >= NZ || tid >= (TY + 2) * IWORDS) return;
+      const int sl = ring(p);
+      const int r = tid / IWORDS, wb = 4 * (IW0 + tid - IWORDS * r);  // the word's first byte
+      const int jj = j0 - 1 + r;
+      if (jj < 0 || jj >= NY) return;
+      const uint32_t word = *reinterpret_cast<const uint32_t*>(&is[sl][r][wb]);
+      if (!(word & 0x07070707u)) return;
+      double* row = &xs[sl][r][roff(r, p)];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int col = wb + b - IOFF;
+        if (col < 0 || col >= TXN + 2) continue;
+        const uint32_t m = (word >> (8 * b)) & 7u;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if ((m >> c) & 1u) row[3 * col + c] = 0.0;
+      }
+    };
+
+    double acc[2][3][3];
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) acc[n][r][a] = 0.0;
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      issue(k0 - 1);
+      issue(k0);
+      issue(k0 + 1);  // k1 >= k0 + 1
+    }
+    wait(k0 - 1);
+    mask(k0 - 1);
+    __syncthreads();
+    for (int p = k0 - 1; p <= k1; ++p) {
+      if (active && p >= 0 && p < NZ) {
+        const int zc = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
+        const double* sp = &xs[ring(p)][0][0];
+        const int offs = roff(ty, p) | (roff(ty + 1, p) << 1) | (roff(ty + 2, p) << 2);
+        if (yf == 0) plane_dispatch<0, RSP>(P, sp, tx, ty, zc, acc, offs);
+        else if (yf == 1) plane_dispatch<1, RSP>(P, sp, tx, ty, zc, acc, offs);
+        else plane_dispatch<2, RSP>(P, sp, tx, ty, zc, acc, offs);
+      }
+      if (active && p - 1 >= k0) {  // nodes (i, j, p-1) and (i+1, j, p-1) are complete
+        const int so = ring(p - 1);
+        const uint32_t oi0 = is[so][ty + 1][IOFF + 2 * tx + 1], oi1 = is[so][ty + 1][IOFF + 2 * tx + 2];
+        const double E0 = Es[oi0 >> 3], E1 = Es[oi1 >> 3];
+        const int64_t onode = i + (int64_t)NX * (j + (int64_t)NY * (p - 1));
+        // own nodes' staged inputs (raw x unless constrained)
+        const double* xrow = &xs[so][ty + 1][roff(ty + 1, p - 1) + 3 * (2 * tx + 1)];
+        double* yo = y + 3 * onode;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const bool c0 = (oi0 >> a) & 1, c1 = (oi1 >> a) & 1;
+          const double x0 = c0 ? (v0 ? __ldg(&x[3 * onode + a]) : 0.0) : xrow[a];
+          const double x1 = c1 ? (v1 ? __ldg(&x[3 * onode + 3 + a]) : 0.0) : xrow[3 + a];
+          const double y0 = c0 ? x0 : E0 * acc[0][0][a];
+          const double y1 = c1 ? x1 : E1 * acc[1][0][a];
+          if (v0) yo[a] = y0;
+          if (v1) yo[3 + a] = y1;
+          if constexpr (DOT) {
+            dsum = fma(v0 ? x0 : 0.0, y0, dsum);
+            dsum = fma(v1 ? x1 : 0.0, y1, dsum);
+          }
+        }
+      }
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          acc[n][0][a] = acc[n][1][a];
+          acc[n][1][a] = acc[n][2][a];
+          acc[n][2][a] = 0.0;
+        }
+      if (p < k1) {
+        wait(p + 1);
+        mask(p + 1);
+      }
+      __syncthreads();
+      if (tid == 0 && p + 3 <= k1) {
+        fence_proxy_async_smem();
+        issue(p + 3);
+      }
+    }
+  }
+  if constexpr (DOT) {
+    const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int nb = gridDim.x * gridDim.y * gridDim.z;
+    if (dot.finish) {
+      block_to_slot_and_finish(dsum, dot.part_main, bid, nb, nullptr, 0, dot.counter, dot.out);
+    } else {
+      double a[1] = {dsum};
+      block_reduce<1>(a);
+      if (threadIdx.x == 0) dot.part_main[bid] = a[0];
+    }
+  }
+}
+
+// Padded info copy for the TMA kernel: row (j, k) of NX bytes at 16 + ipx (j + NY k); every other
+// byte is 7 (all three components masked = outside the domain).
+__global__ void k_info_pad(const uint8_t* __restrict__ info, uint8_t* __restrict__ out, int NX, int NY, int NZ,
+                           int ipx, int64_t total) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = q - 16;
+    uint8_t v = 7;
+    if (r >= 0) {
+      const int64_t row = r / ipx;
+      const int i = static_cast<int>(r - row * ipx);
+      if (i < NX && row < (int64_t)NY * NZ) v = info[i + (int64_t)NX * row];
+    }
+    out[q] = v;
   }
 }
 
@@ -680,6 +949,34 @@ bool snap(double s[27][3][3], int broken) {
 
 }  // namespace
 
+void encode_map_1d(CUtensorMap* map, const void* base, uint64_t n, CUtensorMapDataType type, uint32_t box) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    AFEM_CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  const cuuint64_t dims[1] = {n};
+  const cuuint64_t unused_stride[1] = {16};  // rank 1 has no strides, but the driver rejects a null array
+  const cuuint32_t boxd[1] = {box}, estr[1] = {1};
+  const CUresult r = enc(map, type, 1, const_cast<void*>(base), dims, unused_stride, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
+// x map of the main kernel for this x (8-byte aligned: the map starts at the 16-byte boundary at or
+// below x and element coordinates are shifted by one when x sits 8 bytes above it)
+static void stencil_x_map(StencilPlan& pl, const double* x) {
+  if (pl.mx_ptr == x) return;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(x), b = a & ~uintptr_t(15);
+  pl.xshift = static_cast<int>((a - b) / 8);
+  const uint64_t n = 3ull * pl.p.NX * pl.p.NY * pl.p.NZ + pl.xshift;
+  encode_map_1d(&pl.mx, reinterpret_cast<const void*>(b), n, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, XBOX);
+  pl.mx_ptr = x;
+}
+
 StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   if (!s.grid || s.dim != 3) return nullptr;
   if (s.mats.empty() || s.mats.size() >= kVoid) return nullptr;
@@ -706,8 +1003,6 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   std::vector<double> K(576);
   AFEM_CK(cudaMemcpyAsync(K.data(), dK.p, 576 * 8, cudaMemcpyDeviceToHost, c.stream));
   AFEM_CK(cudaStreamSynchronize(c.stream));
-  for (int r = 0; r < 24; ++r)
-    for (int q = 0; q < 24; ++q) P.K[r][q] = K[r * 24 + q];
   plan->Kg = std::move(dK);
   {
     const int r0 = 3 * local_node(0, 0, 0);
@@ -719,7 +1014,6 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   double fam[27][3][3];
   family_stencil(K, 0, 0, fam);
   if (!snap(fam, 0)) return nullptr;
-  std::memcpy(P.S, fam, sizeof P.S);
   // Symmetry-unique interior values; every entry must agree with its representative.
   double smax = 0.0;
   for (int d = 0; d < 27; ++d)
@@ -780,10 +1074,16 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   if (!attrs) {
     AFEM_CK(cudaFuncSetAttribute(k_stencil_main<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
     AFEM_CK(cudaFuncSetAttribute(k_stencil_main<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+    AFEM_CK(cudaFuncSetAttribute(k_stencil_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     attrs = true;
   }
+  plan->tma = std::getenv("AFEM_STENCIL_LDGSTS") == nullptr;  // A/B switch: the cp.async-staged kernel
   int occ = 1;
-  AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<true>, NT, kMainSmem));
+  if (plan->tma)
+    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_tma<true>, NT, kTmaSmem));
+  else
+    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<true>, NT, kMainSmem));
   const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
   const int64_t tiles = (int64_t)((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY);
   int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
@@ -795,11 +1095,21 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   const int64_t nn = s.n_nodes;
   plan->info.alloc(nn + 4);  // +4: the main kernel copies the aligned 4-byte word holding a node's byte
   AFEM_CK(cudaMemsetAsync(plan->info.p, 0, nn + 4, c.stream));
+
   DevArray<uint64_t> keys(nn);
   DevArray<unsigned long long> cnt(1);
   AFEM_CK(cudaMemsetAsync(cnt.p, 0, 8, c.stream));
   launch(c, k_stencil_classify, grid_for(nn, 256, 148 * 32), 256, 0, P.NX, P.NY, P.NZ, P.NXm, s.phase.p, op.mask.p,
          plan->info.p, keys.p, cnt.p);
+  if (plan->tma) {
+    const int ntiles_x = (P.NXm + TXN - 1) / TXN;
+    plan->ipx = ((std::max(ntiles_x * TXN + 1, P.NX + 1) + 15) / 16) * 16;  // >= 1 pad byte after each tile
+    const int64_t tot = 16 + (int64_t)plan->ipx * P.NY * P.NZ + 128;       // + the last box's overhang
+    plan->info_pad.alloc(tot);
+    launch(c, k_info_pad, grid_for(tot, 256, 148 * 16), 256, 0, plan->info.p, plan->info_pad.p, P.NX, P.NY, P.NZ,
+           plan->ipx, tot);
+    encode_map_1d(&plan->mi, plan->info_pad.p, tot, CU_TENSOR_MAP_DATA_TYPE_UINT8, IBOX);
+  }
   unsigned long long nf = 0;
   AFEM_CK(cudaMemcpyAsync(&nf, cnt.p, 8, cudaMemcpyDeviceToHost, c.stream));
   AFEM_CK(cudaStreamSynchronize(c.stream));
@@ -970,7 +1280,15 @@ static void stencil_apply_launch(StencilPlan& pl, const MfOp& op, const double* 
   const int ntx = (P.NXm + TXN - 1) / TXN, nty = (P.NY + TY - 1) / TY;
   const int nb_main = P.NXm > 0 ? pl.main_blocks : 0;
   const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main, skip};
-  if (P.NXm > 0) {  // balanced single wave (kchunk 0)
+  if (P.NXm > 0 && pl.tma) {  // balanced single wave (kchunk 0)
+    stencil_x_map(pl, x);
+    if (dot_out)
+      launch(c, k_stencil_tma<true>, nb_main, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, 0, P.NZ, dot, ntx,
+             nty);
+    else
+      launch(c, k_stencil_tma<false>, nb_main, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, 0, P.NZ, dot, ntx,
+             nty);
+  } else if (P.NXm > 0) {
     if (dot_out)
       launch(c, k_stencil_main<true>, nb_main, NT, kMainSmem, P, x, pl.info.p, y, 0, 0, P.NZ, dot, ntx, nty);
     else
@@ -1003,7 +1321,12 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
     const int want = std::max(1, kMainBlocksPerSm * c.num_sms / std::max(tiles, 1));
     const int kc = std::max(4, (ke - kb + want - 1) / want);
     const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TY - 1) / TY, (ke - kb + kc - 1) / kc);
-    launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, kc, kb, ke, dot, 0, 0);
+    if (pl.tma) {
+      stencil_x_map(pl, x);
+      launch(c, k_stencil_tma<false>, grid, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, kc, kb, ke, dot, 0, 0);
+    } else {
+      launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, kc, kb, ke, dot, 0, 0);
+    }
   }
   const int64_t i0 = pl.piece_items[pa], i1 = pl.piece_items[pb];
   if (i1 > i0) {
