@@ -689,10 +689,11 @@ class Dist:
                        failure=rep.failure.decode())
 
     def solve_bvp(self, sys: System, rtol=1e-10, atol=1e-14, max_iter=25, lin_rtol=1e-13, lin_max_iter=10000,
-                  precond=JACOBI, x0=None, operator_kind=MATRIX_FREE):
-        """Distributed solve_bvp (collective): matrix-free or assembled slab tangent, CG."""
+                  precond=JACOBI, x0=None, operator_kind=MATRIX_FREE, method=CG, restart=30):
+        """Distributed solve_bvp (collective): matrix-free or assembled slab tangent; CG, GMRES or
+        BiCGStab for the linear steps."""
         cfg = afem_newton_cfg(rtol, atol, max_iter, operator_kind,
-                              afem_solver_cfg(CG, precond, lin_rtol, lin_max_iter, 30))
+                              afem_solver_cfg(method, precond, lin_rtol, lin_max_iter, restart))
         rep = afem_newton_report()
         norms = np.zeros(max_iter + 2)
         u = np.zeros(sys.n)

@@ -92,7 +92,6 @@ struct StencilPlan {
   std::vector<int64_t> piece_items;
   int iocc = 1;
   // TMA staging of the main kernel (k_stencil_tma): info map once per plan, x map per x pointer
-  bool tma = true;
   DevArray<uint8_t> info_pad;  // the TMA kernel's padded info rows (k_info_pad)
   int ipx = 0;
   CUtensorMap mi{}, mx{};
@@ -109,11 +108,7 @@ namespace {
 #define AFEM_STENCIL_TY 4
 #endif
 constexpr int TX = 32, TXN = 2 * TX, TY = AFEM_STENCIL_TY, NT = TX * TY;
-constexpr int NS = 3 + (2 * (TXN + 2) + NT - 1) / NT;  // staging slots per thread: 3 own-row + halo rows
 constexpr int kMainBlocksPerSm = 16 / TY;
-constexpr int RS = 3 * (TXN + 2);            // shared row: interleaved dofs of 66 nodes (198 doubles, 16 B multiple)
-constexpr int NODES = (TY + 2) * (TXN + 2);  // staged nodes per plane (tile + one-node halo)
-constexpr int PER = (NODES + NT - 1) / NT;   // staged nodes per thread
 
 // Structural zero of a family's entry (a, b) at offset d: the brick's reflection symmetry about
 // an axis c that the family keeps intact makes every off-diagonal entry involving c vanish when
@@ -158,24 +153,29 @@ constexpr int broken_of() {
 
 // acc[n][r][a]: node n (0, 1) of the lane, role r (0: node below the plane sees dz = +1, 1: node on
 // the plane dz = 0, 2: node above dz = -1), component a. One neighbour column (DI, DJ), one input
-// component B, the two nodes' inputs x0, x1.
-template <int DI, int DJ, int YF, int ZF, int B>
+// component B, the two nodes' inputs x0, x1. RM: the roles computed (bit r); a segment's first
+// plane only feeds the node above it (RM 4) and its last plane only the node below (RM 1).
+template <int DI, int DJ, int YF, int ZF, int B, int RM>
 __device__ __forceinline__ void nb(const StencilParams& P, double x0, double x1, double (&acc)[2][3][3]) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    if constexpr (true) {
+    if constexpr ((RM & 1) != 0) {
       if (!szero(DI, DJ, 1, a, B, broken_of<DI, DJ, 1, YF, 0>())) {
         const double c = a == 0 ? coef<DI, DJ, 1, YF, 0, 0, B>(P) : (a == 1 ? coef<DI, DJ, 1, YF, 0, 1, B>(P)
                                                                               : coef<DI, DJ, 1, YF, 0, 2, B>(P));
         acc[0][0][a] = fma(c, x0, acc[0][0][a]);
         acc[1][0][a] = fma(c, x1, acc[1][0][a]);
       }
+    }
+    if constexpr ((RM & 2) != 0) {
       if (!szero(DI, DJ, 0, a, B, broken_of<DI, DJ, 0, YF, ZF>())) {
         const double c = a == 0 ? coef<DI, DJ, 0, YF, ZF, 0, B>(P) : (a == 1 ? coef<DI, DJ, 0, YF, ZF, 1, B>(P)
                                                                                : coef<DI, DJ, 0, YF, ZF, 2, B>(P));
         acc[0][1][a] = fma(c, x0, acc[0][1][a]);
         acc[1][1][a] = fma(c, x1, acc[1][1][a]);
       }
+    }
+    if constexpr ((RM & 4) != 0) {
       if (!szero(DI, DJ, -1, a, B, broken_of<DI, DJ, -1, YF, 0>())) {
         const double c = a == 0 ? coef<DI, DJ, -1, YF, 0, 0, B>(P) : (a == 1 ? coef<DI, DJ, -1, YF, 0, 1, B>(P)
                                                                                : coef<DI, DJ, -1, YF, 0, 2, B>(P));
@@ -187,59 +187,54 @@ __device__ __forceinline__ void nb(const StencilParams& P, double x0, double x1,
 }
 
 // The 12 interleaved dofs of the lane's window in one staged row (left neighbour, node 0, node 1,
-// right neighbour). off = 0: 6 LDS.128 (conflict-free, 48 B lane stride). The TMA-staged rows land
-// 0 or 1 double in (boxes start on 16-byte boundaries), so that kernel reads 12 LDS.64 at the
-// row's offset (the same shared wavefronts: two-way conflicts per half-warp instead of per-quarter
-// 16-byte accesses) with no per-row code variants.
-template <bool ALIGNED>
+// right neighbour): 12 LDS.64 at the row's offset (TMA boxes start on 16-byte boundaries, so a row
+// lands 0 or 1 double in). 48-byte lane stride: two-way conflicts per half-warp, the same shared
+// wavefronts as 16-byte loads of an aligned row, and no per-row code variants.
 __device__ __forceinline__ void load_window(const double* __restrict__ srow, int tx, int off, double (&w)[12]) {
-  if constexpr (ALIGNED) {
-    const double2* r2 = reinterpret_cast<const double2*>(srow + 6 * tx);
+  const double* r = srow + off + 6 * tx;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      const double2 v = r2[k];
-      w[2 * k] = v.x;
-      w[2 * k + 1] = v.y;
-    }
-  } else {
-    const double* r = srow + off + 6 * tx;
-#pragma unroll
-    for (int k = 0; k < 12; ++k) w[k] = r[k];
-  }
+  for (int k = 0; k < 12; ++k) w[k] = r[k];
 }
 
-template <int DJ, int YF, int ZF, bool ALIGNED>
+template <int DJ, int YF, int ZF, int RM>
 __device__ __forceinline__ void row_step(const StencilParams& P, const double* __restrict__ srow, int tx, int off,
                                          double (&acc)[2][3][3]) {
   double w[12];
-  load_window<ALIGNED>(srow, tx, off, w);
-  nb<-1, DJ, YF, ZF, 0>(P, w[0], w[3], acc);
-  nb<-1, DJ, YF, ZF, 1>(P, w[1], w[4], acc);
-  nb<-1, DJ, YF, ZF, 2>(P, w[2], w[5], acc);
-  nb<0, DJ, YF, ZF, 0>(P, w[3], w[6], acc);
-  nb<0, DJ, YF, ZF, 1>(P, w[4], w[7], acc);
-  nb<0, DJ, YF, ZF, 2>(P, w[5], w[8], acc);
-  nb<1, DJ, YF, ZF, 0>(P, w[6], w[9], acc);
-  nb<1, DJ, YF, ZF, 1>(P, w[7], w[10], acc);
-  nb<1, DJ, YF, ZF, 2>(P, w[8], w[11], acc);
+  load_window(srow, tx, off, w);
+  nb<-1, DJ, YF, ZF, 0, RM>(P, w[0], w[3], acc);
+  nb<-1, DJ, YF, ZF, 1, RM>(P, w[1], w[4], acc);
+  nb<-1, DJ, YF, ZF, 2, RM>(P, w[2], w[5], acc);
+  nb<0, DJ, YF, ZF, 0, RM>(P, w[3], w[6], acc);
+  nb<0, DJ, YF, ZF, 1, RM>(P, w[4], w[7], acc);
+  nb<0, DJ, YF, ZF, 2, RM>(P, w[5], w[8], acc);
+  nb<1, DJ, YF, ZF, 0, RM>(P, w[6], w[9], acc);
+  nb<1, DJ, YF, ZF, 1, RM>(P, w[7], w[10], acc);
+  nb<1, DJ, YF, ZF, 2, RM>(P, w[8], w[11], acc);
 }
 
-template <int YF, int ZF, int STRIDE>
+// offs: bit r = the window offset of staged row ty + r
+template <int YF, int ZF, int STRIDE, int RM>
 __device__ __forceinline__ void plane_step(const StencilParams& P, const double* __restrict__ s, int tx, int ty,
                                            int offs, double (&acc)[2][3][3]) {
-  constexpr bool AL = STRIDE == RS;  // the cp.async-staged kernel's rows are 16-byte aligned
-  row_step<-1, YF, ZF, AL>(P, s + (ty + 0) * STRIDE, tx, offs & 1, acc);
-  row_step<0, YF, ZF, AL>(P, s + (ty + 1) * STRIDE, tx, (offs >> 1) & 1, acc);
-  row_step<1, YF, ZF, AL>(P, s + (ty + 2) * STRIDE, tx, (offs >> 2) & 1, acc);
+  row_step<-1, YF, ZF, RM>(P, s + (ty + 0) * STRIDE, tx, offs & 1, acc);
+  row_step<0, YF, ZF, RM>(P, s + (ty + 1) * STRIDE, tx, (offs >> 1) & 1, acc);
+  row_step<1, YF, ZF, RM>(P, s + (ty + 2) * STRIDE, tx, (offs >> 2) & 1, acc);
 }
 
-// offs: bit r = the window offset of staged row ty + r (0 for the cp.async-staged kernel)
-template <int YF, int STRIDE = RS>
+template <int YF, int STRIDE, int RM>
 __device__ __forceinline__ void plane_dispatch(const StencilParams& P, const double* s, int tx, int ty, int zc,
-                                               double (&acc)[2][3][3], int offs = 0) {
-  if (zc == 0) plane_step<YF, 0, STRIDE>(P, s, tx, ty, offs, acc);
-  else if (zc == 1) plane_step<YF, 1, STRIDE>(P, s, tx, ty, offs, acc);
-  else plane_step<YF, 2, STRIDE>(P, s, tx, ty, offs, acc);
+                                               double (&acc)[2][3][3], int offs) {
+  if (zc == 0) plane_step<YF, 0, STRIDE, RM>(P, s, tx, ty, offs, acc);
+  else if (zc == 1) plane_step<YF, 1, STRIDE, RM>(P, s, tx, ty, offs, acc);
+  else plane_step<YF, 2, STRIDE, RM>(P, s, tx, ty, offs, acc);
+}
+
+template <int STRIDE, int RM>
+__device__ __forceinline__ void plane_any(const StencilParams& P, const double* s, int tx, int ty, int yf, int zc,
+                                          double (&acc)[2][3][3], int offs) {
+  if (yf == 0) plane_dispatch<0, STRIDE, RM>(P, s, tx, ty, zc, acc, offs);
+  else if (yf == 1) plane_dispatch<1, STRIDE, RM>(P, s, tx, ty, zc, acc, offs);
+  else plane_dispatch<2, STRIDE, RM>(P, s, tx, ty, zc, acc, offs);
 }
 
 __host__ __device__ __forceinline__ int local_node(int lx, int ly, int lz) {
@@ -261,205 +256,7 @@ struct DotArgs {
   const int* skip;  // CG speculation: the apply is a no-op while *skip != 0
 };
 
-constexpr int RING = 4;  // plane slots: p (computing), p+1 (landed), p+2 (in flight), one spare
-constexpr size_t kMainSmem = sizeof(double) * RING * (TY + 2) * RS + sizeof(uint32_t) * RING * NT * NS;
-
-// DOT: also emit the block partial of x.y (the CG p^T A p).
-template <bool DOT>
-__global__ void __launch_bounds__(NT, kMainBlocksPerSm) k_stencil_main(const __grid_constant__ StencilParams P,
-                                                        const double* __restrict__ x,
-                                                        const uint8_t* __restrict__ info, double* __restrict__ y,
-                                                        int kchunk, int kbeg, int kend, DotArgs dot, int ntx,
-                                                        int nty) {
-  if (dot.skip && *dot.skip) return;
-  double dsum = 0.0;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double (*sm)[TY + 2][RS] = reinterpret_cast<double (*)[TY + 2][RS]>(smem_raw);
-  uint32_t (*sinfo)[NT][NS] =
-      reinterpret_cast<uint32_t (*)[NT][NS]>(smem_raw + sizeof(double) * RING * (TY + 2) * RS);
-  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  const int NX = P.NX, NY = P.NY, NZ = P.NZ;
-  // Segments (tile, plane range k0 .. k1-1). Fixed z chunks (kchunk > 0): grid = (x tiles, y tiles,
-  // chunks), one segment per CTA. Balanced (kchunk == 0): one resident wave, each CTA an equal
-  // contiguous range of tile-major (tile, plane) units; a range crossing a tile boundary restarts
-  // the plane pipeline.
-  const int nzr = kend - kbeg;
-  int64_t u = 0, ue = 1;
-  if (kchunk <= 0) {
-    const int64_t U = (int64_t)ntx * nty * nzr;
-    u = U * blockIdx.x / gridDim.x;
-    ue = U * (blockIdx.x + 1) / gridDim.x;
-  }
-  while (u < ue) {
-  int bx, by, k0, k1;
-  if (kchunk > 0) {
-    bx = blockIdx.x;
-    by = blockIdx.y;
-    k0 = kbeg + blockIdx.z * kchunk;
-    k1 = min(k0 + kchunk, kend);
-    u = ue;
-  } else {
-    const int tile = static_cast<int>(u / nzr), kk = static_cast<int>(u % nzr);
-    const int kl = static_cast<int>(min(static_cast<int64_t>(nzr), kk + (ue - u)));
-    bx = tile % ntx;
-    by = tile / ntx;
-    k0 = kbeg + kk;
-    k1 = kbeg + kl;
-    u += kl - kk;
-  }
-  const int i0 = bx * TXN, j0 = by * TY;
-  const int i = i0 + 2 * tx, j = j0 + ty;
-  const bool active = j < NY;
-  const bool v0 = i < P.NXm, v1 = i + 1 < P.NXm;  // the lane's two nodes exist (ragged last tile)
-  const int yf = j == 0 ? 1 : (j == NY - 1 ? 2 : 0);
-  const int64_t plane = (int64_t)NX * NY;
-
-  // Plane staging with cp.async (LDGSTS): no registers held across the compute; out-of-domain
-  // nodes are zero-filled (src-size 0); Dirichlet masks are applied to the thread's own slots after
-  // the wait, before the block barrier. Slots (warp-row mapping): s0/s1/s2 = row ty, columns lane,
-  // lane+32, lane+64 (< 66); s3 = rows 8-9 spread over the block. The info byte of each slot's node
-  // travels the same way (the aligned 4-byte word holding it, into private shared words).
-  // Plane p lives in ring slot (p + 1) % RING; two planes are in flight while one is computed.
-  const int lane = tx;
-  auto slot = [&](int s, int& r, int& col) -> bool {
-    if (s < 3) {
-      r = ty;
-      col = lane + 32 * s;
-      return col < TXN + 2;
-    }
-    const int q = (s - 3) * NT + static_cast<int>(threadIdx.x);  // halo rows TY, TY+1 over the block
-    r = TY + q / (TXN + 2);
-    col = q % (TXN + 2);
-    return q < 2 * (TXN + 2);
-  };
-  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(&sm[0][0][0]));
-  const uint32_t ibase = static_cast<uint32_t>(__cvta_generic_to_shared(&sinfo[0][threadIdx.x][0]));
-  auto ring = [](int p) { return (p + 1) & (RING - 1); };
-  auto fetch = [&](int p) -> uint32_t {  // returns the slot selector bits needed to land plane p
-    const int buf = ring(p);
-    const bool inplane = p >= 0 && p < NZ;
-    const int64_t pb = plane * (inplane ? p : 0);
-    uint32_t sel = 0;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      int r, col;
-      const bool used = slot(s, r, col);
-      const int ii = i0 - 1 + col, jj = j0 - 1 + r;
-      const bool ok = used && inplane && ii >= 0 && ii < NX && jj >= 0 && jj < NY;
-      const int64_t node = ok ? pb + ii + (int64_t)NX * jj : 0;
-      if (used) {
-        const uint32_t dst = sbase + 8u * static_cast<uint32_t>(buf * (TY + 2) * RS + r * RS + 3 * col);
-        const double* src = x + 3 * node;
-        const int sz = ok ? 8 : 0;
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst + 8u * c), "l"(src + c), "r"(sz)
-                       : "memory");
-      }
-      const uint32_t idst = ibase + 4u * static_cast<uint32_t>(buf * NT * NS + s);
-      const uint8_t* isrc = info + (node & ~int64_t(3));
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(idst), "l"(isrc), "r"(ok ? 4 : 0)
-                   : "memory");
-      sel |= (ok ? static_cast<uint32_t>(node & 3) : 4u) << (4 * s);
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-    return sel;
-  };
-  auto land = [&](int p, uint32_t sel) {  // own copies of plane p are complete: apply own masks
-    const int buf = ring(p);
-    double* sb = &sm[buf][0][0];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const uint32_t b = (sel >> (4 * s)) & 7;
-      if (b >= 4) continue;
-      const uint32_t m = (sinfo[buf][threadIdx.x][s] >> (8 * b)) & 7;
-      if (!m) continue;
-      int r, col;
-      slot(s, r, col);
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-        if ((m >> c) & 1) sb[r * RS + 3 * col + c] = 0.0;
-    }
-  };
-
-  double acc[2][3][3];
-#pragma unroll
-  for (int n = 0; n < 2; ++n)
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) acc[n][r][a] = 0.0;
-  const uint32_t sel0 = fetch(k0 - 1);
-  uint32_t sel1 = fetch(k0);
-  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-  land(k0 - 1, sel0);
-  __syncthreads();
-  for (int p = k0 - 1; p <= k1; ++p) {
-    uint32_t sel2 = 0;
-    if (p + 2 <= k1) sel2 = fetch(p + 2);
-    else asm volatile("cp.async.commit_group;\n" ::: "memory");
-    const int64_t onode = i + (int64_t)NX * (active ? j : 0) + plane * max(p - 1, 0);
-    const uint8_t oi0 = __ldg(&info[onode]), oi1 = __ldg(&info[onode + 1]);
-    double xo[6];  // the finishing nodes' raw inputs (Dirichlet rows; the fused dot), issued early
-    if constexpr (DOT) {
-#pragma unroll
-      for (int a = 0; a < 6; ++a) xo[a] = (a < 3 ? v0 : v1) ? __ldg(&x[3 * onode + a]) : 0.0;
-    }
-    if (active && p >= 0 && p < NZ) {
-      const int zc = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
-      const double* s = &sm[ring(p)][0][0];
-      if (yf == 0) plane_dispatch<0>(P, s, tx, ty, zc, acc);
-      else if (yf == 1) plane_dispatch<1>(P, s, tx, ty, zc, acc);
-      else plane_dispatch<2>(P, s, tx, ty, zc, acc);
-    }
-    if (active && p - 1 >= k0) {  // nodes (i, j, p-1) and (i+1, j, p-1) are complete
-      const double E0 = P.E[oi0 >> 3], E1 = P.E[oi1 >> 3];
-      double* yo = y + 3 * onode;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        if constexpr (DOT) {
-          const double y0 = ((oi0 >> a) & 1) ? xo[a] : E0 * acc[0][0][a];
-          const double y1 = ((oi1 >> a) & 1) ? xo[3 + a] : E1 * acc[1][0][a];
-          if (v0) yo[a] = y0;
-          if (v1) yo[3 + a] = y1;
-          dsum = fma(xo[a], y0, dsum);  // xo = 0 on missing nodes
-          dsum = fma(xo[3 + a], y1, dsum);
-        } else {
-          if (v0) yo[a] = ((oi0 >> a) & 1) ? __ldg(&x[3 * onode + a]) : E0 * acc[0][0][a];
-          if (v1) yo[3 + a] = ((oi1 >> a) & 1) ? __ldg(&x[3 * onode + 3 + a]) : E1 * acc[1][0][a];
-        }
-      }
-    }
-#pragma unroll
-    for (int n = 0; n < 2; ++n)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        acc[n][0][a] = acc[n][1][a];
-        acc[n][1][a] = acc[n][2][a];
-        acc[n][2][a] = 0.0;
-      }
-    if (p < k1) {
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // plane p+1 landed (p+2 may be in flight)
-      land(p + 1, sel1);
-    }
-    __syncthreads();
-    sel1 = sel2;
-  }
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncthreads();
-  }
-  if constexpr (DOT) {
-    const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    const int nb = gridDim.x * gridDim.y * gridDim.z;
-    if (dot.finish) {
-      block_to_slot_and_finish(dsum, dot.part_main, bid, nb, nullptr, 0, dot.counter, dot.out);
-    } else {
-      double a[1] = {dsum};
-      block_reduce<1>(a);
-      if (threadIdx.x == 0) dot.part_main[bid] = a[0];
-    }
-  }
-}
+constexpr int RING = 4;  // plane slots: p (computing), p+1 (landed), p+2 (in flight), p+3 (issued)
 
 // k_stencil_tma: the main kernel with Blackwell bulk-async staging. Per CTA plane the (TY + 2)
 // rows of the 64 + 2 node window (interleaved dofs) and their info bytes arrive by TMA: rank-1
@@ -626,9 +423,7 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
         const int zc = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
         const double* sp = &xs[ring(p)][0][0];
         const int offs = roff(ty, p) | (roff(ty + 1, p) << 1) | (roff(ty + 2, p) << 2);
-        if (yf == 0) plane_dispatch<0, RSP>(P, sp, tx, ty, zc, acc, offs);
-        else if (yf == 1) plane_dispatch<1, RSP>(P, sp, tx, ty, zc, acc, offs);
-        else plane_dispatch<2, RSP>(P, sp, tx, ty, zc, acc, offs);
+        plane_any<RSP, 7>(P, sp, tx, ty, yf, zc, acc, offs);
       }
       if (active && p - 1 >= k0) {  // nodes (i, j, p-1) and (i+1, j, p-1) are complete
         const int so = ring(p - 1);
@@ -1072,18 +867,12 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   // z chunks: one full wave of resident CTAs when tiles allow it
   static bool attrs = false;
   if (!attrs) {
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
-    AFEM_CK(cudaFuncSetAttribute(k_stencil_main<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMainSmem));
     AFEM_CK(cudaFuncSetAttribute(k_stencil_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     AFEM_CK(cudaFuncSetAttribute(k_stencil_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     attrs = true;
   }
-  plan->tma = std::getenv("AFEM_STENCIL_LDGSTS") == nullptr;  // A/B switch: the cp.async-staged kernel
   int occ = 1;
-  if (plan->tma)
-    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_tma<true>, NT, kTmaSmem));
-  else
-    AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_main<true>, NT, kMainSmem));
+  AFEM_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil_tma<true>, NT, kTmaSmem));
   const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
   const int64_t tiles = (int64_t)((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY);
   int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
@@ -1101,7 +890,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   AFEM_CK(cudaMemsetAsync(cnt.p, 0, 8, c.stream));
   launch(c, k_stencil_classify, grid_for(nn, 256, 148 * 32), 256, 0, P.NX, P.NY, P.NZ, P.NXm, s.phase.p, op.mask.p,
          plan->info.p, keys.p, cnt.p);
-  if (plan->tma) {
+  {
     const int ntiles_x = (P.NXm + TXN - 1) / TXN;
     plan->ipx = ((std::max(ntiles_x * TXN + 1, P.NX + 1) + 15) / 16) * 16;  // >= 1 pad byte after each tile
     const int64_t tot = 16 + (int64_t)plan->ipx * P.NY * P.NZ + 128;       // + the last box's overhang
@@ -1280,21 +1069,19 @@ static void stencil_apply_launch(StencilPlan& pl, const MfOp& op, const double* 
   const int ntx = (P.NXm + TXN - 1) / TXN, nty = (P.NY + TY - 1) / TY;
   const int nb_main = P.NXm > 0 ? pl.main_blocks : 0;
   const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main, skip};
-  if (P.NXm > 0 && pl.tma) {  // balanced single wave (kchunk 0)
+  // measurement switch (scripts only): AFEM_STENCIL_ONLY=main|items launches one of the two kernels
+  static const char* only = std::getenv("AFEM_STENCIL_ONLY");
+  const bool run_main = !only || only[0] == 'm', run_items = !only || only[0] == 'i';
+  if (P.NXm > 0 && run_main) {  // balanced single wave (kchunk 0)
     stencil_x_map(pl, x);
     if (dot_out)
-      launch(c, k_stencil_tma<true>, nb_main, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, 0, P.NZ, dot, ntx,
-             nty);
+      launch(c, k_stencil_tma<true>, nb_main, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, 0, P.NZ, dot,
+             ntx, nty);
     else
-      launch(c, k_stencil_tma<false>, nb_main, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, 0, P.NZ, dot, ntx,
-             nty);
-  } else if (P.NXm > 0) {
-    if (dot_out)
-      launch(c, k_stencil_main<true>, nb_main, NT, kMainSmem, P, x, pl.info.p, y, 0, 0, P.NZ, dot, ntx, nty);
-    else
-      launch(c, k_stencil_main<false>, nb_main, NT, kMainSmem, P, x, pl.info.p, y, 0, 0, P.NZ, dot, ntx, nty);
+      launch(c, k_stencil_tma<false>, nb_main, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, 0, P.NZ, dot,
+             ntx, nty);
   }
-  if (pl.n_items > 0) {
+  if (pl.n_items > 0 && run_items) {
     const Items it{pl.it_rec.p, pl.it_zm.p, pl.n_items};
     if (dot_out)
       launch(c, k_stencil_items<true>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p,
@@ -1321,12 +1108,8 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
     const int want = std::max(1, kMainBlocksPerSm * c.num_sms / std::max(tiles, 1));
     const int kc = std::max(4, (ke - kb + want - 1) / want);
     const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TY - 1) / TY, (ke - kb + kc - 1) / kc);
-    if (pl.tma) {
-      stencil_x_map(pl, x);
-      launch(c, k_stencil_tma<false>, grid, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, kc, kb, ke, dot, 0, 0);
-    } else {
-      launch(c, k_stencil_main<false>, grid, NT, kMainSmem, P, x, pl.info.p, y, kc, kb, ke, dot, 0, 0);
-    }
+    stencil_x_map(pl, x);
+    launch(c, k_stencil_tma<false>, grid, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, kc, kb, ke, dot, 0, 0);
   }
   const int64_t i0 = pl.piece_items[pa], i1 = pl.piece_items[pb];
   if (i1 > i0) {

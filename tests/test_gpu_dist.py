@@ -257,6 +257,50 @@ def test_distributed_gmres_bicgstab_match_single_domain(afem, method):
     assert results[0]["rep"]["iterations"] == results[1]["rep"]["iterations"]
 
 
+@pytest.mark.parametrize("method", ["gmres", "bicgstab"])
+def test_distributed_newton_with_gmres_bicgstab_linear_steps(afem, method):
+    """Distributed solve_bvp whose linear solver is GMRES(30) or BiCGStab (run_solver's method
+    dispatch, backend.hpp:241-286, over the slab operator's allreduced inner products): converges
+    with the single-domain Newton's iteration count and displacement."""
+    nh = [(2, 1.0, 0.3), (0, 10.0, 0.3)]
+    nx, ny, nz, size = 6, 6, 8, 2
+    meth = afem.GMRES if method == "gmres" else afem.BICGSTAB
+    ctx = afem.Context(0)
+    fib = afem.fibres(12345, 4)
+    g = afem.System.grid(ctx, 3, nx, ny, nz, inclusions=fib, radius=0.2, materials=nh)
+    g.set_benchmark_dirichlet(STRAIN)
+    ug, rg = g.solve_bvp(operator_kind=afem.MATRIX_FREE, method=meth, lin_rtol=1e-11, lin_max_iter=20000)
+    assert rg["converged"]
+    group = afem.ThreadGroup(size)
+    plane = 3 * (nx + 1) * (ny + 1)
+    results = {}
+
+    def work(rank):
+        try:
+            c = afem.Context(0)
+            s, (z0, z1) = afem.slab_system(c, nx, ny, nz, rank, size, inclusions=fib, radius=0.2, materials=nh)
+            d = afem.Dist(c, rank, size, backend="threads", group=group)
+            d.set_benchmark_dirichlet(s, STRAIN)
+            u, rep = d.solve_bvp(s, operator_kind=afem.MATRIX_FREE, method=meth, lin_rtol=1e-11,
+                                 lin_max_iter=20000)
+            results[rank] = dict(z=(z0, z1), u=u, rep=rep)
+        except Exception as e:  # surfaced below
+            results[rank] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(size)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for r in range(size):
+        assert not isinstance(results[r], Exception), results[r]
+        res = results[r]
+        z0, z1 = res["z"]
+        assert res["rep"]["converged"], res["rep"]["failure"]
+        assert res["rep"]["iterations"] == rg["iterations"]
+        assert rel_err(res["u"], ug[plane * z0: plane * (z1 + 1)]) <= 1e-8
+
+
 @pytest.mark.parametrize("size", [2, 3])
 def test_distributed_newton_assembled_tangent_matches_single_domain(afem, size):
     """Distributed solve_bvp on the assembled tangent (EXPLICIT): every Newton iteration each slab
