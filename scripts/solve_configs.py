@@ -1,0 +1,147 @@
+#!/usr/bin/env python
+"""Configs 3 and 4 solved end to end at their stated sizes on one B200 (VERDICT r01 "next" 2).
+
+  C3  Neo-Hookean hex8 RVE 192^3 (21.6 M dofs): matrix NH E=1 nu=0.3, fibres linear E=10, uniaxial
+      strain 0.05. Newton (solve_bvp, newton.hpp:59-152) with the assembled CSR tangent
+      (EXPLICIT). The named linear solver GMRES(30)+Jacobi is run first on the first Newton system
+      (bounded, its residual history recorded: it stagnates on these 10:1 RVEs, as in the CPU
+      restatement), then the full Newton solve runs with Jacobi-PCG on the symmetric NH tangent.
+  C4  J2 hex8 RVE 256^3 (50.9 M dofs, history 8.6 GB in HBM): matrix J2 (E=1, nu=0.3,
+      sigma_y=0.002, H=0.1), fibres linear E=10; strain ramped to 0.02 in 10 load steps
+      (load_stepping, newton.hpp:163-186) with the J2 history committed after every converged
+      step; matrix-free tangent (cached Gauss-point tangents) + Jacobi-PCG.
+
+Warm start per step: the uniaxial affine predictor (the reference's BC-consistent zero start puts
+the whole applied displacement into the last element layer, strain * N, which inverts elements at
+these sizes). One JSON line per config / per C4 load step is appended to --out as it completes.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2604_22087_b200 as afem  # noqa: E402
+from bench import ClockSampler  # noqa: E402
+
+SEED, N_FIBRES, RADIUS = 12345, 40, 0.05
+
+
+def emit(out, rec):
+    line = json.dumps(rec)
+    print(line, flush=True)
+    if out:
+        with open(out, "a") as f:
+            f.write(line + "\n")
+
+
+def affine(coords, strain):
+    u = np.zeros_like(coords)
+    u[0::3] = strain * coords[0::3]
+    return u
+
+
+def c3(a):
+    n = a.n3
+    mats = [(afem.NEOHOOKE, 1.0, 0.3), (afem.LINEAR, 10.0, 0.3)]
+    ctx = afem.Context(0)
+    t0 = time.perf_counter()
+    s = afem.System.grid(ctx, 3, n, n, n, inclusions=afem.fibres(SEED, N_FIBRES), radius=RADIUS, materials=mats)
+    s.set_benchmark_dirichlet(0.05)
+    coords = s.mesh()[0]
+    x0 = s.impose_dirichlet(affine(coords, 0.05))
+    setup = time.perf_counter() - t0
+    rec = dict(config=3, what="C3 NH 192^3 Newton, assembled CSR tangent", n=n, n_dof=s.n, nnz=s.nnz,
+               setup_s=setup, dtype="f64", data="synthetic")
+    # GMRES(30)+Jacobi on the first Newton system (the config's named solver), bounded
+    vals = afem.Values(s)
+    vals.assemble(x0)
+    r = vals.eliminate(s.residual(x0), x0)  # apply_dirichlet (assembly.hpp:242-249)
+    buf = afem.HandoffBuffer(s)
+    buf.handoff(vals)
+    op = afem.explicit_operator(buf)
+    b = -r
+    t = time.perf_counter()
+    _, rg = afem.run_solver(op, b, method=afem.GMRES, precond=afem.JACOBI, rtol=a.lin_rtol, max_iter=a.gmres_iters,
+                            restart=30)
+    gm_s = time.perf_counter() - t
+    h = rg["residual_history"]
+    rec["gmres30_first_system"] = dict(converged=rg["converged"], iterations=rg["iterations"], time_s=gm_s,
+                                       ms_per_iteration=1e3 * gm_s / max(rg["iterations"], 1),
+                                       rres_every_300=[float(v) for v in h[::300]], final_rres=float(h[-1]),
+                                       failure=rg["failure"])
+    del op, buf, vals
+    torch.cuda.empty_cache()
+    clk = ClockSampler(0, period_ms=1000)
+    clk.start()
+    t = time.perf_counter()
+    u, rep = s.solve_bvp(x0=x0, rtol=a.newton_rtol, lin_rtol=a.lin_rtol, lin_max_iter=200000,
+                         operator_kind=afem.EXPLICIT, method=afem.CG, precond=afem.JACOBI)
+    rec["newton_cg"] = dict(converged=rep["converged"], newton_iterations=rep["iterations"],
+                            linear_iterations=rep["total_linear_iterations"],
+                            residual_norms=[float(v) for v in rep["residual_norms"]], time_s=time.perf_counter() - t,
+                            newton_rtol=a.newton_rtol, lin_rtol=a.lin_rtol, failure=rep["failure"],
+                            clocks=clk.stop())
+    rec["u_max_abs"] = float(np.abs(u).max())
+    emit(a.out, rec)
+
+
+def c4(a):
+    n = a.n4
+    mats = [(afem.J2, 1.0, 0.3, 0.002, 0.1), (afem.LINEAR, 10.0, 0.3)]
+    ctx = afem.Context(0)
+    t0 = time.perf_counter()
+    s = afem.System.grid(ctx, 3, n, n, n, inclusions=afem.fibres(SEED, N_FIBRES), radius=RADIUS, materials=mats)
+    coords = s.mesh()[0]
+    setup = time.perf_counter() - t0
+    steps, total = 10, 0.02
+    u = np.zeros(s.n)
+    head = dict(config=4, what="C4 J2 256^3 load stepping, matrix-free cached tangent + Jacobi-PCG", n=n,
+                n_dof=s.n, history_gb=round(s.history_size() * 8 / 1e9, 2), setup_s=setup, steps=steps,
+                total_strain=total, newton_rtol=a.newton_rtol, lin_rtol=a.lin_rtol, dtype="f64", data="synthetic")
+    emit(a.out, head)
+    t_all = time.perf_counter()
+    ok = True
+    for st in range(1, steps + 1):
+        s.set_benchmark_dirichlet(total * st / steps)
+        clk = ClockSampler(0, period_ms=2000)
+        clk.start()
+        t = time.perf_counter()
+        u, rep = s.solve_bvp(x0=u + affine(coords, total / steps), rtol=a.newton_rtol, lin_rtol=a.lin_rtol,
+                             lin_max_iter=200000, operator_kind=afem.MATRIX_FREE, method=afem.CG,
+                             precond=afem.JACOBI)
+        dt = time.perf_counter() - t
+        if rep["converged"]:
+            s.commit_history(u)
+        emit(a.out, dict(config=4, step=st, strain=total * st / steps, converged=rep["converged"],
+                         newton_iterations=rep["iterations"], linear_iterations=rep["total_linear_iterations"],
+                         time_s=dt, residual_norms=[float(v) for v in rep["residual_norms"]],
+                         failure=rep["failure"], clocks=clk.stop()))
+        if not rep["converged"]:
+            ok = False
+            break
+    emit(a.out, dict(config=4, done=True, converged=ok, total_time_s=time.perf_counter() - t_all,
+                     u_max_abs=float(np.abs(u).max())))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="3,4")
+    ap.add_argument("--n3", type=int, default=192)
+    ap.add_argument("--n4", type=int, default=256)
+    ap.add_argument("--newton-rtol", type=float, default=1e-8)
+    ap.add_argument("--lin-rtol", type=float, default=1e-8)
+    ap.add_argument("--gmres-iters", type=int, default=3000)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    for c in map(int, a.configs.split(",")):
+        (c3 if c == 3 else c4)(a)
+
+
+if __name__ == "__main__":
+    main()
