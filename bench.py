@@ -6,23 +6,27 @@ Workload (BASELINE.json configs[1], "config 2"): 3D linear-elastic hex8 RVE, 128
 benchmark BCs at 1% strain, state u0 = BC-consistent; fp64 matrix-free K(u0) x and Jacobi-PCG.
 
   step      one matrix-free operator apply y = K x over the whole mesh (inputs resident in HBM);
-            L2 is flushed between timed applies, outside the timed events, by streaming a 256 MiB
-            buffer through it (written once, read before every apply, so L2 holds clean lines and
-            the apply does not pay the write-back of the flush)
-  value     whole-job DOFs/s = n_dof * steps * n_gpus / max-over-ranks(sum of apply times)
+            back-to-back applies rotate over several (x, y) pairs whose combined footprint is 4x
+            the L2 (one event pair around all steps), so every apply reads x from HBM and pays
+            the write-back of the y lines earlier applies left dirty in L2
+  value     whole-job DOFs/s = global n_dof * steps / max-over-ranks(time of the K applies)
   e2e       the same metric through the C ABI (afem_op_apply) with pinned HOST x/y buffers:
             H2D of x and D2H of y inside every step
   cg        one Jacobi-PCG solve (rtol 1e-8) of K du = -R(u0) on the device: solve time,
-            iterations, true relative residual
+            iterations, true relative residual; at N > 1 the gathered solution is compared with a
+            1-GPU solve of the same global RVE (cg.check_vs_1gpu)
   roofline  HBM: SURVEY §8(d) algorithmic bytes B_MF = 17 n_dof + 33 n_elem per apply; FP64:
             F_MF = 2 nnz(K) per apply against the live-probed DFMA peak
-  cpu_baseline  the CPU restatement (oracle/, the reference has no hex8) timed on this host's
-            cores on a z-slab sample of the same mesh (min over 3 reps)
+  cpu_baseline  the CPU restatement (oracle/, the reference has no hex8) timed on this host on a
+            z-slab sample of the same mesh: ONE core (the reference's execution model), with the
+            threaded port's all-cores figure beside it; its Jacobi-PCG seconds per iteration
+            (extrapolated to the full solve) and one complete 16^3 solve on CPU and GPU
 
 --impl reference runs the CPU path only (oracle port, all host threads) on the same metric/config.
-Multi-GPU (torchrun, N > 1): weak scaling over z-slabs — the global RVE is 128 x 128 x (128 N)
-elements, each rank owns 128 element layers; every apply adds the shared node planes over NCCL and
-the CG dot products are NCCL allreduces. Time is the max over ranks.
+Multi-GPU (torchrun, N > 1): --scaling weak (default) — the global RVE is 128 x 128 x (128 N)
+elements, each rank owns 128 element layers; --scaling strong — one 128^3 (or --n) RVE split into
+N z-slabs. Every apply adds the shared node planes over NCCL and the CG dot products are NCCL
+allreduces. Time is the max over ranks.
 """
 import argparse
 import json
@@ -55,6 +59,9 @@ def parse():
     p.add_argument("--no-cg", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: n^3 elements per GPU (z-stacked); strong: one n^3 RVE split into z-slabs")
+    p.add_argument("--no-check", action="store_true", help="N>1: skip the 1-GPU re-solve of the global system")
     return p.parse_args()
 
 
@@ -156,6 +163,109 @@ def pick_slab(n, threads, target_s):
     return max(1, min(n, int(target_s / max(t, 1e-6))))
 
 
+def check_vs_one_gpu(afem, ctx, D, sys_, du, rep, n, nz_glob, fib, rank, world, z0, z1, dist):
+    """N > 1: gather the slab-decomposed CG solution on rank 0 and compare it with a 1-GPU Jacobi-PCG
+    solve of the same global RVE (same BCs, rtol 1e-8). Returns the comparison on rank 0."""
+    plane = 3 * (n + 1) ** 2
+    loc = du.cpu().numpy() if hasattr(du, "cpu") else np.asarray(du)
+    parts = [None] * world if rank == 0 else None
+    dist.gather_object((z0, z1, loc), parts, dst=0)
+    if rank != 0:
+        return None
+    xg = np.zeros(plane * (nz_glob + 1))
+    for a, b_, v in parts:
+        xg[plane * a: plane * (b_ + 1)] = v
+    g = afem.System.grid(ctx, 3, n, n, nz_glob, lz=nz_glob / n, inclusions=fib, radius=RADIUS, materials=MATS)
+    g.set_benchmark_dirichlet(STRAIN)
+    ug = g.impose_dirichlet(np.zeros(g.n))
+    opg = afem.matrix_free_operator(g, ug)
+    bg = -g.constrain_residual(g.residual(ug), ug)
+    x1, r1 = afem.run_solver(opg, bg, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=200000)
+    rel = float(np.abs(xg - x1).max() / max(np.abs(x1).max(), 1e-300))
+    return {"rel_diff_u": rel, "tol": 1e-7, "ok": bool(rel <= 1e-7 and r1["converged"]),
+            "iterations_1gpu": r1["iterations"], "iterations_ngpu": rep["iterations"],
+            "note": "both solves stop at true relative residual <= 1e-8; u agrees to ~cond(K) * 1e-8"}
+
+
+def cpu_cg_sample(mesh_arrays, n, nz_s, iters):
+    """The CPU restatement's Jacobi-PCG (krylov.hpp:350-408, single thread) on a z-slab sample:
+    seconds per iteration, from the difference of a 1-iteration and a (1 + iters)-iteration capped
+    solve (cancels the setup: Jacobi diagonal, initial and re-verified residuals)."""
+    from oracle.pyoracle import Oracle
+    orc = Oracle("restate")
+    coords, conn, phase = mesh_arrays
+    s = orc.system(3, coords, conn, phase, MATS, lite=True)
+    node, comp, val = orc.bcs(3, n, n, nz_s, 1.0, STRAIN)
+    s.set_dirichlet(node, comp, val)
+    u = np.zeros(s.n)
+    u[3 * node + comp] = val
+    b = -s.constrain_residual(s.residual(u), u)
+    t = []
+    its = []
+    for k in (1, 1 + iters):
+        t0 = time.perf_counter()
+        _, rep = s.solve(1, u, b, method=0, precond=1, rtol=1e-8, max_iter=k)
+        t.append(time.perf_counter() - t0)
+        its.append(rep["iterations"])
+    return (t[1] - t[0]) / max(its[1] - its[0], 1), its[1] - its[0], s.n
+
+
+def cpu_small_solve(afem, ctx, n):
+    """A complete Jacobi-PCG solve (rtol 1e-8) of the C2 problem at n^3 on the CPU restatement (one
+    thread) and on the GPU: end-to-end solve seconds on both and the solution difference."""
+    from oracle.pyoracle import Oracle
+    fib = afem.fibres(SEED, N_FIBRES)
+    g = afem.System.grid(ctx, 3, n, n, n, inclusions=fib, radius=RADIUS, materials=MATS)
+    g.set_benchmark_dirichlet(STRAIN)
+    ug = g.impose_dirichlet(np.zeros(g.n))
+    b = -g.constrain_residual(g.residual(ug), ug)
+    t0 = time.perf_counter()
+    xg, rg = afem.run_solver(afem.matrix_free_operator(g, ug), b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8,
+                             max_iter=200000)
+    gpu_s = time.perf_counter() - t0
+    orc = Oracle("restate")
+    coords, conn, phase = g.mesh()
+    o = orc.system(3, coords, conn, phase, MATS, lite=True)
+    o.set_dirichlet(*orc.bcs(3, n, n, n, 1.0, STRAIN))
+    t0 = time.perf_counter()
+    xo, ro = o.solve(1, ug, b, method=0, precond=1, rtol=1e-8, max_iter=200000)
+    cpu_s = time.perf_counter() - t0
+    return {"n": n, "n_dof": g.n, "cpu_s": cpu_s, "cpu_iterations": ro["iterations"], "gpu_s": gpu_s,
+            "gpu_iterations": rg["iterations"], "speedup": cpu_s / gpu_s,
+            "rel_diff_u": float(np.abs(xg - xo).max() / max(np.abs(xo).max(), 1e-300)),
+            "gpu_path": "afem.run_solver (host b/x, setup + solve)"}
+
+
+def cpu_baseline(n, sys_, cg):
+    """cpu_baseline: the CPU restatement (oracle/, the reference has no hex8) on this host, ONE core —
+    the reference's execution model; the all-threads figure of the threaded port is
+    reported beside it. CG: seconds per Jacobi-PCG iteration on the same sample, extrapolated to the
+    full mesh and the GPU's iteration count, plus a complete small solve on both sides."""
+    import paper_2604_22087_b200 as afem
+    threads = os.cpu_count() or 1
+    nz1 = pick_slab(n, 1, 4.0)
+    mesh1 = host_mesh_slab(sys_, n, nz1)
+    val1, t1, dofs1 = cpu_sample(n, nz1, 1, 3, mesh_arrays=mesh1)
+    nzt = pick_slab(n, threads, 2.0)
+    valt, tt, dofst = cpu_sample(n, nzt, threads, 3, mesh_arrays=host_mesh_slab(sys_, n, nzt))
+    sec_it, its, _ = cpu_cg_sample(mesh1, n, nz1, 3)
+    cpu_cg = {"sec_per_iteration_sample": sec_it, "sample_iterations": its, "sample_dofs": dofs1,
+              "cores": 1}
+    if cg is not None:
+        full = sec_it * sys_.n / dofs1
+        cpu_cg.update({"extrapolated_sec_per_iteration_full": full,
+                       "extrapolated_solve_s": full * cg["iterations"],
+                       "gpu_solve_s": cg["solve_s"], "gpu_iterations": cg["iterations"],
+                       "note": "CPU seconds/iteration x (full dofs / sample dofs) x the GPU's iteration count"})
+    cpu_cg["small_full_solve"] = cpu_small_solve(afem, sys_.ctx, 16)
+    return {"value": val1, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"z-slab {n}x{n}x{nz1} elements ({dofs1} dofs) of the same mesh, MF apply, one thread, min of 3",
+            "host_cores": threads,
+            "all_threads": {"value": valt, "cores": threads,
+                            "sample": f"z-slab {n}x{n}x{nzt} ({dofst} dofs), threaded port, min of 3"},
+            "cg": cpu_cg}
+
+
 def reference_arm(args, rank, world):
     """--impl reference: the CPU path (oracle port) on this host's cores, rank 0 only."""
     if rank != 0:
@@ -172,13 +282,23 @@ def reference_arm(args, rank, world):
     T = sum(times)
     value = dofs * len(times) / T
     sample = f"z-slab {args.n}x{args.n}x{nz_s} elements ({dofs} dofs) of the {args.n}^3 workload, one MF apply per step"
+    # the CG leg of the metric: the restatement's Jacobi-PCG (single-threaded, like the reference)
+    from oracle.pyoracle import Oracle
+    nz1 = pick_slab(args.n, 1, 1.0)
+    orc = Oracle("restate")
+    mesh1 = orc.mesh3d(args.n, args.n, nz1, orc.fibres(SEED, N_FIBRES), RADIUS, lz=nz1 / args.n)
+    sec_it, its, d1 = cpu_cg_sample(mesh1, args.n, nz1, 3)
+    full_dofs = 3 * (args.n + 1) ** 3
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"C2 hex8 {args.n}^3 linear-elastic fibre RVE, matrix-free K(u0)x (CPU port)",
                    "parallelism": "host threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         "note": "threaded restatement (oracle/restate.hpp); the reference itself is single-threaded"},
+        "cg": {"sec_per_iteration_sample": sec_it, "sample_dofs": d1, "sample_iterations": its, "cores": 1,
+               "extrapolated_sec_per_iteration_full": sec_it * full_dofs / d1},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -205,14 +325,16 @@ def ours(args, rank, world, local_rank):
         uid = [afem.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         D = afem.Dist(ctx, rank, world, backend="nccl", uid=uid[0])
-        sys_, _ = afem.slab_system(ctx, n, n, n * world, rank, world, lz=float(world), inclusions=fib,
-                                   radius=RADIUS, materials=MATS)
+        nz_g = n * world if args.scaling == "weak" else n
+        sys_, (z0, z1) = afem.slab_system(ctx, n, n, nz_g, rank, world, lz=nz_g / n, inclusions=fib,
+                                          radius=RADIUS, materials=MATS)
         D.set_benchmark_dirichlet(sys_, STRAIN, 1.0)
     else:
         sys_ = afem.System.grid(ctx, 3, n, n, n, inclusions=fib, radius=RADIUS, materials=MATS)
         sys_.set_benchmark_dirichlet(STRAIN)
     n_dof, n_elem = sys_.n, sys_.info.n_elem
-    global_dofs = 3 * (n + 1) ** 2 * (n * world + 1)
+    nz_glob = n * world if args.scaling == "weak" else n
+    global_dofs = 3 * (n + 1) ** 2 * (nz_glob + 1)
     u0 = sys_.impose_dirichlet(np.zeros(n_dof))
     op = D.matrix_free_operator(sys_, u0) if D else afem.matrix_free_operator(sys_, u0)
     assert op.uses_stencil, "structured stencil path not selected"
@@ -220,30 +342,37 @@ def ours(args, rank, world, local_rank):
 
     g = torch.Generator(device="cuda").manual_seed(SEED + rank)
     x = torch.rand(n_dof, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
-    y = torch.empty_like(x)
+    # L2 policy: back-to-back applies rotate over R (x, y) pairs whose combined footprint is >= 4x
+    # the 126 MB L2, so every apply streams its x from HBM and pays the write-back of the dirty y
+    # lines earlier applies left in L2 (a read flush between timed applies would evict them outside
+    # the events); one apply moves B_MF > L2 bytes, so the shared element data is re-read as well
+    R = max(2, -(-4 * 126 * 2 ** 20 // (16 * n_dof)))
+    xs_ = [x] + [x.clone() for _ in range(R - 1)]
+    ys_ = [torch.empty_like(x) for _ in range(R)]
     flush = torch.ones(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
     sink = torch.empty((), dtype=torch.float64, device="cuda")
 
-    for _ in range(args.warmup):
-        op.apply_device(x.data_ptr(), y.data_ptr())
+    for k in range(max(args.warmup, R)):
+        op.apply_device(xs_[k % R].data_ptr(), ys_[k % R].data_ptr())
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
     if dist:
         dist.barrier()
+    torch.sum(flush, dim=0, out=sink)  # cold start: nothing of the workload in L2
     torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = ctx.launches
+    e_start.record(stream)
     for k in range(args.steps):
-        torch.sum(flush, dim=0, out=sink)  # read-only L2 flush
-        evs[k][0].record(stream)
-        op.apply_device(x.data_ptr(), y.data_ptr())
-        evs[k][1].record(stream)
+        op.apply_device(xs_[k % R].data_ptr(), ys_[k % R].data_ptr())
+    e_end.record(stream)
     launches = ctx.launches - l0
     torch.cuda.synchronize()
-    ms = [a.elapsed_time(b) for a, b in evs]
-    T = sum(ms)
+    T = e_start.elapsed_time(e_end)
+    y = ys_[(args.steps - 1) % R]
+    del xs_[1:], ys_[:-1]
     if dist:
         t = torch.tensor([T], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -278,7 +407,10 @@ def ours(args, rank, world, local_rank):
             if best is None or solve_s < best[0]:
                 best = (solve_s, rep)
         solve_s, rep = best
-        cg = {"solve_s": solve_s, "iterations": rep["iterations"], "converged": rep["converged"],
+        check = None
+        if D and not args.no_check:
+            check = check_vs_one_gpu(afem, ctx, D, sys_, du, rep, n, nz_glob, fib, rank, world, z0, z1, dist)
+        cg = {"check_vs_1gpu": check,"solve_s": solve_s, "iterations": rep["iterations"], "converged": rep["converged"],
               "true_rel_residual": float(rep["residual_history"][-1]), "rtol": 1e-8, "precond": "jacobi",
               "ms_per_iteration": 1e3 * solve_s / max(rep["iterations"], 1), "best_of": 2,
               "clocks": cg_clk.stop()}
@@ -330,23 +462,23 @@ def ours(args, rank, world, local_rank):
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        nz_s = pick_slab(n, threads, 2.0)
-        val, t, dofs = cpu_sample(n, nz_s, threads, 3, mesh_arrays=host_mesh_slab(sys_, n, nz_s))
-        cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"z-slab {n}x{n}x{nz_s} elements ({dofs} dofs) of the same mesh, MF apply, min of 3"}
+        cpu = cpu_baseline(n, sys_, cg)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t_apply, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": 1e3 * t_apply, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"C2 hex8 {n}^3 linear-elastic fibre RVE, matrix-free K(u0)x + Jacobi-PCG",
                    "elements": n_elem, "n_dof": n_dof, "nnz_K": sys_.nnz, "fibres": N_FIBRES, "radius": RADIUS,
                    "fibre_volume_fraction": vf, "E": [1.0, 10.0], "nu": 0.3, "strain": STRAIN,
-                   "l2": "flushed between timed applies (256 MiB buffer read through L2)",
+                   "l2": (f"inputs larger than L2: {R} rotating (x, y) pairs ({R * 16 * n_dof / 2**20:.0f} MiB), "
+                          "back-to-back applies, one event pair around all steps; B_MF per apply "
+                          f"{(17 * n_dof + 33 * n_elem) / 2**20:.0f} MiB > 126 MB L2"),
+                   "scaling": args.scaling,
                    "global_dofs": global_dofs,
                    "parallelism": (f"z-slab decomposition over {world} GPUs (NCCL plane halo + allreduce), "
-                                   f"{n} element layers per GPU" if world > 1 else "1 GPU")},
+                                   f"{nz_glob // world}-{-(-nz_glob // world)} element layers per GPU"
+                                   if world > 1 else "1 GPU")},
         "cg": cg, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
     }
     print(json.dumps(line), flush=True)

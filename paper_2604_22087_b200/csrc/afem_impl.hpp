@@ -125,6 +125,10 @@ struct Operator {
   // operator sums its owned dofs and allreduces (dist.cu).
   virtual double inner(const double* a, const double* b);
   virtual void inner_dev(const double* a, const double* b, double* out_dev);
+  // first row of the owned range the inner products run over, and the sum of device scalars
+  // across ranks (the fused GMRES passes); a single-domain operator owns every row
+  virtual int64_t dot_begin() const { return 0; }
+  virtual void allreduce_dev(double*, int) {}
   // ||b - A x||; keeps r = b - A x when r is given
   virtual double resid(const double* b, const double* x, double* scratch, double* r);
 };

@@ -50,6 +50,8 @@ struct DistMfOp : Operator {
   double inner(const double* a, const double* b) override;
   void inner_dev(const double* a, const double* b, double* out_dev) override;
   double resid(const double* b, const double* x, double* scratch, double* r) override;
+  int64_t dot_begin() const override { return owned_offset; }
+  void allreduce_dev(double* d, int k) override { comm->allreduce_sum(d, k, sys->ctx->stream); }
   void halo_add(double* v, const double* x_for_mask, bool diag_mode);
   // the received neighbour partials added into v's shared planes (+ unit Dirichlet rows)
   void halo_finish(double* v, const double* x_for_mask, bool diag_mode);

@@ -1,5 +1,9 @@
 // Krylov solvers on the device: Jacobi-preconditioned CG (krylov.hpp:350-408) and restarted,
-// left-preconditioned GMRES(m) with modified Gram-Schmidt (krylov.hpp:415-530).
+// left-preconditioned GMRES(m) (krylov.hpp:415-530). The reference orthogonalises with modified
+// Gram-Schmidt; here each Arnoldi step is CGS2 (classical Gram-Schmidt twice) in three fused
+// kernels — Jacobi + all first-pass inner products, update + all second-pass inner products + the
+// norm, update + normalisation — with one host sync per step (the Givens rotations stay on the
+// host, as in the reference).
 //
 // CG keeps every scalar (rz, pAp, alpha, beta, the residual history) in device memory. One
 // iteration is four launches — operator apply, pAp reduction, the fused x/r/z update with the
@@ -559,6 +563,157 @@ void cg(Operator& op, const SolverCfg& cfg, const double* b, double* x, const do
   }
 }
 
+
+// ---- fused Arnoldi step (GMRES): classical Gram-Schmidt with one re-orthogonalisation (CGS2)
+// in three passes over the basis instead of 2(j+1) modified-Gram-Schmidt kernels. Every pass
+// reads the j+1 basis vectors once and reduces all its inner products in the same launch
+// (per-block partials, then the last block sums them in a fixed order: deterministic).
+constexpr int kGmMax = 32;  // inner products one pass carries (basis vectors + the norm)
+
+// Block sums of acc[0..nv) -> part[k * gridDim.x + block]; the last block to finish writes the
+// fixed-order grid sums to out[0..nv).
+// WithExtra: one more value (extra) in slot nv.
+template <bool WithExtra>
+__device__ __forceinline__ void gm_reduce(const double (&acc)[kGmMax], int nv, double extra, double* part,
+                                          unsigned int* counter, double* out) {
+  __shared__ double sh[kGmMax + 1][kRedThreads / 32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kGmMax; ++k) {
+    if (k < nv) {
+      double t = acc[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) sh[k][w] = t;
+    }
+  }
+  if (WithExtra) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) extra += __shfl_xor_sync(0xffffffffu, extra, o);
+    if (lane == 0) sh[nv][w] = extra;
+    ++nv;
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double t = 0.0;
+    for (int q = 0; q < nw; ++q) t += sh[threadIdx.x][q];
+    part[threadIdx.x * gridDim.x + blockIdx.x] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int k = w; k < nv; k += nw) {  // one warp per inner product, fixed lane assignment
+    double t = 0.0;
+    for (unsigned b = lane; b < gridDim.x; b += 32) t += __ldcg(&part[k * gridDim.x + b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) out[k] = t;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// w = M^-1 src (Jacobi: inv, else src is already preconditioned and w == src); h1[k] = V_k . w
+// over the owned rows [off, n), k < nv.
+__global__ void __launch_bounds__(kRedThreads) k_gm_pass1(const double* __restrict__ src, const double* __restrict__ inv,
+                                                          double* w, const double* __restrict__ V, int64_t ld, int nv,
+                                                          int64_t n, int64_t off, double* part, unsigned int* counter,
+                                                          double* h1) {
+  double acc[kGmMax];
+#pragma unroll
+  for (int k = 0; k < kGmMax; ++k) acc[k] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double wi = src[i];
+    if (inv) {
+      wi *= inv[i];
+      w[i] = wi;
+    }
+    if (i >= off) {
+#pragma unroll
+      for (int k = 0; k < kGmMax; ++k)
+        if (k < nv) acc[k] += __ldcs(&V[k * ld + i]) * wi;
+    }
+  }
+  gm_reduce<false>(acc, nv, 0.0, part, counter, h1);
+}
+
+// a load the compiler may not merge with an earlier one (keeps the first pass's values out of registers)
+__device__ __forceinline__ double gm_reload(const double* p) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// w -= V h1 (in place); out[k] = V_k . w (k < nv), out[nv] = w . w, owned rows.
+__global__ void __launch_bounds__(kRedThreads) k_gm_pass2(double* w, const double* __restrict__ V, int64_t ld, int nv,
+                                                          const double* __restrict__ h1, int64_t n, int64_t off,
+                                                          double* part, unsigned int* counter, double* out) {
+  __shared__ double hs[kGmMax];
+  if (threadIdx.x < nv) hs[threadIdx.x] = h1[threadIdx.x];
+  __syncthreads();
+  double acc[kGmMax], ww = 0.0;
+#pragma unroll
+  for (int k = 0; k < kGmMax; ++k) acc[k] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < kGmMax; ++k)
+      if (k < nv) wi -= hs[k] * V[k * ld + i];
+    w[i] = wi;
+    if (i >= off) {
+#pragma unroll
+      for (int k = 0; k < kGmMax; ++k)
+        if (k < nv) acc[k] += gm_reload(&V[k * ld + i]) * wi;  // second touch: L1/L2
+      ww += wi * wi;
+    }
+  }
+  gm_reduce<true>(acc, nv, ww, part, counter, out);
+}
+
+// h2 = out[0..nv), |w|^2 = out[nv]: hnext = sqrt(|w|^2 - |h2|^2) (w - V h2 is orthogonal to V);
+// hcol = h1 + h2, hcol[nv] = hnext; unless hnext <= happy_tol: vnext = (w - V h2) / hnext.
+__global__ void __launch_bounds__(256) k_gm_pass3(const double* __restrict__ w, double* __restrict__ vnext,
+                                                  const double* __restrict__ V, int64_t ld, int nv,
+                                                  const double* __restrict__ h1, const double* __restrict__ h2n,
+                                                  double happy_tol, double* hcol, int64_t n) {
+  __shared__ double hs[kGmMax];
+  __shared__ double hn;
+  if (threadIdx.x < nv) hs[threadIdx.x] = h2n[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s2 = 0.0;
+    for (int k = 0; k < nv; ++k) s2 += hs[k] * hs[k];
+    hn = sqrt(fmax(h2n[nv] - s2, 0.0));
+    if (blockIdx.x == 0) {
+      for (int k = 0; k < nv; ++k) hcol[k] = h1[k] + hs[k];
+      hcol[nv] = hn;
+    }
+  }
+  __syncthreads();
+  const double d = hn;
+  if (d <= happy_tol) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < kGmMax; ++k)
+      if (k < nv) wi -= hs[k] * __ldcs(&V[k * ld + i]);
+    vnext[i] = wi / d;
+  }
+}
+
+// x += sum_k y_k V_k in the order of the reference's sequential axpys (krylov.hpp:517-519)
+__global__ void k_gm_update_x(double* x, const double* __restrict__ V, int64_t ld, const double* __restrict__ y,
+                              int cols, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = x[i];
+    for (int k = 0; k < cols; ++k) s += y[k] * V[k * ld + i];
+    x[i] = s;
+  }
+}
+
 // The preconditioner of a solve: Jacobi (inverse diagonal, fused into the CG kernels), ILU(0), or none.
 struct Pc {
   const double* inv = nullptr;
@@ -622,6 +777,15 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
   DevArray<double> tmp(n), r(n), w(n), scratch(n), V(static_cast<size_t>(restart + 1) * n);
   DevArray<double> hcol(restart + 2);
   auto vec = [&](int k) { return V.p + static_cast<int64_t>(k) * n; };
+  // fused CGS2 Arnoldi (one pass carries at most kGmMax inner products); AFEM_GMRES_MGS=1 keeps the
+  // reference's modified Gram-Schmidt kernel by kernel (A/B measurements)
+  static const bool force_mgs = std::getenv("AFEM_GMRES_MGS") != nullptr;
+  const bool fused = !force_mgs && restart + 1 <= kGmMax;
+  const unsigned rg = red_grid(n);
+  const int64_t off = op.dot_begin();
+  DevArray<double> part(fused ? static_cast<size_t>(rg) * kGmMax : 0), h1(kGmMax), h2(kGmMax + 1), yd(restart);
+  DevArray<unsigned int> ctr(1);
+  AFEM_CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned int), c.stream));
   const double bnorm = std::sqrt(op.inner(b, b));
   const double denom = bnorm > 0.0 ? bnorm : 1.0;
   pc.apply(c, b, tmp.p, n);
@@ -645,20 +809,36 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
     int j = 0, cols = 0;
     for (; j < restart && rep.iterations < cfg.max_iter; ++j) {
       op.apply(vec(j), tmp.p);
-      pc.apply(c, tmp.p, w.p, n);
-      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, scalars stay on the device
-        op.inner_dev(vec(i), w.p, hcol.p + i);
-        add_scaled_dev(c, hcol.p + i, -1.0, vec(i), w.p, n);
-      }
-      op.inner_dev(w.p, w.p, hcol.p + j + 1);
       std::vector<double> hc(j + 2);
-      AFEM_CK(cudaMemcpyAsync(hc.data(), hcol.p, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-      AFEM_CK(cudaStreamSynchronize(c.stream));
+      double hnext;
+      if (fused) {
+        // CGS2 Arnoldi step: three passes over V, two (allreduced) reductions, one host sync
+        const int nv = j + 1;
+        if (!pc.inv) pc.apply(c, tmp.p, w.p, n);
+        launch(c, k_gm_pass1, rg, kRedThreads, 0, pc.inv ? tmp.p : w.p, pc.inv, w.p, V.p, n, nv, n, off, part.p,
+               ctr.p, h1.p);
+        op.allreduce_dev(h1.p, nv);
+        launch(c, k_gm_pass2, rg, kRedThreads, 0, w.p, V.p, n, nv, h1.p, n, off, part.p, ctr.p, h2.p);
+        op.allreduce_dev(h2.p, nv + 1);
+        launch(c, k_gm_pass3, eg, 256, 0, w.p, vec(j + 1), V.p, n, nv, h1.p, h2.p, beta * 1e-16, hcol.p, n);
+        AFEM_CK(cudaMemcpyAsync(hc.data(), hcol.p, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        AFEM_CK(cudaStreamSynchronize(c.stream));
+        hnext = hc[j + 1];
+      } else {
+        pc.apply(c, tmp.p, w.p, n);
+        for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, scalars stay on the device
+          op.inner_dev(vec(i), w.p, hcol.p + i);
+          add_scaled_dev(c, hcol.p + i, -1.0, vec(i), w.p, n);
+        }
+        op.inner_dev(w.p, w.p, hcol.p + j + 1);
+        AFEM_CK(cudaMemcpyAsync(hc.data(), hcol.p, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        AFEM_CK(cudaStreamSynchronize(c.stream));
+        hnext = std::sqrt(hc[j + 1]);
+      }
       for (int i = 0; i <= j; ++i) H(i, j) = hc[i];
-      const double hnext = std::sqrt(hc[j + 1]);
       H(j + 1, j) = hnext;
       const bool happy = hnext <= beta * 1e-16;
-      if (!happy) launch(c, k_scale_into, eg, 256, 0, w.p, hnext, vec(j + 1), n);
+      if (!happy && !fused) launch(c, k_scale_into, eg, 256, 0, w.p, hnext, vec(j + 1), n);
       for (int i = 0; i < j; ++i) {
         const double t = cs[i] * H(i, j) + sn[i] * H(i + 1, j);
         H(i + 1, j) = -sn[i] * H(i, j) + cs[i] * H(i + 1, j);
@@ -696,7 +876,11 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
       y[i] = s / H(i, i);
     }
     if (!rep.failure.empty()) break;
-    for (int k = 0; k < cols; ++k) axpy(c, y[k], vec(k), x, n);
+    if (cols > 0) {
+      AFEM_CK(cudaMemcpyAsync(yd.p, y.data(), cols * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+      launch(c, k_gm_update_x, eg, 256, 0, x, V.p, n, yd.p, cols, n);
+      AFEM_CK(cudaStreamSynchronize(c.stream));  // y is a host temporary
+    }
     true_rres = op.resid(b, x, tmp.p, r.p) / denom;
   }
   true_rres = op.resid(b, x, scratch.p, nullptr) / denom;

@@ -93,6 +93,8 @@ def c3(a):
 
 def c4(a):
     n = a.n4
+    if a.lin_rtol4 is not None:
+        a.lin_rtol = a.lin_rtol4
     mats = [(afem.J2, 1.0, 0.3, 0.002, 0.1), (afem.LINEAR, 10.0, 0.3)]
     ctx = afem.Context(0)
     t0 = time.perf_counter()
@@ -136,6 +138,8 @@ def main():
     ap.add_argument("--n4", type=int, default=256)
     ap.add_argument("--newton-rtol", type=float, default=1e-8)
     ap.add_argument("--lin-rtol", type=float, default=1e-8)
+    ap.add_argument("--lin-rtol4", type=float, default=None,
+                    help="C4 linear tolerance (inexact Newton; default --lin-rtol)")
     ap.add_argument("--gmres-iters", type=int, default=3000)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
