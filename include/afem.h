@@ -221,6 +221,24 @@ afem_status afem_op_create_explicit(afem_buffer b, afem_op* out);
 /* matrix_free_operator(batches, u, dirichlet) (backend.hpp:222-236): copies u and the constraint
  * mask, assembles the Jacobi diagonal (unit on constrained dofs). */
 afem_status afem_op_create_mf(afem_system sys, const double* u, afem_op* out);
+/* Operator over a caller-supplied CSR pattern (HOST row_ptr n+1 / cols nnz, int32 like the
+ * reference CsrMatrix, sparse.hpp:79-95): the explicit operator of the namespace-adfem drop-in
+ * overlay for patterns that no device system produced. y = A x accumulates each row in column
+ * order with separately rounded multiply/add, bitwise equal to CsrMatrix::apply (sparse.hpp:105-115)
+ * on a non-FMA host build. Values are (re)loaded with afem_op_set_values (host or device, nnz).
+ * Solvable with CG / GMRES / BiCGStab and NONE / JACOBI. */
+afem_status afem_op_create_csr(afem_ctx ctx, int64_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* cols,
+                               afem_op* out);
+afem_status afem_op_set_values(afem_op op, const double* values);
+/* detail::eliminate_dirichlet (assembly.hpp:218-240) on a caller CSR (row_ptr n+1, cols / values
+ * nnz, int32 indices) with a per-dof constraint table (constrained u8, prescribed f64), in place on
+ * values and residual; same operation order and rounding as the reference loop (bitwise). */
+afem_status afem_eliminate_csr(afem_ctx ctx, int64_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* cols,
+                               double* values, double* residual, const uint8_t* constrained,
+                               const double* prescribed, const double* u);
+/* constrain_residual (assembly.hpp:255-260) with a per-dof constraint table, in place. */
+afem_status afem_constrain_masked(afem_ctx ctx, int64_t n, double* residual, const uint8_t* constrained,
+                                  const double* prescribed, const double* u);
 afem_status afem_op_destroy(afem_op op);
 afem_status afem_op_kind(afem_op op, int32_t* kind);
 afem_status afem_op_dim(afem_op op, int64_t* n);
@@ -248,6 +266,11 @@ afem_status afem_solve(afem_op op, const afem_solver_cfg* cfg, const double* b, 
 /* solve_bvp (newton.hpp:59-152) over the system's mesh, materials and Dirichlet table. */
 afem_status afem_solve_bvp(afem_system sys, const afem_newton_cfg* cfg, const double* x0, double* u,
                            afem_newton_report* rep, double* norms, int32_t norms_cap);
+/* solve_bvp with the per-iteration linear SolveReports (NewtonReport::linear_reports,
+ * newton.hpp:38, 120): up to linear_cap reports, residual histories not included. */
+afem_status afem_solve_bvp_ex(afem_system sys, const afem_newton_cfg* cfg, const double* x0, double* u,
+                              afem_newton_report* rep, double* norms, int32_t norms_cap,
+                              afem_solve_report* linear, int32_t linear_cap);
 /* load_stepping (newton.hpp:163-186) for grid systems (benchmark_bcs regenerated per step). */
 afem_status afem_load_stepping(afem_system sys, double total_strain, int32_t n_steps,
                                const afem_newton_cfg* cfg, double* u, int32_t* failed_step,

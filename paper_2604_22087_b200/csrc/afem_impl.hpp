@@ -240,6 +240,15 @@ struct Ilu0 {
 // ---- direct.cu (BandedFactorization, krylov.hpp:196-307): false + failure text on breakdown
 bool direct_solve(System& s, const double* vals, bool chol, const double* b, double* x, std::string& failure);
 
+// ---- csrop.cu (caller-supplied CSR: the drop-in overlay's explicit operator)
+std::unique_ptr<Operator> make_csr_op(Ctx& c, int64_t n, int64_t nnz, const int32_t* h_row_ptr,
+                                      const int32_t* h_cols);
+double* csr_op_values(Operator& o, int64_t* nnz);  // device values of a make_csr_op operator
+void eliminate_csr(Ctx& c, int64_t n, const int32_t* row_ptr, const int32_t* cols, double* values, double* residual,
+                   const uint8_t* constrained, const double* prescribed, const double* u);
+void constrain_masked(Ctx& c, int64_t n, double* residual, const uint8_t* constrained, const double* prescribed,
+                      const double* u);
+
 // ---- stencil.cu
 StencilPlan* make_stencil_plan(System& s, const MfOp& op);  // nullptr when not applicable
 void stencil_apply(StencilPlan& p, const MfOp& op, const double* x, double* y, double* dot_out = nullptr,

@@ -1066,6 +1066,104 @@ afem_status afem_solve_bvp(afem_system sys, const afem_newton_cfg* cfg, const do
   });
 }
 
+afem_status afem_solve_bvp_ex(afem_system sys, const afem_newton_cfg* cfg, const double* x0, double* u,
+                              afem_newton_report* rep, double* norms, int32_t cap, afem_solve_report* linear,
+                              int32_t linear_cap) {
+  return guarded([&] {
+    System& s = SYS(sys);
+    need(cfg, "cfg");
+    need(u, "u");
+    Ctx& c = *s.ctx;
+    Out<double> du(c, u, s.n_dof, false);
+    if (x0) {
+      In<double> dx0(c, x0, s.n_dof);
+      copy(c, dx0.d, du.d, s.n_dof);
+    } else {
+      fill(c, 0.0, du.d, s.n_dof);
+    }
+    NewtonReport r;
+    newton(s, cfg, du.d, r);
+    du.finish();
+    fill_newton(r, rep, norms, cap);
+    if (linear)
+      for (int32_t k = 0; k < linear_cap && k < static_cast<int32_t>(r.linear.size()); ++k)
+        fill_report(r.linear[k], &linear[k], nullptr, 0);
+  });
+}
+
+afem_status afem_op_create_csr(afem_ctx ctx, int64_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* cols,
+                               afem_op* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(row_ptr, "row_ptr");
+    need(out, "out");
+    if (nnz > 0) need(cols, "cols");
+    Ctx& c = begin(ctx->c);
+    if (is_device_ptr(row_ptr) || is_device_ptr(cols))
+      throw std::invalid_argument("afem_op_create_csr: row_ptr / cols must be host arrays");
+    auto h = std::make_unique<afem_op_s>();
+    h->op = make_csr_op(c, n, nnz, row_ptr, cols);
+    *out = h.release();
+  });
+}
+
+afem_status afem_op_set_values(afem_op op, const double* values) {
+  return guarded([&] {
+    need(op, "op");
+    Operator& o = *op->op;
+    int64_t nnz = 0;
+    double* dst = csr_op_values(o, &nnz);
+    Ctx& c = begin(*o.sys->ctx);
+    if (nnz > 0) {
+      need(values, "values");
+      AFEM_CK(cudaMemcpyAsync(dst, values, nnz * sizeof(double), cudaMemcpyDefault, c.stream));
+      AFEM_CK(cudaStreamSynchronize(c.stream));
+    }
+  });
+}
+
+afem_status afem_eliminate_csr(afem_ctx ctx, int64_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* cols,
+                               double* values, double* residual, const uint8_t* constrained,
+                               const double* prescribed, const double* u) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(row_ptr, "row_ptr");
+    need(residual, "residual");
+    need(constrained, "constrained");
+    need(prescribed, "prescribed");
+    need(u, "u");
+    if (nnz > 0) {
+      need(cols, "cols");
+      need(values, "values");
+    }
+    Ctx& c = begin(ctx->c);
+    In<int32_t> drp(c, row_ptr, n + 1), dci(c, cols, nnz);
+    In<uint8_t> dm(c, constrained, n);
+    In<double> dp(c, prescribed, n), du(c, u, n);
+    Out<double> dv(c, values, nnz, true), dr(c, residual, n, true);
+    eliminate_csr(c, n, drp.d, dci.d, dv.d, dr.d, dm.d, dp.d, du.d);
+    dv.finish();
+    dr.finish();
+  });
+}
+
+afem_status afem_constrain_masked(afem_ctx ctx, int64_t n, double* residual, const uint8_t* constrained,
+                                  const double* prescribed, const double* u) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(residual, "residual");
+    need(constrained, "constrained");
+    need(prescribed, "prescribed");
+    need(u, "u");
+    Ctx& c = begin(ctx->c);
+    In<uint8_t> dm(c, constrained, n);
+    In<double> dp(c, prescribed, n), du(c, u, n);
+    Out<double> dr(c, residual, n, true);
+    constrain_masked(c, n, dr.d, dm.d, dp.d, du.d);
+    dr.finish();
+  });
+}
+
 afem_status afem_load_stepping(afem_system sys, double total_strain, int32_t n_steps, const afem_newton_cfg* cfg,
                                double* u, int32_t* failed_step, int32_t* converged, int32_t* step_iterations) {
   return guarded([&] {

@@ -1,0 +1,43 @@
+"""The reference's OWN test suite on the B200 backend.
+
+tests/cpp/build/ref_suite_b200 is proj/tests/test_*.cpp (160 unit tests, compiled in place, never
+copied) built against the namespace-adfem drop-in (include/adfem_dropin shadows adfem/assembly.hpp,
+backend.hpp and newton.hpp): every build_batches -> precompute_sparsity -> assemble_* ->
+apply_dirichlet -> HandoffBuffer -> explicit / matrix-free operator -> run_solver -> solve_bvp call
+the tests make runs on the device through the C ABI. acceptance_b200 is proj/tests/acceptance.cpp
+(C01-C10), C10 driving the reference bench harness (dropin_bench) over the same drop-in.
+The CPU twin (ref_suite_cpu, the unmodified reference with the same gtest / Eigen shims) is checked
+in test_ref_suite_cpu.py.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BUILD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "build")
+
+
+def _run(exe, *args, timeout=1200):
+    path = os.path.join(BUILD, exe)
+    if not os.path.exists(path):
+        pytest.skip(f"{exe} not built (needs the reference tree at build time)")
+    p = subprocess.run([path, *args], capture_output=True, text=True, timeout=timeout)
+    print(p.stdout[-20000:])
+    m = re.search(r"\[==========\] (\d+) tests ran\.\n\[  PASSED  \] (\d+) tests\.", p.stdout)
+    assert m, p.stdout[-4000:] + p.stderr[-4000:]
+    return p, int(m.group(1)), int(m.group(2))
+
+
+def test_reference_unit_suite_on_b200():
+    p, ran, passed = _run("ref_suite_b200")
+    failed = re.findall(r"^\[  FAILED  \] (\S+)$", p.stdout, re.M)
+    assert ran == 160 and passed == ran and p.returncode == 0, f"failed: {failed}"
+
+
+def test_reference_acceptance_on_b200():
+    p, ran, passed = _run("acceptance_b200")
+    failed = re.findall(r"^\[  FAILED  \] (\S+)$", p.stdout, re.M)
+    assert ran == 10 and passed == ran and p.returncode == 0, f"failed: {failed}"
