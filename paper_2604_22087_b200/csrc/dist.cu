@@ -346,7 +346,7 @@ std::unique_ptr<DistMfOp> make_dist_csr_op(System& s, Comm* comm, const double* 
 namespace {
 
 struct DcgDev {
-  double rz, pap, beta, denom, rtol, loc[2];
+  double rz, pap, beta, denom, rtol, loc[2], alpha;
   int it, max_iter, done, fail, conv;
 };
 
@@ -404,13 +404,14 @@ __global__ void k_dcg_pap(const double* p, const double* ap, int64_t n, int64_t 
     if (threadIdx.x == 0) st->pap = v[0];
 }
 
-__global__ void k_dcg_update(double* x, const double* p, double* r, const double* ap, const double* inv, int64_t n,
-                             int64_t off, double* partials, unsigned* counter, DcgDev* st) {
+// r -= alpha Ap and the owned (r.r, r.z); x += alpha p is deferred to k_dcg_p, which reads p anyway
+// (the converging iteration's x update runs once after the loop, k_dcg_x_epilogue)
+__global__ void k_dcg_update(double* r, const double* ap, const double* inv, int64_t n, int64_t off,
+                             double* partials, unsigned* counter, DcgDev* st) {
   if (st->done || !(st->pap > 0.0)) return;
   const double a = st->rz / st->pap;
   double rr = 0.0, rz = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    x[i] += a * p[i];
     const double ri = r[i] - a * ap[i];
     r[i] = ri;
     if (i >= off) {
@@ -423,6 +424,7 @@ __global__ void k_dcg_update(double* x, const double* p, double* r, const double
     if (threadIdx.x == 0) {
       st->loc[0] = v[0];
       st->loc[1] = v[1];
+      st->alpha = a;
     }
 }
 
@@ -431,6 +433,7 @@ __global__ void k_dcg_finish(DcgDev* st, double* hist) {
   if (!(st->pap > 0.0)) {  // krylov.hpp:377-381
     st->fail = 1;
     st->done = 1;
+    st->alpha = 0.0;
     return;
   }
   const int it = st->it + 1;
@@ -447,11 +450,22 @@ __global__ void k_dcg_finish(DcgDev* st, double* hist) {
   }
 }
 
-__global__ void k_dcg_p(const double* r, const double* inv, double* p, int64_t n, const DcgDev* st) {
+// x += alpha p (deferred from k_dcg_update), then p = M r + beta p
+__global__ void k_dcg_p(const double* r, const double* inv, double* p, double* x, int64_t n, const DcgDev* st) {
   if (st->done) return;
-  const double b = st->beta;
+  const double a = st->alpha, b = st->beta;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double pi = p[i];
+    x[i] += a * pi;
+    p[i] = (inv ? r[i] * inv[i] : r[i]) + b * pi;
+  }
+}
+
+// the converging (or last) iteration's deferred x += alpha p (alpha = 0 after a pAp failure)
+__global__ void k_dcg_x_epilogue(double* x, const double* p, int64_t n, const DcgDev* st) {
+  const double a = st->alpha;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = (inv ? r[i] * inv[i] : r[i]) + b * p[i];
+    x[i] += a * p[i];
 }
 
 __global__ void k_inv(const double* d, double* inv, int64_t n, unsigned long long* first_zero) {
@@ -528,16 +542,17 @@ void dist_solve(DistMfOp& op, const SolverCfg& cfg, const double* b, const doubl
           op.apply(p.p, ap.p);
           launch(c, k_dcg_pap, rg, kRedThreads, 0, p.p, ap.p, n, off, c.red_partials.p, c.red_counter.p, st.p);
           op.comm->allreduce_sum(pap, 1, c.stream);
-          launch(c, k_dcg_update, rg, kRedThreads, 0, x, p.p, r.p, ap.p, inv.p, n, off, c.red_partials.p,
-                 c.red_counter.p, st.p);
+          launch(c, k_dcg_update, rg, kRedThreads, 0, r.p, ap.p, inv.p, n, off, c.red_partials.p, c.red_counter.p,
+                 st.p);
           op.comm->allreduce_sum(loc, 2, c.stream);
           launch(c, k_dcg_finish, 1, 1, 0, st.p, hist.p);
-          launch(c, k_dcg_p, eg, 256, 0, r.p, inv.p, p.p, n, st.p);
+          launch(c, k_dcg_p, eg, 256, 0, r.p, inv.p, p.p, x, n, st.p);
         }
         hs = fetch_dev(c, st.p);
         if (hs.done) break;
         chunk = std::min(chunk * 2, 64);
       }
+      launch(c, k_dcg_x_epilogue, eg, 256, 0, x, p.p, n, st.p);
       const int it0 = rep.iterations;
       rep.iterations = hs.it;
       if (hs.it > it0) {
