@@ -78,12 +78,20 @@ struct StencilPlan {
   int kchunk = 16;
   int nchunks = 1;
   int main_blocks = 1;  // balanced main-kernel grid
-  // the plain apply (no fused dot, no skip flag) as an instantiated two-kernel graph, keyed on (x, y)
-  const double* gx = nullptr;
-  double* gy = nullptr;
-  cudaGraphExec_t gexec = nullptr;
+  // the plain apply (no fused dot, no skip flag) as instantiated two-kernel graphs keyed on (x, y):
+  // a pair's graph is captured on its second use (a pointer pair seen once, e.g. one GMRES basis
+  // vector, launches directly) and the kGraphSlots most recent pairs stay instantiated
+  static constexpr int kGraphSlots = 8;
+  struct GraphSlot {
+    const double* x = nullptr;
+    double* y = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t used = 0;
+  } graphs[kGraphSlots];
+  uint64_t graph_clock = 0;
   ~StencilPlan() {
-    if (gexec) cudaGraphExecDestroy(gexec);
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
   }
   // z pieces for the pipelined host-buffer apply (afem_op_apply with host x / y): items are
   // ordered piece-major, piece_items[p] = first item of piece p (multiple of 32)
@@ -256,7 +264,13 @@ struct DotArgs {
   const int* skip;  // CG speculation: the apply is a no-op while *skip != 0
 };
 
-constexpr int RING = 4;  // plane slots: p (computing), p+1 (landed), p+2 (in flight), p+3 (issued)
+// planes per CTA barrier and ring slots (one output plane + PPB computing + PPB landed / in flight). PPB = 2 halves the
+// per-plane __syncthreads of PPB = 1 (barrier stalls were 17 % of the samples, profiles/r02_*).
+#ifndef AFEM_STENCIL_PPB
+#define AFEM_STENCIL_PPB 2
+#endif
+constexpr int PPB = AFEM_STENCIL_PPB;
+constexpr int RING = 2 * PPB + 1;  // + the slot of plane pb - 1, whose nodes are written at step pb
 
 // k_stencil_tma: the main kernel with Blackwell bulk-async staging. Per CTA plane the (TY + 2)
 // rows of the 64 + 2 node window (interleaved dofs) and their info bytes arrive by TMA: rank-1
@@ -313,7 +327,7 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
   }
   __syncthreads();
   uint32_t phase = 0;  // bit s: parity of slot s's next completion
-  auto ring = [](int p) { return (p + 1) & (RING - 1); };
+  auto ring = [](int p) { return (p + 1) % RING; };  // p >= -1
   const int nzr = kend - kbeg;
   int64_t u = 0, ue = 1;
   if (kchunk <= 0) {
@@ -409,61 +423,75 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
       for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int a = 0; a < 3; ++a) acc[n][r][a] = 0.0;
+    // one CTA barrier per PPB planes: planes pb .. pb + PPB - 1 are computed back to back (step p
+    // also writes the nodes of plane p - 1), the next PPB are waited for and masked, then the
+    // barrier frees the slots of planes pb - 1 .. pb + PPB - 2 for the planes 2 PPB ahead
     if (tid == 0) {
       fence_proxy_async_smem();
-      issue(k0 - 1);
-      issue(k0);
-      issue(k0 + 1);  // k1 >= k0 + 1
-    }
-    wait(k0 - 1);
-    mask(k0 - 1);
-    __syncthreads();
-    for (int p = k0 - 1; p <= k1; ++p) {
-      if (active && p >= 0 && p < NZ) {
-        const int zc = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
-        const double* sp = &xs[ring(p)][0][0];
-        const int offs = roff(ty, p) | (roff(ty + 1, p) << 1) | (roff(ty + 2, p) << 2);
-        plane_any<RSP, 7>(P, sp, tx, ty, yf, zc, acc, offs);
-      }
-      if (active && p - 1 >= k0) {  // nodes (i, j, p-1) and (i+1, j, p-1) are complete
-        const int so = ring(p - 1);
-        const uint32_t oi0 = is[so][ty + 1][IOFF + 2 * tx + 1], oi1 = is[so][ty + 1][IOFF + 2 * tx + 2];
-        const double E0 = Es[oi0 >> 3], E1 = Es[oi1 >> 3];
-        const int64_t onode = i + (int64_t)NX * (j + (int64_t)NY * (p - 1));
-        // own nodes' staged inputs (raw x unless constrained)
-        const double* xrow = &xs[so][ty + 1][roff(ty + 1, p - 1) + 3 * (2 * tx + 1)];
-        double* yo = y + 3 * onode;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const bool c0 = (oi0 >> a) & 1, c1 = (oi1 >> a) & 1;
-          const double x0 = c0 ? (v0 ? __ldg(&x[3 * onode + a]) : 0.0) : xrow[a];
-          const double x1 = c1 ? (v1 ? __ldg(&x[3 * onode + 3 + a]) : 0.0) : xrow[3 + a];
-          const double y0 = c0 ? x0 : E0 * acc[0][0][a];
-          const double y1 = c1 ? x1 : E1 * acc[1][0][a];
-          if (v0) yo[a] = y0;
-          if (v1) yo[3 + a] = y1;
-          if constexpr (DOT) {
-            dsum = fma(v0 ? x0 : 0.0, y0, dsum);
-            dsum = fma(v1 ? x1 : 0.0, y1, dsum);
+      for (int q = 0; q < 2 * PPB; ++q)
+        if (k0 - 1 + q <= k1) issue(k0 - 1 + q);
+    }
+#pragma unroll
+    for (int q = 0; q < PPB; ++q)
+      if (k0 - 1 + q <= k1) {
+        wait(k0 - 1 + q);
+        mask(k0 - 1 + q);
+      }
+    __syncthreads();
+    for (int pb = k0 - 1; pb <= k1; pb += PPB) {
+#pragma unroll 1
+      for (int p = pb; p < pb + PPB && p <= k1; ++p) {
+        if (active && p >= 0 && p < NZ) {
+          const int zc = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
+          const double* sp = &xs[ring(p)][0][0];
+          const int offs = roff(ty, p) | (roff(ty + 1, p) << 1) | (roff(ty + 2, p) << 2);
+          plane_any<RSP, 7>(P, sp, tx, ty, yf, zc, acc, offs);
+        }
+        if (active && p - 1 >= k0) {  // nodes (i, j, p-1) and (i+1, j, p-1) are complete
+          const int so = ring(p - 1);
+          const uint32_t oi0 = is[so][ty + 1][IOFF + 2 * tx + 1], oi1 = is[so][ty + 1][IOFF + 2 * tx + 2];
+          const double E0 = Es[oi0 >> 3], E1 = Es[oi1 >> 3];
+          const int64_t onode = i + (int64_t)NX * (j + (int64_t)NY * (p - 1));
+          // own nodes' staged inputs (raw x unless constrained)
+          const double* xrow = &xs[so][ty + 1][roff(ty + 1, p - 1) + 3 * (2 * tx + 1)];
+          double* yo = y + 3 * onode;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const bool c0 = (oi0 >> a) & 1, c1 = (oi1 >> a) & 1;
+            const double x0 = c0 ? (v0 ? __ldg(&x[3 * onode + a]) : 0.0) : xrow[a];
+            const double x1 = c1 ? (v1 ? __ldg(&x[3 * onode + 3 + a]) : 0.0) : xrow[3 + a];
+            const double y0 = c0 ? x0 : E0 * acc[0][0][a];
+            const double y1 = c1 ? x1 : E1 * acc[1][0][a];
+            if (v0) yo[a] = y0;
+            if (v1) yo[3 + a] = y1;
+            if constexpr (DOT) {
+              dsum = fma(v0 ? x0 : 0.0, y0, dsum);
+              dsum = fma(v1 ? x1 : 0.0, y1, dsum);
+            }
           }
         }
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            acc[n][0][a] = acc[n][1][a];
+            acc[n][1][a] = acc[n][2][a];
+            acc[n][2][a] = 0.0;
+          }
       }
 #pragma unroll
-      for (int n = 0; n < 2; ++n)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          acc[n][0][a] = acc[n][1][a];
-          acc[n][1][a] = acc[n][2][a];
-          acc[n][2][a] = 0.0;
+      for (int q = 0; q < PPB; ++q)
+        if (pb + PPB + q <= k1) {
+          wait(pb + PPB + q);
+          mask(pb + PPB + q);
         }
-      if (p < k1) {
-        wait(p + 1);
-        mask(p + 1);
-      }
       __syncthreads();
-      if (tid == 0 && p + 3 <= k1) {
+      if (tid == 0) {
         fence_proxy_async_smem();
-        issue(p + 3);
+#pragma unroll
+        for (int q = 0; q < PPB; ++q)
+          if (pb + 2 * PPB + q <= k1) issue(pb + 2 * PPB + q);  // into the slots of planes pb - 1 + q
       }
     }
   }
@@ -1044,9 +1072,20 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, 
     stencil_apply_launch(pl, op, x, y, dot_out, skip);
     return;
   }
-  if (!pl.gexec || pl.gx != x || pl.gy != y) {  // (re)capture on the context's private stream
-    if (pl.gexec) cudaGraphExecDestroy(pl.gexec);
-    pl.gexec = nullptr;
+  StencilPlan::GraphSlot* slot = nullptr;
+  for (auto& g : pl.graphs)
+    if (g.used && g.x == x && g.y == y) slot = &g;
+  if (!slot) {  // first use of this pair: direct launches, remember the pair (least recently used slot)
+    slot = &pl.graphs[0];
+    for (auto& g : pl.graphs)
+      if (g.used < slot->used) slot = &g;
+    if (slot->exec) cudaGraphExecDestroy(slot->exec);
+    *slot = StencilPlan::GraphSlot{x, y, nullptr, ++pl.graph_clock};
+    stencil_apply_launch(pl, op, x, y, nullptr, nullptr);
+    return;
+  }
+  slot->used = ++pl.graph_clock;
+  if (!slot->exec) {  // second use: capture on the context's private stream
     cudaGraph_t g = nullptr;
     {
       CaptureGuard cap(c);
@@ -1054,11 +1093,9 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, 
       g = cap.end();
     }
     ScopeExit free_graph([&] { cudaGraphDestroy(g); });
-    AFEM_CK(cudaGraphInstantiate(&pl.gexec, g, 0));
-    pl.gx = x;
-    pl.gy = y;
+    AFEM_CK(cudaGraphInstantiate(&slot->exec, g, 0));
   }
-  AFEM_CK(cudaGraphLaunch(pl.gexec, c.stream));
+  AFEM_CK(cudaGraphLaunch(slot->exec, c.stream));
   c.launches += (pl.p.NXm > 0 ? 1 : 0) + (pl.n_items > 0 ? 1 : 0);
 }
 

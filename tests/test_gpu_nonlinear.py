@@ -171,3 +171,68 @@ def test_grid_tangent_slabs_bitwise_and_oracle(afem, ctx, orc, mats, monkeypatch
     for planes in ("1", "2", "3", "5"):
         monkeypatch.setenv("AFEM_JAC_SLAB", planes)
         assert np.array_equal(s.jacobian(u), K)
+
+
+# ---- the stated configs' materials and fibre generator at larger sizes
+C3_MATS = [(2, 1.0, 0.3), (0, 10.0, 0.3)]
+C4_MATS = [(3, 1.0, 0.3, 0.002, 0.1), (0, 10.0, 0.3)]
+
+
+def stated_case(afem, ctx, orc, n, mats, strain):
+    """C2-C5 fibre generator (mt19937_64(12345), 40 fibres, r = 0.05) at n^3."""
+    s = afem.System.grid(ctx, 3, n, n, n, inclusions=afem.fibres(12345, 40), radius=0.05, materials=mats)
+    s.set_benchmark_dirichlet(strain)
+    coords, conn, phase = s.mesh()
+    o = orc.system(3, coords, conn, phase, mats, grid=(n, n, n, 1.0, 1.0, 1.0))
+    o.set_dirichlet(*orc.bcs(3, n, n, n, 1.0, strain))
+    assert 0 < phase.mean() < 1
+    return s, o
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_stated_config_kernels_n32(afem, ctx, orc, cfg):
+    """Residual, tangent, diagonal and matrix-free apply of configs 3 / 4 at 32^3 (107 k dofs, 8.2 M
+    tangent values) against the restatement; C4 from a plastic committed history."""
+    mats = C3_MATS if cfg == "c3" else C4_MATS
+    s, o = stated_case(afem, ctx, orc, 32, mats, 0.05 if cfg == "c3" else 0.02)
+    if cfg == "c4":
+        u0 = s.impose_dirichlet(random_vector(s.n, 0.02, 21))
+        s.commit_history(u0)
+        o.commit_history(u0)
+        assert rel_err(s.history(), o.history()) <= TOL and np.abs(o.history()[6::8]).max() > 0
+    u = s.impose_dirichlet(random_vector(s.n, 0.03, 22))
+    x = random_vector(s.n, 1.0, 23)
+    assert rel_err(s.residual(u), o.residual(u)) <= TOL
+    assert rel_err(s.jacobian(u), o.jacobian(u)) <= TOL
+    assert rel_err(s.diagonal(u), o.diagonal(u)) <= TOL
+    op = afem.matrix_free_operator(s, u)
+    assert rel_err(op.apply(x), o.mf_apply(u, x)) <= TOL
+    assert rel_err(op.diagonal(), o.mf_diagonal(u)) <= TOL
+
+
+def _affine(coords, strain):
+    u = np.zeros_like(coords)
+    u[0::3] = strain * coords[0::3]
+    return u
+
+
+def test_stated_config3_newton_n12(afem, ctx, orc):
+    """C3's solve path (Newton, assembled tangent, CG+Jacobi, affine warm start) at 12^3 with the
+    stated fibre generator: Newton counts equal, u within 1e-8."""
+    s, o = stated_case(afem, ctx, orc, 12, C3_MATS, 0.05)
+    x0 = s.impose_dirichlet(_affine(s.mesh()[0], 0.05))
+    ug, rg = s.solve_bvp(x0=x0, rtol=1e-10, lin_rtol=1e-12, operator_kind=afem.EXPLICIT, method=afem.CG,
+                         precond=afem.JACOBI)
+    uo, ro = o.solve_bvp(x0=x0, rtol=1e-10, lin_rtol=1e-12, operator_kind=0, method=0, precond=1)
+    assert rg["converged"] and ro["converged"] and rg["iterations"] == ro["iterations"] >= 2
+    assert rel_err(ug, uo) <= TOL_U
+
+
+def test_stated_config4_load_path_n12(afem, ctx, orc):
+    """C4's load path (J2, history committed per step, matrix-free cached tangent) at 12^3, 4 steps."""
+    s, o = stated_case(afem, ctx, orc, 12, C4_MATS, 0.02)
+    ug, rg = s.load_stepping(0.02, 4, lin_rtol=1e-12, operator_kind=afem.MATRIX_FREE)
+    uo, ro = o.load_stepping(0.02, 4, lin_rtol=1e-12, operator_kind=1)
+    assert rg["converged"] and ro["converged"]
+    assert list(rg["step_iterations"]) == list(ro["step_iterations"])
+    assert rel_err(ug, uo) <= TOL_U and rel_err(s.history(), o.history()) <= 1e-8
