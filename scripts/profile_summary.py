@@ -52,7 +52,7 @@ keys = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg", "smsp__inst_executed
         "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"]
 summary = {}
 traffic = 0.0
-for kern in ["k_stencil_main", "k_stencil_items"]:
+for kern in ["k_stencil_tma", "k_stencil_main", "k_stencil_items"]:
     raw = page(rep, kern, "raw")
     if len(raw) < 3:
         continue
