@@ -89,6 +89,7 @@ struct Mirror {
 
 inline std::uint64_t batches_key(std::span<const ElementBatch> batches, int n_dof) {
   Fnv f;
+  f.pod(context());  // mirrors are per thread context (a context's stream is not shared across threads)
   f.pod(n_dof);
   f.pod(batches.size());
   for (const ElementBatch& b : batches) {

@@ -43,20 +43,17 @@ inline void check(afem_status s) {
   }
 }
 
-// One device context per host thread (device from AFEM_DEVICE, default 0), created on first use.
+// One device context per host thread (device from AFEM_DEVICE, default 0), created on first use and
+// deliberately never destroyed: device systems cached by the drop-in (assembly.hpp mirrors) may be
+// released by static destructors after the thread's thread_local objects are gone, and they must
+// still find their context (the process exit reclaims it).
 inline afem_ctx context() {
-  struct Holder {
-    afem_ctx h = nullptr;
-    ~Holder() {
-      if (h) afem_ctx_destroy(h);
-    }
-  };
-  static thread_local Holder holder;
-  if (!holder.h) {
+  static thread_local afem_ctx h = nullptr;
+  if (!h) {
     const char* dev = std::getenv("AFEM_DEVICE");
-    check(afem_ctx_create(dev ? std::atoi(dev) : 0, &holder.h));
+    check(afem_ctx_create(dev ? std::atoi(dev) : 0, &h));
   }
-  return holder.h;
+  return h;
 }
 
 // The context is created when the program starts, as a CUDA application initialises its device,

@@ -23,7 +23,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libafem_b200.so")
+# AFEM_LIBRARY: another build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("AFEM_LIBRARY") or os.path.join(HERE, "libafem_b200.so")
 
 LINEAR, SVK = 0, 1                 # MaterialModel (material.hpp:13)
 NEOHOOKE, J2 = 2, 3                # north-star laws beyond the reference (configs 3 and 4)

@@ -534,7 +534,19 @@ __global__ void k_info_pad(const uint8_t* __restrict__ info, uint8_t* __restrict
 // rec: node (low 32 bits, -1 = padding) | oct << 32 | seg << 35 | edge << 39 | pho << 40 |
 // phb << 45 | rem << 50 (items left in the segment, this one included); zm: bit 3b+c = input c of
 // the element's bit corner b ^ rm (the item's reflected frame) is zero (Dirichlet or outside).
-constexpr int kItemThreads = 256;
+// AFEM_ITEMS_PIPE 1: the corner gathers of the next batch are issued before the current batch is
+// computed (register cap 128 for 2 blocks / SM); 0: gathers issued inside each batch.
+#ifndef AFEM_ITEMS_PIPE
+#define AFEM_ITEMS_PIPE 1
+#endif
+#ifndef AFEM_ITEM_THREADS
+#define AFEM_ITEM_THREADS 256
+#endif
+// AFEM_ITEMS_PIPE 2: the round-1 form (loads placed by ptxas next to their uses, 70 registers)
+constexpr bool kItemsPipe = AFEM_ITEMS_PIPE == 1;
+constexpr bool kItemsInline = AFEM_ITEMS_PIPE == 2;
+constexpr int kItemThreads = AFEM_ITEM_THREADS;
+constexpr int kItemMinBlocks = kItemsInline ? 1 : 512 / kItemThreads;
 constexpr uint64_t kPadRec = 0xffffffffull;
 
 struct Items {
@@ -543,8 +555,34 @@ struct Items {
   int64_t n;  // multiple of 32
 };
 
+// The 8 corner gathers of an item (16 loads: a 16-byte-aligned pair + the third component per
+// corner), issued one batch ahead of their use by k_stencil_items (the kernel is latency-bound on
+// them). Pad records (node < 0) and all-zero corners read x[0..2] (a safe address, value unused).
+struct ItemFrame {
+  int node, SX, SY, SZ;
+};
+__device__ __forceinline__ ItemFrame item_frame(uint64_t rec, int NX, int NXY) {
+  const int node = static_cast<int>(static_cast<uint32_t>(rec));
+  const int rm = (static_cast<uint32_t>(rec >> 32) & 7) ^ 7;
+  return ItemFrame{node, (rm & 1) ? -1 : 1, (rm & 2) ? -NX : NX, (rm & 4) ? -NXY : NXY};
+}
+__device__ __forceinline__ int corner_a0(const ItemFrame& f, uint32_t zm, int b) {
+  const int nd = f.node + ((b & 1) ? f.SX : 0) + ((b & 2) ? f.SY : 0) + ((b & 4) ? f.SZ : 0);
+  return (f.node < 0 || ((zm >> (3 * b)) & 7) == 7) ? 0 : 3 * nd;
+}
+__device__ __forceinline__ void item_gather(const double* __restrict__ x, const ItemFrame& f, uint32_t zm,
+                                            double2 (&pr)[8], double (&sg)[8]) {
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const int a0 = corner_a0(f, zm, b);
+    const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);
+    pr[b] = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
+    sg[b] = __ldg(x + (odd ? a0 : a0 + 2));
+  }
+}
+
 template <bool DOT>
-__global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, const __grid_constant__ RowsK0 K0,
+__global__ void __launch_bounds__(kItemThreads, kItemMinBlocks) k_stencil_items(int NX, int NY, const __grid_constant__ RowsK0 K0,
                                                                  const double* __restrict__ Epar,
                                                                  const double* __restrict__ x,
                                                                  const uint8_t* __restrict__ info, Items it,
@@ -560,19 +598,42 @@ __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, 
   const int64_t nb = it.n >> 5;
   const int64_t blo = nb * blockIdx.x / gridDim.x, bhi = nb * (blockIdx.x + 1) / gridDim.x;
   const int NXY = NX * NY;
-  uint64_t nrec = kPadRec;
-  uint32_t nzm = 0;
+  // software pipeline: records two batches ahead, corner gathers one batch ahead
+  uint64_t nrec = kPadRec, nnrec = kPadRec;
+  uint32_t nzm = 0, nnzm = 0;
   if (blo + warp < bhi) {
     nrec = __ldg(&it.rec[(blo + warp) * 32 + lane]);
     nzm = __ldg(&it.zm[(blo + warp) * 32 + lane]);
   }
+  if (blo + warp + nw < bhi) {
+    nnrec = __ldg(&it.rec[(blo + warp + nw) * 32 + lane]);
+    nnzm = __ldg(&it.zm[(blo + warp + nw) * 32 + lane]);
+  }
+  double2 npr[8];
+  double nsg[8];
+  if constexpr (kItemsPipe) item_gather(x, item_frame(nrec, NX, NXY), nzm, npr, nsg);
   for (int64_t bt = blo + warp; bt < bhi; bt += nw) {
     const uint64_t rec = nrec;
     const uint32_t zm = nzm;
-    if (bt + nw < bhi) {  // next batch's record, one batch ahead
-      nrec = __ldg(&it.rec[(bt + nw) * 32 + lane]);
-      nzm = __ldg(&it.zm[(bt + nw) * 32 + lane]);
+    double2 prs[8];
+    double sgs[8];
+    if constexpr (kItemsPipe) {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        prs[b] = npr[b];
+        sgs[b] = nsg[b];
+      }
     }
+    nrec = nnrec;
+    nzm = nnzm;
+    nnrec = kPadRec;
+    nnzm = 0;
+    if (bt + 2 * nw < bhi) {
+      nnrec = __ldg(&it.rec[(bt + 2 * nw) * 32 + lane]);
+      nnzm = __ldg(&it.zm[(bt + 2 * nw) * 32 + lane]);
+    }
+    if constexpr (kItemsPipe) item_gather(x, item_frame(nrec, NX, NXY), nzm, npr, nsg);  // the next batch's corners
+    else if constexpr (!kItemsInline) item_gather(x, item_frame(rec, NX, NXY), zm, prs, sgs);
     const int node = static_cast<int>(static_cast<uint32_t>(rec));
     const uint32_t w = static_cast<uint32_t>(rec >> 32);
     double r0 = 0.0, r1 = 0.0, r2 = 0.0;
@@ -597,14 +658,21 @@ __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, 
       // reflected frame: the node sits at bit corner 0; frame corner b is element corner b ^ rm, and
       // component c of x and row c of y flip sign with bit c of rm
       const double s0 = (rm & 1) ? -1.0 : 1.0, s1 = (rm & 2) ? -1.0 : 1.0, s2 = (rm & 4) ? -1.0 : 1.0;
+      const ItemFrame fr{node, SX, SY, SZ};
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
-        const int nd = node + ((b & 1) ? SX : 0) + ((b & 2) ? SY : 0) + ((b & 4) ? SZ : 0);
         const uint32_t zb = (zm >> (3 * b)) & 7;
-        const int a0 = zb == 7 ? 0 : 3 * nd;  // all-zero corners (outside) read a safe address
-        const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);  // 16 B-aligned pair
-        const double2 pr = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
-        const double sg = __ldg(x + (odd ? a0 : a0 + 2));
+        const int a0 = corner_a0(fr, zm, b);
+        const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);
+        double2 pr;
+        double sg;
+        if constexpr (kItemsInline) {
+          pr = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
+          sg = __ldg(x + (odd ? a0 : a0 + 2));
+        } else {
+          pr = prs[b];
+          sg = sgs[b];
+        }
         const double c0 = (zb & 1) ? 0.0 : s0 * (odd ? sg : pr.x);
         const double c1 = (zb & 2) ? 0.0 : s1 * (odd ? pr.x : pr.y);
         const double c2 = (zb & 4) ? 0.0 : s2 * (odd ? pr.y : sg);

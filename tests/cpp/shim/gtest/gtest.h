@@ -206,6 +206,7 @@ inline int run_all(int argc, char** argv) {
   }
   std::printf("[==========] %d tests ran.\n[  PASSED  ] %d tests.\n", run, run - static_cast<int>(failed.size()));
   for (const auto& f : failed) std::printf("[  FAILED  ] %s\n", f.c_str());
+  std::fflush(stdout);
   return failed.empty() ? 0 : 1;
 }
 
