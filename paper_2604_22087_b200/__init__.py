@@ -235,6 +235,15 @@ def fibres(seed: int, n: int, lx: float = 1.0, ly: float = 1.0) -> np.ndarray:
     return out
 
 
+def _ctx_alive(obj) -> bool:
+    """True unless the Context `obj` depends on (directly, or through its system) is already gone."""
+    ctx = getattr(obj, "ctx", None)
+    if ctx is None:
+        sys_ = getattr(obj, "sys", None)
+        ctx = getattr(sys_, "ctx", None) if sys_ is not None else None
+    return ctx is None or getattr(ctx, "h", None) is not None
+
+
 class Context:
     """One device + one stream. ``stream`` may be a torch.cuda.Stream (or raw cudaStream_t int)."""
 
@@ -307,7 +316,9 @@ class System:
         return cls(ctx, dim, None, None, None, materials, _handle=h)
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
+        # a garbage cycle (e.g. a failed test's traceback) may finalise the Context first: then the
+        # device objects are left to the process exit rather than destroyed against a dead context
+        if getattr(self, "h", None) and _lib is not None and _ctx_alive(self):
             _lib.afem_system_destroy(self.h)
             self.h = None
 
@@ -475,7 +486,7 @@ class Values:
         return out
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
+        if getattr(self, "h", None) and _lib is not None and _ctx_alive(self):
             _lib.afem_values_destroy(self.h)
             self.h = None
 
@@ -523,7 +534,7 @@ class HandoffBuffer:
         return p.value
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
+        if getattr(self, "h", None) and _lib is not None and _ctx_alive(self):
             _lib.afem_buffer_destroy(self.h)
             self.h = None
 
@@ -569,7 +580,7 @@ class LinearOperator:
         return bool(f.value)
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
+        if getattr(self, "h", None) and _lib is not None and _ctx_alive(self):
             _lib.afem_op_destroy(self.h)
             self.h = None
 
@@ -728,7 +739,7 @@ class Dist:
         return out.value
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
+        if getattr(self, "h", None) and _lib is not None and _ctx_alive(self):
             _lib.afem_dist_destroy(self.h)
             self.h = None
 

@@ -616,25 +616,35 @@ __device__ __forceinline__ void gm_reduce(const double (&acc)[kGmMax], int nv, d
   if (threadIdx.x == 0) *counter = 0u;
 }
 
-// w = M^-1 src (Jacobi: inv, else src is already preconditioned and w == src); h1[k] = V_k . w
-// over the owned rows [off, n), k < nv.
+// Step j's basis vector V_{nv-1} arrives unnormalised (pass 3 of the previous step writes
+// w - V h2 and its exact norm s): A V_{nv-1} was applied to it, so w = M^-1 src / s, and V_{nv-1} is
+// normalised in place here (s = 1 for the restart vector). Then h1[k] = V_k . w over the owned rows
+// [off, n), k < nv. Jacobi: inv; else src is already preconditioned and w == src.
 __global__ void __launch_bounds__(kRedThreads) k_gm_pass1(const double* __restrict__ src, const double* __restrict__ inv,
-                                                          double* w, const double* __restrict__ V, int64_t ld, int nv,
+                                                          double* w, double* V, int64_t ld, int nv, double s_last,
                                                           int64_t n, int64_t off, double* part, unsigned int* counter,
                                                           double* h1) {
   double acc[kGmMax];
 #pragma unroll
   for (int k = 0; k < kGmMax; ++k) acc[k] = 0.0;
+  double* vl = V + (nv - 1) * ld;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double wi = src[i];
-    if (inv) {
-      wi *= inv[i];
-      w[i] = wi;
+    if (inv) wi *= inv[i];
+    double vlast = vl[i];
+    if (s_last != 1.0) {
+      wi /= s_last;
+      vlast /= s_last;
+      vl[i] = vlast;
     }
+    if (inv || s_last != 1.0) w[i] = wi;
     if (i >= off) {
 #pragma unroll
+      for (int k = 0; k < kGmMax - 1; ++k)
+        if (k < nv - 1) acc[k] += __ldcs(&V[k * ld + i]) * wi;
+#pragma unroll
       for (int k = 0; k < kGmMax; ++k)
-        if (k < nv) acc[k] += __ldcs(&V[k * ld + i]) * wi;
+        if (k == nv - 1) acc[k] += vlast * wi;
     }
   }
   gm_reduce<false>(acc, nv, 0.0, part, counter, h1);
@@ -647,14 +657,14 @@ __device__ __forceinline__ double gm_reload(const double* p) {
   return v;
 }
 
-// w -= V h1 (in place); out[k] = V_k . w (k < nv), out[nv] = w . w, owned rows.
+// w -= V h1 (in place); h2[k] = V_k . w (k < nv), owned rows.
 __global__ void __launch_bounds__(kRedThreads) k_gm_pass2(double* w, const double* __restrict__ V, int64_t ld, int nv,
                                                           const double* __restrict__ h1, int64_t n, int64_t off,
-                                                          double* part, unsigned int* counter, double* out) {
+                                                          double* part, unsigned int* counter, double* h2) {
   __shared__ double hs[kGmMax];
   if (threadIdx.x < nv) hs[threadIdx.x] = h1[threadIdx.x];
   __syncthreads();
-  double acc[kGmMax], ww = 0.0;
+  double acc[kGmMax];
 #pragma unroll
   for (int k = 0; k < kGmMax; ++k) acc[k] = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -667,41 +677,34 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_pass2(double* w, const doubl
 #pragma unroll
       for (int k = 0; k < kGmMax; ++k)
         if (k < nv) acc[k] += gm_reload(&V[k * ld + i]) * wi;  // second touch: L1/L2
-      ww += wi * wi;
     }
   }
-  gm_reduce<true>(acc, nv, ww, part, counter, out);
+  gm_reduce<false>(acc, nv, 0.0, part, counter, h2);
 }
 
-// h2 = out[0..nv), |w|^2 = out[nv]: hnext = sqrt(|w|^2 - |h2|^2) (w - V h2 is orthogonal to V);
-// hcol = h1 + h2, hcol[nv] = hnext; unless hnext <= happy_tol: vnext = (w - V h2) / hnext.
-__global__ void __launch_bounds__(256) k_gm_pass3(const double* __restrict__ w, double* __restrict__ vnext,
-                                                  const double* __restrict__ V, int64_t ld, int nv,
-                                                  const double* __restrict__ h1, const double* __restrict__ h2n,
-                                                  double happy_tol, double* hcol, int64_t n) {
+// vnext = w - V h2 (left unnormalised: pass 1 of the next step divides by its norm) and
+// vn2[0] = |vnext|^2 over the owned rows, reduced exactly (the H subdiagonal is the true norm of
+// the twice-orthogonalised vector, as in the reference's MGS); block 0 writes hcol = h1 + h2.
+__global__ void __launch_bounds__(kRedThreads) k_gm_pass3(const double* __restrict__ w, double* __restrict__ vnext,
+                                                          const double* __restrict__ V, int64_t ld, int nv,
+                                                          const double* __restrict__ h1, const double* __restrict__ h2,
+                                                          double* hcol, int64_t n, int64_t off, double* part,
+                                                          unsigned int* counter, double* vn2) {
   __shared__ double hs[kGmMax];
-  __shared__ double hn;
-  if (threadIdx.x < nv) hs[threadIdx.x] = h2n[threadIdx.x];
+  if (threadIdx.x < nv) hs[threadIdx.x] = h2[threadIdx.x];
+  if (blockIdx.x == 0 && threadIdx.x < nv) hcol[threadIdx.x] = h1[threadIdx.x] + h2[threadIdx.x];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double s2 = 0.0;
-    for (int k = 0; k < nv; ++k) s2 += hs[k] * hs[k];
-    hn = sqrt(fmax(h2n[nv] - s2, 0.0));
-    if (blockIdx.x == 0) {
-      for (int k = 0; k < nv; ++k) hcol[k] = h1[k] + hs[k];
-      hcol[nv] = hn;
-    }
-  }
-  __syncthreads();
-  const double d = hn;
-  if (d <= happy_tol) return;
+  double acc[kGmMax];
+  acc[0] = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double wi = w[i];
 #pragma unroll
     for (int k = 0; k < kGmMax; ++k)
       if (k < nv) wi -= hs[k] * __ldcs(&V[k * ld + i]);
-    vnext[i] = wi / d;
+    vnext[i] = wi;
+    if (i >= off) acc[0] += wi * wi;
   }
+  gm_reduce<false>(acc, 1, 0.0, part, counter, vn2);
 }
 
 // x += sum_k y_k V_k in the order of the reference's sequential axpys (krylov.hpp:517-519)
@@ -783,7 +786,8 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
   const bool fused = !force_mgs && restart + 1 <= kGmMax;
   const unsigned rg = red_grid(n);
   const int64_t off = op.dot_begin();
-  DevArray<double> part(fused ? static_cast<size_t>(rg) * kGmMax : 0), h1(kGmMax), h2(kGmMax + 1), yd(restart);
+  DevArray<double> part(fused ? static_cast<size_t>(rg) * kGmMax : 0), h1(kGmMax), h2(kGmMax), yd(restart);
+  double s_last = 1.0;  // norm of the unnormalised last basis vector (fused path)
   DevArray<unsigned int> ctr(1);
   AFEM_CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned int), c.stream));
   const double bnorm = std::sqrt(op.inner(b, b));
@@ -812,18 +816,21 @@ void gmres(Operator& op, const SolverCfg& cfg, const double* b, double* x, const
       std::vector<double> hc(j + 2);
       double hnext;
       if (fused) {
-        // CGS2 Arnoldi step: three passes over V, two (allreduced) reductions, one host sync
+        // CGS2 Arnoldi step: three passes over V, allreduced per-pass scalars, one host sync
         const int nv = j + 1;
         if (!pc.inv) pc.apply(c, tmp.p, w.p, n);
-        launch(c, k_gm_pass1, rg, kRedThreads, 0, pc.inv ? tmp.p : w.p, pc.inv, w.p, V.p, n, nv, n, off, part.p,
-               ctr.p, h1.p);
+        launch(c, k_gm_pass1, rg, kRedThreads, 0, pc.inv ? tmp.p : w.p, pc.inv, w.p, V.p, n, nv,
+               j == 0 ? 1.0 : s_last, n, off, part.p, ctr.p, h1.p);
         op.allreduce_dev(h1.p, nv);
         launch(c, k_gm_pass2, rg, kRedThreads, 0, w.p, V.p, n, nv, h1.p, n, off, part.p, ctr.p, h2.p);
-        op.allreduce_dev(h2.p, nv + 1);
-        launch(c, k_gm_pass3, eg, 256, 0, w.p, vec(j + 1), V.p, n, nv, h1.p, h2.p, beta * 1e-16, hcol.p, n);
+        op.allreduce_dev(h2.p, nv);
+        launch(c, k_gm_pass3, rg, kRedThreads, 0, w.p, vec(j + 1), V.p, n, nv, h1.p, h2.p, hcol.p, n, off, part.p,
+               ctr.p, hcol.p + nv);
+        op.allreduce_dev(hcol.p + nv, 1);
         AFEM_CK(cudaMemcpyAsync(hc.data(), hcol.p, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
         AFEM_CK(cudaStreamSynchronize(c.stream));
-        hnext = hc[j + 1];
+        hnext = std::sqrt(hc[j + 1]);
+        s_last = hnext;
       } else {
         pc.apply(c, tmp.p, w.p, n);
         for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, scalars stay on the device

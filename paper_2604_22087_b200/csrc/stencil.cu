@@ -264,13 +264,15 @@ struct DotArgs {
   const int* skip;  // CG speculation: the apply is a no-op while *skip != 0
 };
 
-// planes per CTA barrier and ring slots (one output plane + PPB computing + PPB landed / in flight). PPB = 2 halves the
-// per-plane __syncthreads of PPB = 1 (barrier stalls were 17 % of the samples, profiles/r02_*).
+// Planes per CTA barrier (PPB) and ring slots: the output plane pb - 1, PPB computing, and the
+// landed / in-flight planes (2 for PPB = 1, PPB otherwise). PPB = 2 halves the barriers but was
+// measured slower (ncu 53.2 -> 56.8 us, profiles/r02_*): the barrier stall is the warps' skew, not
+// the barrier count.
 #ifndef AFEM_STENCIL_PPB
-#define AFEM_STENCIL_PPB 2
+#define AFEM_STENCIL_PPB 1
 #endif
 constexpr int PPB = AFEM_STENCIL_PPB;
-constexpr int RING = 2 * PPB + 1;  // + the slot of plane pb - 1, whose nodes are written at step pb
+constexpr int RING = 2 * PPB + (PPB == 1 ? 2 : 1);
 
 // k_stencil_tma: the main kernel with Blackwell bulk-async staging. Per CTA plane the (TY + 2)
 // rows of the 64 + 2 node window (interleaved dofs) and their info bytes arrive by TMA: rank-1
@@ -370,19 +372,26 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
       for (int q = tid; q < RING * RSP; q += NT) xs[q / RSP][r][q % RSP] = 0.0;
     }
     __syncthreads();
-    auto issue = [&](int p) {  // one thread: plane p into its slot
+    // plane p into its slot, issued by lane 0 of every warp (warp w copies rows w, w + TY, ...; warp
+    // 0 also posts the expected bytes — a copy may complete first, the phase still needs that
+    // arrival), so no single warp carries the issue work into the next barrier
+    auto issue = [&](int p) {
+      if ((tid & 31) != 0) return;
+      const int w = tid >> 5;
       const int sl = ring(p);
       const uint32_t bar = smem_u32(&bars[sl]);
+      fence_proxy_async_smem();  // this thread's view of the slot's generic writes before the overwrite
       if (p < 0 || p >= NZ) {
-        mbar_arrive(bar);
+        if (w == 0) mbar_arrive(bar);
         return;
       }
-      int rows = 0;
+      if (w == 0) {
+        int rows = 0;
 #pragma unroll
-      for (int r = 0; r < TY + 2; ++r) rows += (j0 - 1 + r >= 0 && j0 - 1 + r < NY) ? 1 : 0;
-      mbar_arrive_expect_tx(bar, static_cast<uint32_t>(rows * (XBOX * 8 + IBOX)));
-#pragma unroll
-      for (int r = 0; r < TY + 2; ++r) {
+        for (int r = 0; r < TY + 2; ++r) rows += (j0 - 1 + r >= 0 && j0 - 1 + r < NY) ? 1 : 0;
+        mbar_arrive_expect_tx(bar, static_cast<uint32_t>(rows * (XBOX * 8 + IBOX)));
+      }
+      for (int r = w; r < TY + 2; r += TY) {
         const int jj = j0 - 1 + r;
         if (jj < 0 || jj >= NY) continue;
         const int row = jj + NY * p;
@@ -425,13 +434,10 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
         for (int a = 0; a < 3; ++a) acc[n][r][a] = 0.0;
     // one CTA barrier per PPB planes: planes pb .. pb + PPB - 1 are computed back to back (step p
     // also writes the nodes of plane p - 1), the next PPB are waited for and masked, then the
-    // barrier frees the slots of planes pb - 1 .. pb + PPB - 2 for the planes 2 PPB ahead
-    if (tid == 0) {
-      fence_proxy_async_smem();
+    // barrier frees the slots of planes pb - 1 .. pb + PPB - 2 for the planes RING - 1 ahead
 #pragma unroll
-      for (int q = 0; q < 2 * PPB; ++q)
-        if (k0 - 1 + q <= k1) issue(k0 - 1 + q);
-    }
+    for (int q = 0; q < RING - 1; ++q)
+      if (k0 - 1 + q <= k1) issue(k0 - 1 + q);
 #pragma unroll
     for (int q = 0; q < PPB; ++q)
       if (k0 - 1 + q <= k1) {
@@ -487,12 +493,9 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
           mask(pb + PPB + q);
         }
       __syncthreads();
-      if (tid == 0) {
-        fence_proxy_async_smem();
 #pragma unroll
-        for (int q = 0; q < PPB; ++q)
-          if (pb + 2 * PPB + q <= k1) issue(pb + 2 * PPB + q);  // into the slots of planes pb - 1 + q
-      }
+      for (int q = 0; q < PPB; ++q)
+        if (pb + RING - 1 + q <= k1) issue(pb + RING - 1 + q);  // into the slots of planes pb - 1 + q
     }
   }
   if constexpr (DOT) {
@@ -534,19 +537,7 @@ __global__ void k_info_pad(const uint8_t* __restrict__ info, uint8_t* __restrict
 // rec: node (low 32 bits, -1 = padding) | oct << 32 | seg << 35 | edge << 39 | pho << 40 |
 // phb << 45 | rem << 50 (items left in the segment, this one included); zm: bit 3b+c = input c of
 // the element's bit corner b ^ rm (the item's reflected frame) is zero (Dirichlet or outside).
-// AFEM_ITEMS_PIPE 1: the corner gathers of the next batch are issued before the current batch is
-// computed (register cap 128 for 2 blocks / SM); 0: gathers issued inside each batch.
-#ifndef AFEM_ITEMS_PIPE
-#define AFEM_ITEMS_PIPE 1
-#endif
-#ifndef AFEM_ITEM_THREADS
-#define AFEM_ITEM_THREADS 256
-#endif
-// AFEM_ITEMS_PIPE 2: the round-1 form (loads placed by ptxas next to their uses, 70 registers)
-constexpr bool kItemsPipe = AFEM_ITEMS_PIPE == 1;
-constexpr bool kItemsInline = AFEM_ITEMS_PIPE == 2;
-constexpr int kItemThreads = AFEM_ITEM_THREADS;
-constexpr int kItemMinBlocks = kItemsInline ? 1 : 512 / kItemThreads;
+constexpr int kItemThreads = 256;
 constexpr uint64_t kPadRec = 0xffffffffull;
 
 struct Items {
@@ -555,34 +546,8 @@ struct Items {
   int64_t n;  // multiple of 32
 };
 
-// The 8 corner gathers of an item (16 loads: a 16-byte-aligned pair + the third component per
-// corner), issued one batch ahead of their use by k_stencil_items (the kernel is latency-bound on
-// them). Pad records (node < 0) and all-zero corners read x[0..2] (a safe address, value unused).
-struct ItemFrame {
-  int node, SX, SY, SZ;
-};
-__device__ __forceinline__ ItemFrame item_frame(uint64_t rec, int NX, int NXY) {
-  const int node = static_cast<int>(static_cast<uint32_t>(rec));
-  const int rm = (static_cast<uint32_t>(rec >> 32) & 7) ^ 7;
-  return ItemFrame{node, (rm & 1) ? -1 : 1, (rm & 2) ? -NX : NX, (rm & 4) ? -NXY : NXY};
-}
-__device__ __forceinline__ int corner_a0(const ItemFrame& f, uint32_t zm, int b) {
-  const int nd = f.node + ((b & 1) ? f.SX : 0) + ((b & 2) ? f.SY : 0) + ((b & 4) ? f.SZ : 0);
-  return (f.node < 0 || ((zm >> (3 * b)) & 7) == 7) ? 0 : 3 * nd;
-}
-__device__ __forceinline__ void item_gather(const double* __restrict__ x, const ItemFrame& f, uint32_t zm,
-                                            double2 (&pr)[8], double (&sg)[8]) {
-#pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    const int a0 = corner_a0(f, zm, b);
-    const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);
-    pr[b] = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
-    sg[b] = __ldg(x + (odd ? a0 : a0 + 2));
-  }
-}
-
 template <bool DOT>
-__global__ void __launch_bounds__(kItemThreads, kItemMinBlocks) k_stencil_items(int NX, int NY, const __grid_constant__ RowsK0 K0,
+__global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, const __grid_constant__ RowsK0 K0,
                                                                  const double* __restrict__ Epar,
                                                                  const double* __restrict__ x,
                                                                  const uint8_t* __restrict__ info, Items it,
@@ -598,42 +563,19 @@ __global__ void __launch_bounds__(kItemThreads, kItemMinBlocks) k_stencil_items(
   const int64_t nb = it.n >> 5;
   const int64_t blo = nb * blockIdx.x / gridDim.x, bhi = nb * (blockIdx.x + 1) / gridDim.x;
   const int NXY = NX * NY;
-  // software pipeline: records two batches ahead, corner gathers one batch ahead
-  uint64_t nrec = kPadRec, nnrec = kPadRec;
-  uint32_t nzm = 0, nnzm = 0;
+  uint64_t nrec = kPadRec;
+  uint32_t nzm = 0;
   if (blo + warp < bhi) {
     nrec = __ldg(&it.rec[(blo + warp) * 32 + lane]);
     nzm = __ldg(&it.zm[(blo + warp) * 32 + lane]);
   }
-  if (blo + warp + nw < bhi) {
-    nnrec = __ldg(&it.rec[(blo + warp + nw) * 32 + lane]);
-    nnzm = __ldg(&it.zm[(blo + warp + nw) * 32 + lane]);
-  }
-  double2 npr[8];
-  double nsg[8];
-  if constexpr (kItemsPipe) item_gather(x, item_frame(nrec, NX, NXY), nzm, npr, nsg);
   for (int64_t bt = blo + warp; bt < bhi; bt += nw) {
     const uint64_t rec = nrec;
     const uint32_t zm = nzm;
-    double2 prs[8];
-    double sgs[8];
-    if constexpr (kItemsPipe) {
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        prs[b] = npr[b];
-        sgs[b] = nsg[b];
-      }
+    if (bt + nw < bhi) {  // next batch's record, one batch ahead
+      nrec = __ldg(&it.rec[(bt + nw) * 32 + lane]);
+      nzm = __ldg(&it.zm[(bt + nw) * 32 + lane]);
     }
-    nrec = nnrec;
-    nzm = nnzm;
-    nnrec = kPadRec;
-    nnzm = 0;
-    if (bt + 2 * nw < bhi) {
-      nnrec = __ldg(&it.rec[(bt + 2 * nw) * 32 + lane]);
-      nnzm = __ldg(&it.zm[(bt + 2 * nw) * 32 + lane]);
-    }
-    if constexpr (kItemsPipe) item_gather(x, item_frame(nrec, NX, NXY), nzm, npr, nsg);  // the next batch's corners
-    else if constexpr (!kItemsInline) item_gather(x, item_frame(rec, NX, NXY), zm, prs, sgs);
     const int node = static_cast<int>(static_cast<uint32_t>(rec));
     const uint32_t w = static_cast<uint32_t>(rec >> 32);
     double r0 = 0.0, r1 = 0.0, r2 = 0.0;
@@ -658,21 +600,14 @@ __global__ void __launch_bounds__(kItemThreads, kItemMinBlocks) k_stencil_items(
       // reflected frame: the node sits at bit corner 0; frame corner b is element corner b ^ rm, and
       // component c of x and row c of y flip sign with bit c of rm
       const double s0 = (rm & 1) ? -1.0 : 1.0, s1 = (rm & 2) ? -1.0 : 1.0, s2 = (rm & 4) ? -1.0 : 1.0;
-      const ItemFrame fr{node, SX, SY, SZ};
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
+        const int nd = node + ((b & 1) ? SX : 0) + ((b & 2) ? SY : 0) + ((b & 4) ? SZ : 0);
         const uint32_t zb = (zm >> (3 * b)) & 7;
-        const int a0 = corner_a0(fr, zm, b);
-        const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);
-        double2 pr;
-        double sg;
-        if constexpr (kItemsInline) {
-          pr = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
-          sg = __ldg(x + (odd ? a0 : a0 + 2));
-        } else {
-          pr = prs[b];
-          sg = sgs[b];
-        }
+        const int a0 = zb == 7 ? 0 : 3 * nd;  // all-zero corners (outside) read a safe address
+        const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);  // 16 B-aligned pair
+        const double2 pr = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
+        const double sg = __ldg(x + (odd ? a0 : a0 + 2));
         const double c0 = (zb & 1) ? 0.0 : s0 * (odd ? sg : pr.x);
         const double c1 = (zb & 2) ? 0.0 : s1 * (odd ? pr.x : pr.y);
         const double c2 = (zb & 4) ? 0.0 : s2 * (odd ? pr.y : sg);
