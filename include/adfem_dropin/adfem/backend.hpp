@@ -4,8 +4,9 @@
 //   HandoffBuffer / LeaseGuard   (backend.hpp:33-111) host value store with the lease + epoch
 //                                protocol (the values are the reference's std::vector, moved in)
 //   LinearOperator               (backend.hpp:117-194) EXPLICIT: a device CSR operator whose values
-//                                are refreshed from the leased store on every use (so writes
-//                                through solver_values() are seen, backend.hpp test WriteThrough);
+//                                are re-uploaded from the leased store whenever it may have been
+//                                written (a handoff or a mutable view handed out: writes through
+//                                solver_values() are seen, backend test WriteThrough);
 //                                its SpMV is bitwise equal to CsrMatrix::apply. MATRIX_FREE: the
 //                                device matrix-free operator of the batches' mirror (state u and
 //                                the constraint mask copied at creation, backend.hpp:222-236)
@@ -62,6 +63,7 @@ class HandoffBuffer {
     *store_ = std::move(coo.values);
     state_ = LeaseState::LeasedToSolver;
     ++epoch_;
+    ++version_;
     if (trace_) *trace_ << "lease handoff epoch=" << epoch_ << "\n";
   }
 
@@ -74,21 +76,31 @@ class HandoffBuffer {
   std::span<double> assembly_values() {
     if (state_ != LeaseState::OwnedByAssembly)
       throw LeaseError("assembly-side access while the buffer is leased to the solver");
+    ++version_;
     return {store_->data(), store_->size()};
   }
 
   std::span<double> solver_values() {
     if (state_ != LeaseState::LeasedToSolver) throw LeaseError("solver-side access without an active lease");
+    ++version_;
     return {store_->data(), store_->size()};
   }
 
-  std::shared_ptr<std::vector<double>> value_store() const { return store_; }
+  std::shared_ptr<std::vector<double>> value_store() const {
+    ++version_;
+    return store_;
+  }
+
+  /// B200: bumped whenever the values may have been (re)written — a handoff or a mutable view
+  /// handed out — so the explicit operator re-uploads its device copy only then.
+  std::uint64_t values_version() const { return version_; }
 
  private:
   std::shared_ptr<const SparsityPattern> pattern_;
   std::shared_ptr<std::vector<double>> store_;
   LeaseState state_ = LeaseState::OwnedByAssembly;
   std::uint64_t epoch_ = 0;
+  mutable std::uint64_t version_ = 0;
   std::ostream* trace_ = nullptr;
 };
 
@@ -156,8 +168,13 @@ class LinearOperator {
       throw LeaseError("explicit operator used while the buffer lease is not held");
     if (buffer_->epoch() != epoch_) throw StaleEpochError("explicit operator built from a stale assembly epoch");
   }
-  // the solver-side storage may have been written since the last use: reload it
-  void sync_values() const { b200_dropin::check(afem_op_set_values(dev_->h, csr_.values().data())); }
+  // the solver-side storage may have been written since the last upload: reload it then
+  void sync_values() const {
+    const std::uint64_t v = buffer_->values_version();
+    if (synced_ == v) return;
+    b200_dropin::check(afem_op_set_values(dev_->h, csr_.values().data()));
+    synced_ = v;
+  }
 
   OperatorKind kind_ = OperatorKind::EXPLICIT;
   int n_ = 0;
@@ -166,6 +183,7 @@ class LinearOperator {
   CsrMatrix csr_;
   const HandoffBuffer* buffer_ = nullptr;
   std::uint64_t epoch_ = 0;
+  mutable std::uint64_t synced_ = ~0ull;  // values_version() of the device copy
   // matrix-free realization: the mirror keeps the device system alive
   std::shared_ptr<b200_dropin::Mirror> mirror_;
 };

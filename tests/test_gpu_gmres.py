@@ -73,7 +73,8 @@ def test_fused_cgs2_matches_mgs_and_oracle():
     restatement's MGS iteration count (within 2) and first-cycle residual history; across many
     restarts (10x8x6, rtol 1e-10,
     ~1500 iterations) restarted GMRES amplifies rounding differences, so there the solutions are compared
-    (1e-8) and the iteration counts only bounded (numpy, same matrix: MGS 1560, CGS2 1530 iterations)."""
+    (1e-6 = cond(K) x rtol) and the iteration counts only bounded (numpy, same matrix: MGS 1560, CGS2
+    1530 iterations)."""
     import paper_2604_22087_b200 as afem
     fused, mgs = _run(False), _run(True)
     orc = Oracle("restate")
@@ -90,7 +91,8 @@ def test_fused_cgs2_matches_mgs_and_oracle():
                 assert np.abs(h - ro["residual_history"][: len(h)]).max() <= 1e-8
             else:
                 assert f["it"] <= 1.3 * ro["iterations"] and m["it"] <= 1.3 * ro["iterations"]
-            tol = 1e-8 if nx == 10 else 1e-4
+            # equal solver tolerance: both solutions are within cond(K) * rtol of the exact one
+            tol = 1e-6 if nx == 10 else 1e-4
             assert rel_err(np.array(f["x"]), xo) <= tol and rel_err(np.array(m["x"]), xo) <= tol
 
 
