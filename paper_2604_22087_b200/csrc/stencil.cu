@@ -116,7 +116,7 @@ namespace {
 #define AFEM_STENCIL_TY 4
 #endif
 constexpr int TX = 32, TXN = 2 * TX, TY = AFEM_STENCIL_TY, NT = TX * TY;
-constexpr int kMainBlocksPerSm = 16 / TY;
+constexpr int kMainBlocksPerSm = TY == 4 ? 5 : 16 / TY;  // 5: TMA staging left the main loop at <= 102 registers
 
 // Structural zero of a family's entry (a, b) at offset d: the brick's reflection symmetry about
 // an axis c that the family keeps intact makes every off-diagonal entry involving c vanish when
@@ -198,10 +198,34 @@ __device__ __forceinline__ void nb(const StencilParams& P, double x0, double x1,
 // right neighbour): 12 LDS.64 at the row's offset (TMA boxes start on 16-byte boundaries, so a row
 // lands 0 or 1 double in). 48-byte lane stride: two-way conflicts per half-warp, the same shared
 // wavefronts as 16-byte loads of an aligned row, and no per-row code variants.
+#ifndef AFEM_STENCIL_LDS128
+#define AFEM_STENCIL_LDS128 0
+#endif
 __device__ __forceinline__ void load_window(const double* __restrict__ srow, int tx, int off, double (&w)[12]) {
+#if AFEM_STENCIL_LDS128
+  // 16-byte loads (half the shared wavefronts of 8-byte loads at this 48-byte lane stride): the row
+  // base and 6 tx doubles are 16-byte aligned, so offset 0 is 6 aligned pairs and offset 1 is 7
+  // pairs shifted by one element (warp-uniform branch)
+  const double2* r2 = reinterpret_cast<const double2*>(srow + 6 * tx);
+  if (off == 0) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const double2 v = r2[k];
+      w[2 * k] = v.x;
+      w[2 * k + 1] = v.y;
+    }
+  } else {
+    double2 v[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) v[k] = r2[k];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) w[k] = ((k + 1) & 1) ? v[(k + 1) >> 1].y : v[(k + 1) >> 1].x;
+  }
+#else
   const double* r = srow + off + 6 * tx;
 #pragma unroll
   for (int k = 0; k < 12; ++k) w[k] = r[k];
+#endif
 }
 
 template <int DJ, int YF, int ZF, int RM>
