@@ -123,7 +123,10 @@ namespace {
 #define AFEM_STENCIL_TY 4
 #endif
 constexpr int TX = 32, TXN = 2 * TX, TY = AFEM_STENCIL_TY, NT = TX * TY;
-constexpr int kMainBlocksPerSm = TY == 4 ? 5 : 16 / TY;  // 5: TMA staging left the main loop at <= 102 registers
+#ifndef AFEM_MAIN_MINB
+#define AFEM_MAIN_MINB (TY == 4 ? 5 : 16 / TY)  // 5: TMA staging left the main loop at <= 96 registers
+#endif
+constexpr int kMainBlocksPerSm = AFEM_MAIN_MINB;
 
 // Structural zero of a family's entry (a, b) at offset d: the brick's reflection symmetry about
 // an axis c that the family keeps intact makes every off-diagonal entry involving c vanish when

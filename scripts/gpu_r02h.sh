@@ -4,10 +4,11 @@
 mkdir -p gpurun_out
 timeout 900 python -X faulthandler -m pytest tests/test_gpu_stencil.py tests/test_gpu_fullsize.py tests/test_gpu_parity.py -q > gpurun_out/pytest_h.log 2>&1
 echo "pytest exit $?: $(tail -1 gpurun_out/pytest_h.log)"; grep -E "^FAILED|^E " gpurun_out/pytest_h.log | head -10
-for v in fused split; do
+for v in fused split minb4 minb4split; do
   for rep in 1 2; do
-    if [ $v = split ]; then sp=1; else sp=; fi
-    AFEM_STENCIL_SPLIT=$sp timeout 300 python bench.py --steps 40 --warmup 12 --no-cpu --e2e-steps 1 > gpurun_out/abh_${v}_$rep.json 2>gpurun_out/abh_${v}_$rep.err
+    sp=; lib=
+    case $v in split) sp=1;; minb4) lib=paper_2604_22087_b200/variants/libafem_minb4.so;; minb4split) sp=1; lib=paper_2604_22087_b200/variants/libafem_minb4.so;; esac
+    AFEM_LIBRARY=$lib AFEM_STENCIL_SPLIT=$sp timeout 300 python bench.py --steps 40 --warmup 12 --no-cpu --e2e-steps 1 > gpurun_out/abh_${v}_$rep.json 2>gpurun_out/abh_${v}_$rep.err
     python -c "import json; d=json.loads(open('gpurun_out/abh_${v}_$rep.json').read().strip().splitlines()[-1]); print('$v', round(d['ms_per_step']*1e3,2), 'us', round(d['value']/1e9,2), 'GDOF/s cg', round(d['cg']['solve_s'],3), d['cg']['iterations'])"
   done
 done
