@@ -74,13 +74,6 @@ struct StencilPlan {
   DevArray<double> Kg;   // Khat (row-major 24 x 24)
   RowsK0 k0;             // the correction kernel's coefficients
   int64_t n_items = 0;   // tile correction items incl. padding
-  // the same items ordered by the main kernel's (tile, plane) units, each unit starting on a batch
-  // boundary: the full apply runs them in the main kernel's tail (k_stencil_tma, FUSED), each CTA
-  // the items of the nodes it wrote (unit_batch[u] = first batch of unit u, U + 1 entries)
-  DevArray<uint64_t> ut_rec;
-  DevArray<uint32_t> ut_zm;
-  DevArray<int32_t> unit_batch;
-  bool fused_items = false;
   int64_t n_fix_nodes = 0, n_edge_nodes = 0;
   int kchunk = 16;
   int nchunks = 1;
@@ -337,25 +330,10 @@ static_assert((TY + 2) * IWORDS <= NT, "one info word per thread");
 static_assert(XBOX <= RSP && IBOX <= IRP && XBOX <= 256, "TMA box sizes");
 
 template <bool DOT>
-__device__ __forceinline__ void item_batch(uint64_t rec, uint32_t zm, int NX, int NXY, const double (&Ks)[3][24],
-                                           const double* Es, const double* __restrict__ x,
-                                           const uint8_t* __restrict__ info, double* __restrict__ y, double& dsum);
-
-// The correction items of the nodes a CTA wrote, run by the same CTA after its planes (full apply).
-struct UnitItems {
-  const uint64_t* rec;
-  const uint32_t* zm;
-  const int32_t* unit_batch;
-  const uint8_t* info;
-  int enabled;
-};
-
-template <bool DOT>
 __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
     k_stencil_tma(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mi,
                   const __grid_constant__ StencilParams P, int xshift, int ipx, const double* __restrict__ x,
-                  double* __restrict__ y, int kchunk, int kbeg, int kend, DotArgs dot, int ntx, int nty,
-                  const __grid_constant__ RowsK0 K0, UnitItems ui) {
+                  double* __restrict__ y, int kchunk, int kbeg, int kend, DotArgs dot, int ntx, int nty) {
   if (dot.skip && *dot.skip) return;
   double dsum = 0.0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -386,7 +364,6 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
     u = U * blockIdx.x / gridDim.x;
     ue = U * (blockIdx.x + 1) / gridDim.x;
   }
-  const int64_t u_first = u, u_end = ue;
   while (u < ue) {
     int bx, by, k0, k1;
     if (kchunk > 0) {
@@ -548,18 +525,6 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
         if (pb + RING - 1 + q <= k1) issue(pb + RING - 1 + q);  // into the slots of planes pb - 1 + q
     }
   }
-  if (ui.enabled && kchunk <= 0) {
-    // fused correction items: this CTA's units' batches, after its own y writes are visible
-    __shared__ __align__(16) double Ks[3][24];
-    if (tid < 72) Ks[tid / 24][tid % 24] = K0.k[tid / 24][tid % 24];
-    __syncthreads();
-    const int lane = tid & 31, warp = tid >> 5;
-    const int64_t blo = ui.unit_batch[u_first], bhi = ui.unit_batch[u_end];
-    const int NXY = NX * NY;
-    for (int64_t bt = blo + warp; bt < bhi; bt += TY)
-      item_batch<DOT>(__ldg(&ui.rec[bt * 32 + lane]), __ldg(&ui.zm[bt * 32 + lane]), NX, NXY, Ks, Es, x, ui.info,
-                      y, dsum);
-  }
   if constexpr (DOT) {
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int nb = gridDim.x * gridDim.y * gridDim.z;
@@ -608,92 +573,6 @@ struct Items {
   int64_t n;  // multiple of 32
 };
 
-// One 32-item batch of correction items (k_stencil_items, and the fused tail of k_stencil_tma): each
-// lane one (node, octant) item, fixed-order segmented sums per node, the segment head updates y.
-template <bool DOT>
-__device__ __forceinline__ void item_batch(uint64_t rec, uint32_t zm, int NX, int NXY, const double (&Ks)[3][24],
-                                           const double* Es, const double* __restrict__ x,
-                                           const uint8_t* __restrict__ info, double* __restrict__ y, double& dsum) {
-  const int node = static_cast<int>(static_cast<uint32_t>(rec));
-  const uint32_t w = static_cast<uint32_t>(rec >> 32);
-  double r0 = 0.0, r1 = 0.0, r2 = 0.0;
-  const int L = node >= 0 ? (w >> 3) & 15 : 0;
-  const bool edge = (w >> 7) & 1;
-  // the head's own node: info, current y and x, loaded before the compute (no other thread of
-  // this kernel writes this node's y)
-  uint32_t inf = 0;
-  double yn[3] = {0.0, 0.0, 0.0}, xn3[3] = {0.0, 0.0, 0.0};
-  if (L > 0) {
-    inf = __ldg(&info[node]);
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      if (!edge) yn[a] = y[3 * (int64_t)node + a];
-      if (DOT || edge) xn3[a] = __ldg(&x[3 * (int64_t)node + a]);
-    }
-  }
-  if (node >= 0) {
-    const int rm = (w & 7) ^ 7;  // the node's bit corner in the element (octant o = its mirror)
-    // frame corner b lies at +-bit_c(b) along axis c from the node (minus where rm has bit c)
-    const int SX = (rm & 1) ? -1 : 1, SY = (rm & 2) ? -NX : NX, SZ = (rm & 4) ? -NXY : NXY;
-    // reflected frame: the node sits at bit corner 0; frame corner b is element corner b ^ rm, and
-    // component c of x and row c of y flip sign with bit c of rm
-    const double s0 = (rm & 1) ? -1.0 : 1.0, s1 = (rm & 2) ? -1.0 : 1.0, s2 = (rm & 4) ? -1.0 : 1.0;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const int nd = node + ((b & 1) ? SX : 0) + ((b & 2) ? SY : 0) + ((b & 4) ? SZ : 0);
-      const uint32_t zb = (zm >> (3 * b)) & 7;
-      const int a0 = zb == 7 ? 0 : 3 * nd;  // all-zero corners (outside) read a safe address
-      const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);  // 16 B-aligned pair
-      const double2 pr = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
-      const double sg = __ldg(x + (odd ? a0 : a0 + 2));
-      const double c0 = (zb & 1) ? 0.0 : s0 * (odd ? sg : pr.x);
-      const double c1 = (zb & 2) ? 0.0 : s1 * (odd ? pr.x : pr.y);
-      const double c2 = (zb & 4) ? 0.0 : s2 * (odd ? pr.y : sg);
-      const double cv[3] = {c0, c1, c2};
-#pragma unroll
-      for (int cc = 0; cc < 3; ++cc) {
-        r0 = fma(Ks[0][3 * b + cc], cv[cc], r0);
-        r1 = fma(Ks[1][3 * b + cc], cv[cc], r1);
-        r2 = fma(Ks[2][3 * b + cc], cv[cc], r2);
-      }
-    }
-    const double dE = Es[(w >> 8) & 31] - Es[(w >> 13) & 31];
-    r0 *= s0 * dE;
-    r1 *= s1 * dE;
-    r2 *= s2 * dE;
-  }
-  // segmented tree sum: rem = items from this lane to its segment's end (<= 8, never crossing the
-  // batch); after the step with offset d every lane holds the sum of [lane, min(lane + 2d, end))
-  const int rem = static_cast<int>((rec >> 50) & 15);
-#pragma unroll
-  for (int d = 1; d < 8; d <<= 1) {
-    const double v0 = __shfl_down_sync(0xffffffffu, r0, d);
-    const double v1 = __shfl_down_sync(0xffffffffu, r1, d);
-    const double v2 = __shfl_down_sync(0xffffffffu, r2, d);
-    if (d < rem) {
-      r0 += v0;
-      r1 += v1;
-      r2 += v2;
-    }
-  }
-  if (L > 0) {
-    const double rr3[3] = {r0, r1, r2};
-    double* yo = y + 3 * (int64_t)node;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const bool con = (inf >> a) & 1;
-      if (edge) {  // edge column: the whole row sum, written
-        const double ya = con ? xn3[a] : rr3[a];
-        yo[a] = ya;
-        if constexpr (DOT) dsum = fma(xn3[a], ya, dsum);
-      } else if (!con) {
-        yo[a] = yn[a] + rr3[a];
-        if constexpr (DOT) dsum = fma(xn3[a], rr3[a], dsum);
-      }
-    }
-  }
-}
-
 template <bool DOT>
 __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, const __grid_constant__ RowsK0 K0,
                                                                  const double* __restrict__ Epar,
@@ -724,7 +603,84 @@ __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, 
       nrec = __ldg(&it.rec[(bt + nw) * 32 + lane]);
       nzm = __ldg(&it.zm[(bt + nw) * 32 + lane]);
     }
-    item_batch<DOT>(rec, zm, NX, NXY, Ks, Es, x, info, y, dsum);
+    const int node = static_cast<int>(static_cast<uint32_t>(rec));
+    const uint32_t w = static_cast<uint32_t>(rec >> 32);
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+    const int L = node >= 0 ? (w >> 3) & 15 : 0;
+    const bool edge = (w >> 7) & 1;
+    // the head's own node: info, current y and x, loaded before the compute (no other thread of
+    // this kernel writes this node's y)
+    uint32_t inf = 0;
+    double yn[3] = {0.0, 0.0, 0.0}, xn3[3] = {0.0, 0.0, 0.0};
+    if (L > 0) {
+      inf = __ldg(&info[node]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (!edge) yn[a] = y[3 * (int64_t)node + a];
+        if (DOT || edge) xn3[a] = __ldg(&x[3 * (int64_t)node + a]);
+      }
+    }
+    if (node >= 0) {
+      const int rm = (w & 7) ^ 7;  // the node's bit corner in the element (octant o = its mirror)
+      // frame corner b lies at +-bit_c(b) along axis c from the node (minus where rm has bit c)
+      const int SX = (rm & 1) ? -1 : 1, SY = (rm & 2) ? -NX : NX, SZ = (rm & 4) ? -NXY : NXY;
+      // reflected frame: the node sits at bit corner 0; frame corner b is element corner b ^ rm, and
+      // component c of x and row c of y flip sign with bit c of rm
+      const double s0 = (rm & 1) ? -1.0 : 1.0, s1 = (rm & 2) ? -1.0 : 1.0, s2 = (rm & 4) ? -1.0 : 1.0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int nd = node + ((b & 1) ? SX : 0) + ((b & 2) ? SY : 0) + ((b & 4) ? SZ : 0);
+        const uint32_t zb = (zm >> (3 * b)) & 7;
+        const int a0 = zb == 7 ? 0 : 3 * nd;  // all-zero corners (outside) read a safe address
+        const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);  // 16 B-aligned pair
+        const double2 pr = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
+        const double sg = __ldg(x + (odd ? a0 : a0 + 2));
+        const double c0 = (zb & 1) ? 0.0 : s0 * (odd ? sg : pr.x);
+        const double c1 = (zb & 2) ? 0.0 : s1 * (odd ? pr.x : pr.y);
+        const double c2 = (zb & 4) ? 0.0 : s2 * (odd ? pr.y : sg);
+        const double cv[3] = {c0, c1, c2};
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          r0 = fma(Ks[0][3 * b + cc], cv[cc], r0);
+          r1 = fma(Ks[1][3 * b + cc], cv[cc], r1);
+          r2 = fma(Ks[2][3 * b + cc], cv[cc], r2);
+        }
+      }
+      const double dE = Es[(w >> 8) & 31] - Es[(w >> 13) & 31];
+      r0 *= s0 * dE;
+      r1 *= s1 * dE;
+      r2 *= s2 * dE;
+    }
+    // segmented tree sum: rem = items from this lane to its segment's end (<= 8, never crossing the
+    // batch); after the step with offset d every lane holds the sum of [lane, min(lane + 2d, end))
+    const int rem = static_cast<int>((rec >> 50) & 15);
+#pragma unroll
+    for (int d = 1; d < 8; d <<= 1) {
+      const double v0 = __shfl_down_sync(0xffffffffu, r0, d);
+      const double v1 = __shfl_down_sync(0xffffffffu, r1, d);
+      const double v2 = __shfl_down_sync(0xffffffffu, r2, d);
+      if (d < rem) {
+        r0 += v0;
+        r1 += v1;
+        r2 += v2;
+      }
+    }
+    if (L > 0) {
+      const double rr3[3] = {r0, r1, r2};
+      double* yo = y + 3 * (int64_t)node;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const bool con = (inf >> a) & 1;
+        if (edge) {  // edge column: the whole row sum, written
+          const double ya = con ? xn3[a] : rr3[a];
+          yo[a] = ya;
+          if constexpr (DOT) dsum = fma(xn3[a], ya, dsum);
+        } else if (!con) {
+          yo[a] = yn[a] + rr3[a];
+          if constexpr (DOT) dsum = fma(xn3[a], rr3[a], dsum);
+        }
+      }
+    }
   }
   if constexpr (DOT)
     block_to_slot_and_finish(dsum, dot.part_items, blockIdx.x, gridDim.x, dot.part_main, dot.n_main, dot.counter,
@@ -1107,68 +1063,6 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
     }
     plan->n_items = static_cast<int64_t>(trec.size());
     while (static_cast<int>(plan->piece_items.size()) <= plan->npieces) plan->piece_items.push_back(plan->n_items);
-
-    // unit-ordered copy for the fused tail: unit u = (by * ntx + bx) * NZ + k of the node's main
-    // tile (edge-column nodes beyond the last tile go with that tile's unit: no CTA writes them in
-    // the main loop), each unit's items starting on a batch boundary
-    const int ntx = (P.NXm + TXN - 1) / TXN;
-    static const bool split = std::getenv("AFEM_STENCIL_SPLIT") != nullptr;  // A/B: separate items kernel
-    if (ntx > 0 && !split) {
-      const int64_t U = (int64_t)ntx * ntyc * P.NZ;
-      struct UItem { int64_t u; uint32_t node; uint32_t o; uint64_t rec; uint32_t zm; };
-      std::vector<UItem> ui;
-      ui.reserve(ti.size());
-      for (const TItem& t : ti) {
-        const uint32_t node = static_cast<uint32_t>(t.rec);
-        const int ni = static_cast<int>(node % P.NX);
-        const int64_t nr = node / P.NX;
-        const int nj = static_cast<int>(nr % P.NY), nk = static_cast<int>(nr / P.NY);
-        const int bx = std::min(ni / TXN, ntx - 1), by = nj / TY;
-        ui.push_back({((int64_t)by * ntx + bx) * P.NZ + nk, node, static_cast<uint32_t>((t.rec >> 32) & 7), t.rec,
-                      t.zm});
-      }
-      std::sort(ui.begin(), ui.end(), [](const UItem& a, const UItem& b) {
-        return a.u != b.u ? a.u < b.u : (a.node != b.node ? a.node < b.node : a.o < b.o);
-      });
-      std::vector<uint64_t> urec;
-      std::vector<uint32_t> uzm;
-      std::vector<int32_t> ub(static_cast<size_t>(U) + 1, 0);
-      auto pad = [&] {
-        while (urec.size() % 32) {
-          urec.push_back(kPadRec);
-          uzm.push_back(0);
-        }
-      };
-      int64_t next_u = 0;
-      for (size_t q2 = 0; q2 < ui.size();) {
-        if (ui[q2].u >= next_u) {  // a new unit starts on a batch boundary
-          pad();
-          for (; next_u <= ui[q2].u; ++next_u) ub[next_u] = static_cast<int32_t>(urec.size() / 32);
-        }
-        size_t e = q2;  // segment: one target node
-        while (e < ui.size() && ui[e].node == ui[q2].node) ++e;
-        const uint64_t L = e - q2;
-        if ((urec.size() % 32) + L > 32) pad();
-        for (size_t t = q2; t < e; ++t) {
-          // the segment fields (L at bit 35, remaining count at bit 50) of this ordering
-          const uint64_t base = ui[t].rec & ~((15ull << 35) | (15ull << 50));
-          urec.push_back(base | (t == q2 ? (L << 35) : 0ull) | (static_cast<uint64_t>(e - t) << 50));
-          uzm.push_back(ui[t].zm);
-        }
-        q2 = e;
-      }
-      pad();
-      for (; next_u <= U; ++next_u) ub[next_u] = static_cast<int32_t>(urec.size() / 32);
-      plan->ut_rec.alloc(std::max<size_t>(urec.size(), 1));
-      plan->ut_zm.alloc(std::max<size_t>(uzm.size(), 1));
-      plan->unit_batch.alloc(ub.size());
-      if (!urec.empty()) {
-        AFEM_CK(cudaMemcpyAsync(plan->ut_rec.p, urec.data(), urec.size() * 8, cudaMemcpyHostToDevice, c.stream));
-        AFEM_CK(cudaMemcpyAsync(plan->ut_zm.p, uzm.data(), uzm.size() * 4, cudaMemcpyHostToDevice, c.stream));
-      }
-      AFEM_CK(cudaMemcpyAsync(plan->unit_batch.p, ub.data(), ub.size() * 4, cudaMemcpyHostToDevice, c.stream));
-      plan->fused_items = true;
-    }
     plan->it_rec.alloc(std::max<size_t>(trec.size(), 1));
     plan->it_zm.alloc(std::max<size_t>(tzm.size(), 1));
     if (!trec.empty()) {
@@ -1232,7 +1126,7 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, 
     AFEM_CK(cudaGraphInstantiate(&slot->exec, g, 0));
   }
   AFEM_CK(cudaGraphLaunch(slot->exec, c.stream));
-  c.launches += (pl.p.NXm > 0 ? 1 : 0) + (pl.n_items > 0 && !(pl.fused_items && pl.p.NXm > 0) ? 1 : 0);
+  c.launches += (pl.p.NXm > 0 ? 1 : 0) + (pl.n_items > 0 ? 1 : 0);
 }
 
 static void stencil_apply_launch(StencilPlan& pl, const MfOp& op, const double* x, double* y, double* dot_out,
@@ -1241,10 +1135,7 @@ static void stencil_apply_launch(StencilPlan& pl, const MfOp& op, const double* 
   const StencilParams& P = pl.p;
   const int ntx = (P.NXm + TXN - 1) / TXN, nty = (P.NY + TY - 1) / TY;
   const int nb_main = P.NXm > 0 ? pl.main_blocks : 0;
-  const bool fused = pl.fused_items && nb_main > 0;
-  const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, (fused || pl.n_items == 0) ? 1 : 0, nb_main,
-                    skip};
-  const UnitItems ui{pl.ut_rec.p, pl.ut_zm.p, pl.unit_batch.p, pl.info.p, fused ? 1 : 0};
+  const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main, skip};
   // measurement switch (scripts only): AFEM_STENCIL_ONLY=main|items launches one of the two kernels
   static const char* only = std::getenv("AFEM_STENCIL_ONLY");
   const bool run_main = !only || only[0] == 'm', run_items = !only || only[0] == 'i';
@@ -1252,12 +1143,12 @@ static void stencil_apply_launch(StencilPlan& pl, const MfOp& op, const double* 
     stencil_x_map(pl, x);
     if (dot_out)
       launch(c, k_stencil_tma<true>, nb_main, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, 0, P.NZ, dot,
-             ntx, nty, pl.k0, ui);
+             ntx, nty);
     else
       launch(c, k_stencil_tma<false>, nb_main, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, 0, P.NZ, dot,
-             ntx, nty, pl.k0, ui);
+             ntx, nty);
   }
-  if (pl.n_items > 0 && run_items && !fused) {
+  if (pl.n_items > 0 && run_items) {
     const Items it{pl.it_rec.p, pl.it_zm.p, pl.n_items};
     if (dot_out)
       launch(c, k_stencil_items<true>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p,
@@ -1285,9 +1176,7 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
     const int kc = std::max(4, (ke - kb + want - 1) / want);
     const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TY - 1) / TY, (ke - kb + kc - 1) / kc);
     stencil_x_map(pl, x);
-    const UnitItems none{nullptr, nullptr, nullptr, nullptr, 0};
-    launch(c, k_stencil_tma<false>, grid, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, kc, kb, ke, dot, 0, 0,
-           pl.k0, none);
+    launch(c, k_stencil_tma<false>, grid, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, kc, kb, ke, dot, 0, 0);
   }
   const int64_t i0 = pl.piece_items[pa], i1 = pl.piece_items[pb];
   if (i1 > i0) {

@@ -254,50 +254,3 @@ def test_graph_apply_recaptures_on_new_pointers(afem, ctx):
     L.afem_op_apply_async(op.h, C.c_void_p(dx[0].data_ptr()), C.c_void_p(dy[0].data_ptr()))
     torch.cuda.synchronize()
     assert np.array_equal(dy[0].cpu().numpy(), ref[2])
-
-
-FUSED_SNIPPET = r"""
-import sys, numpy as np
-sys.path.insert(0, {root!r})
-import paper_2604_22087_b200 as afem
-ctx = afem.Context(0)
-s = afem.System.grid(ctx, 3, {n}, {m}, {k}, inclusions=afem.fibres(12345, 40), radius=0.05,
-                     materials=[(0, 1.0, 0.3), (0, 10.0, 0.3)])
-s.set_benchmark_dirichlet(0.01)
-u = s.impose_dirichlet(np.zeros(s.n))
-op = afem.matrix_free_operator(s, u)
-x = np.random.default_rng(7).uniform(-1, 1, s.n)
-y = op.apply(x)
-b = -s.constrain_residual(s.residual(u), u)
-xs, rep = afem.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
-np.save({out!r} + "_y.npy", y)
-np.save({out!r} + "_x.npy", xs)
-print(rep["iterations"])
-"""
-
-
-@pytest.mark.parametrize("dims", [(70, 40, 24), (129, 33, 17), (80, 20, 10)])
-def test_fused_items_tail_bitwise_equals_split_kernels(tmp_path, dims):
-    """The full apply runs the correction items in the main kernel's tail (each CTA the items of the
-    nodes it wrote); AFEM_STENCIL_SPLIT=1 runs the separate k_stencil_items kernel. Same items, same
-    per-node order: y bitwise equal; the fused p.Ap sums in another order, so CG iterates agree to
-    the solve tolerance (iteration counts within 1)."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {}
-    for split in (False, True):
-        env = dict(os.environ)
-        env.pop("AFEM_STENCIL_SPLIT", None)
-        if split:
-            env["AFEM_STENCIL_SPLIT"] = "1"
-        out = str(tmp_path / ("split" if split else "fused"))
-        p = subprocess.run([sys.executable, "-c", FUSED_SNIPPET.format(root=root, n=dims[0], m=dims[1], k=dims[2],
-                                                                       out=out)],
-                           capture_output=True, text=True, env=env, timeout=600)
-        assert p.returncode == 0, p.stderr[-3000:]
-        res[split] = (np.load(out + "_y.npy"), np.load(out + "_x.npy"), int(p.stdout.strip().splitlines()[-1]))
-    assert np.array_equal(res[False][0], res[True][0])
-    assert abs(res[False][2] - res[True][2]) <= 1
-    assert rel_err(res[False][1], res[True][1]) <= 1e-7
