@@ -564,10 +564,13 @@ __global__ void k_info_pad(const uint8_t* __restrict__ info, uint8_t* __restrict
 // rec: node (low 32 bits, -1 = padding) | oct << 32 | seg << 35 | edge << 39 | pho << 40 |
 // phb << 45 | rem << 50 (items left in the segment, this one included); zm: bit 3b+c = input c of
 // the element's bit corner b ^ rm (the item's reflected frame) is zero (Dirichlet or outside).
-#ifndef AFEM_ITEMS_SCALAR
-#define AFEM_ITEMS_SCALAR 0
+#ifndef AFEM_ITEM_THREADS
+#define AFEM_ITEM_THREADS 256
 #endif
-constexpr int kItemThreads = 256;
+#ifndef AFEM_ITEM_MINB
+#define AFEM_ITEM_MINB 1
+#endif
+constexpr int kItemThreads = AFEM_ITEM_THREADS;
 constexpr uint64_t kPadRec = 0xffffffffull;
 
 struct Items {
@@ -577,7 +580,7 @@ struct Items {
 };
 
 template <bool DOT>
-__global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, const __grid_constant__ RowsK0 K0,
+__global__ void __launch_bounds__(kItemThreads, AFEM_ITEM_MINB) k_stencil_items(int NX, int NY, const __grid_constant__ RowsK0 K0,
                                                                  const double* __restrict__ Epar,
                                                                  const double* __restrict__ x,
                                                                  const uint8_t* __restrict__ info, Items it,
@@ -635,23 +638,12 @@ __global__ void __launch_bounds__(kItemThreads) k_stencil_items(int NX, int NY, 
         const int nd = node + ((b & 1) ? SX : 0) + ((b & 2) ? SY : 0) + ((b & 4) ? SZ : 0);
         const uint32_t zb = (zm >> (3 * b)) & 7;
         const int a0 = zb == 7 ? 0 : 3 * nd;  // all-zero corners (outside) read a safe address
-#if AFEM_ITEMS_SCALAR
-        // three 8-byte loads (no alignment selects); the reflection signs flip the sign bit on the
-        // integer pipe (bit-identical to the multiplication by -1)
-        const double* xp = x + a0;
-        const unsigned long long v0 = __double_as_longlong(__ldg(xp)), v1 = __double_as_longlong(__ldg(xp + 1)),
-                                 v2 = __double_as_longlong(__ldg(xp + 2));
-        const double c0 = (zb & 1) ? 0.0 : __longlong_as_double(v0 ^ ((rm & 1) ? 0x8000000000000000ull : 0ull));
-        const double c1 = (zb & 2) ? 0.0 : __longlong_as_double(v1 ^ ((rm & 2) ? 0x8000000000000000ull : 0ull));
-        const double c2 = (zb & 4) ? 0.0 : __longlong_as_double(v2 ^ ((rm & 4) ? 0x8000000000000000ull : 0ull));
-#else
         const int odd = static_cast<int>((reinterpret_cast<uintptr_t>(x + a0) >> 3) & 1);  // 16 B-aligned pair
         const double2 pr = __ldg(reinterpret_cast<const double2*>(x + a0 + odd));
         const double sg = __ldg(x + (odd ? a0 : a0 + 2));
         const double c0 = (zb & 1) ? 0.0 : s0 * (odd ? sg : pr.x);
         const double c1 = (zb & 2) ? 0.0 : s1 * (odd ? pr.x : pr.y);
         const double c2 = (zb & 4) ? 0.0 : s2 * (odd ? pr.y : sg);
-#endif
         const double cv[3] = {c0, c1, c2};
 #pragma unroll
         for (int cc = 0; cc < 3; ++cc) {
