@@ -116,11 +116,6 @@ namespace {
 #define AFEM_STENCIL_TY 4
 #endif
 constexpr int TX = 32, TXN = 2 * TX, TY = AFEM_STENCIL_TY, NT = TX * TY;
-// node rows per warp (RW) and per CTA tile (TR); SR rows staged per plane (one-row halo)
-#ifndef AFEM_STENCIL_ROWS
-#define AFEM_STENCIL_ROWS 1
-#endif
-constexpr int RW = AFEM_STENCIL_ROWS, TR = TY * RW, SR = TR + 2;
 #ifndef AFEM_MAIN_MINB
 #define AFEM_MAIN_MINB (16 / TY)  // 4 CTAs x 4 warps (5 CTAs at <= 96 registers measured 2 % slower)
 #endif
@@ -252,56 +247,6 @@ __device__ __forceinline__ void row_step(const StencilParams& P, const double* _
   nb<1, DJ, YF, ZF, 2, RM>(P, w[8], w[11], acc);
 }
 
-// The 9 neighbour-column updates of one staged row whose window is already in registers.
-template <int DJ, int YF, int ZF, int RM>
-__device__ __forceinline__ void row_fma(const StencilParams& P, const double (&w)[12], double (&acc)[2][3][3]) {
-  nb<-1, DJ, YF, ZF, 0, RM>(P, w[0], w[3], acc);
-  nb<-1, DJ, YF, ZF, 1, RM>(P, w[1], w[4], acc);
-  nb<-1, DJ, YF, ZF, 2, RM>(P, w[2], w[5], acc);
-  nb<0, DJ, YF, ZF, 0, RM>(P, w[3], w[6], acc);
-  nb<0, DJ, YF, ZF, 1, RM>(P, w[4], w[7], acc);
-  nb<0, DJ, YF, ZF, 2, RM>(P, w[5], w[8], acc);
-  nb<1, DJ, YF, ZF, 0, RM>(P, w[6], w[9], acc);
-  nb<1, DJ, YF, ZF, 1, RM>(P, w[7], w[10], acc);
-  nb<1, DJ, YF, ZF, 2, RM>(P, w[8], w[11], acc);
-}
-
-// Two node rows per warp (AFEM_STENCIL_ROWS = 2): staged rows rb .. rb + 3 feed row A (rb + 1) and
-// row B (rb + 2); every window is loaded once and used by both rows it touches.
-template <int YFA, int YFB, int ZF, int STRIDE>
-__device__ __forceinline__ void plane2(const StencilParams& P, const double* __restrict__ s, int tx, int rb, int offs,
-                                       double (&accA)[2][3][3], double (&accB)[2][3][3]) {
-  double w[12];
-  load_window(s + (rb + 0) * STRIDE, tx, offs & 1, w);
-  row_fma<-1, YFA, ZF, 7>(P, w, accA);
-  load_window(s + (rb + 1) * STRIDE, tx, (offs >> 1) & 1, w);
-  row_fma<0, YFA, ZF, 7>(P, w, accA);
-  row_fma<-1, YFB, ZF, 7>(P, w, accB);
-  load_window(s + (rb + 2) * STRIDE, tx, (offs >> 2) & 1, w);
-  row_fma<1, YFA, ZF, 7>(P, w, accA);
-  row_fma<0, YFB, ZF, 7>(P, w, accB);
-  load_window(s + (rb + 3) * STRIDE, tx, (offs >> 3) & 1, w);
-  row_fma<1, YFB, ZF, 7>(P, w, accB);
-}
-
-template <int ZF, int STRIDE>
-__device__ __forceinline__ void plane2_yf(const StencilParams& P, const double* s, int tx, int rb, int offs, int yfA,
-                                          int yfB, double (&accA)[2][3][3], double (&accB)[2][3][3]) {
-  if (yfA == 0 && yfB == 0) plane2<0, 0, ZF, STRIDE>(P, s, tx, rb, offs, accA, accB);
-  else if (yfA == 1 && yfB == 0) plane2<1, 0, ZF, STRIDE>(P, s, tx, rb, offs, accA, accB);
-  else if (yfA == 0) plane2<0, 2, ZF, STRIDE>(P, s, tx, rb, offs, accA, accB);
-  else if (yfA == 2) plane2<2, 0, ZF, STRIDE>(P, s, tx, rb, offs, accA, accB);  // B beyond the grid
-  else plane2<1, 2, ZF, STRIDE>(P, s, tx, rb, offs, accA, accB);
-}
-
-template <int STRIDE>
-__device__ __forceinline__ void plane2_any(const StencilParams& P, const double* s, int tx, int rb, int offs, int yfA,
-                                           int yfB, int zc, double (&accA)[2][3][3], double (&accB)[2][3][3]) {
-  if (zc == 0) plane2_yf<0, STRIDE>(P, s, tx, rb, offs, yfA, yfB, accA, accB);
-  else if (zc == 1) plane2_yf<1, STRIDE>(P, s, tx, rb, offs, yfA, yfB, accA, accB);
-  else plane2_yf<2, STRIDE>(P, s, tx, rb, offs, yfA, yfB, accA, accB);
-}
-
 // offs: bit r = the window offset of staged row ty + r
 template <int YF, int ZF, int STRIDE, int RM>
 __device__ __forceinline__ void plane_step(const StencilParams& P, const double* __restrict__ s, int tx, int ty,
@@ -354,11 +299,7 @@ struct DotArgs {
 #define AFEM_STENCIL_PPB 1
 #endif
 constexpr int PPB = AFEM_STENCIL_PPB;
-#ifndef AFEM_STENCIL_RING
-#define AFEM_STENCIL_RING (2 * PPB + (PPB == 1 ? 2 : 1))
-#endif
-constexpr int RING = AFEM_STENCIL_RING;
-static_assert(RING >= 2 * PPB + 1, "ring: output plane + PPB computing + at least PPB in flight");
+constexpr int RING = 2 * PPB + (PPB == 1 ? 2 : 1);
 
 // k_stencil_tma: the main kernel with Blackwell bulk-async staging. Per CTA plane the (TY + 2)
 // rows of the 64 + 2 node window (interleaved dofs) and their info bytes arrive by TMA: rank-1
@@ -383,8 +324,9 @@ constexpr int IBOX = 96;             // info bytes per box (15 pad + 66 window, 
 constexpr int IOFF = 15;             // window byte offset inside an info box
 constexpr int IW0 = IOFF / 4, IW1 = (IOFF + TXN + 2 + 3) / 4;  // info words touching the window
 constexpr int IWORDS = IW1 - IW0;
-constexpr size_t kTmaSmem = 128 + sizeof(double) * RING * SR * RSP + RING * SR * IRP +
+constexpr size_t kTmaSmem = 128 + sizeof(double) * RING * (TY + 2) * RSP + RING * (TY + 2) * IRP +
                             8 * RING + 8 * 32;
+static_assert((TY + 2) * IWORDS <= NT, "one info word per thread");
 static_assert(XBOX <= RSP && IBOX <= IRP && XBOX <= 256, "TMA box sizes");
 
 template <bool DOT>
@@ -398,9 +340,10 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
   // 128-byte aligned base, derived from smem_raw itself so the compiler keeps shared-space
   // accesses (LDS / STS, not generic loads)
   unsigned char* const base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  double (*xs)[SR][RSP] = reinterpret_cast<double (*)[SR][RSP]>(base);
-  uint8_t (*is)[SR][IRP] = reinterpret_cast<uint8_t (*)[SR][IRP]>(base + sizeof(double) * RING * SR * RSP);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + sizeof(double) * RING * SR * RSP + RING * SR * IRP);
+  double (*xs)[TY + 2][RSP] = reinterpret_cast<double (*)[TY + 2][RSP]>(base);
+  uint8_t (*is)[TY + 2][IRP] =
+      reinterpret_cast<uint8_t (*)[TY + 2][IRP]>(base + sizeof(double) * RING * (TY + 2) * RSP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + sizeof(double) * RING * (TY + 2) * RSP + RING * (TY + 2) * IRP);
   double* Es = reinterpret_cast<double*>(bars + RING);
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
@@ -438,13 +381,11 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
       k1 = kbeg + kl;
       u += kl - kk;
     }
-    const int i0 = bx * TXN, j0 = by * TR;
-    const int i = i0 + 2 * tx, j = j0 + RW * ty;  // the warp's first row (RW rows: j .. j + RW - 1)
+    const int i0 = bx * TXN, j0 = by * TY;
+    const int i = i0 + 2 * tx, j = j0 + ty;
     const bool active = j < NY;
     const bool v0 = i < P.NXm, v1 = i + 1 < P.NXm;
     const int yf = j == 0 ? 1 : (j == NY - 1 ? 2 : 0);
-    const bool activeB = RW > 1 && j + 1 < NY;  // RW = 2: the warp's second row
-    const int yfB = j + 1 == NY - 1 ? 2 : 0;
     // window offset (0 / 1 double) of staged row r of plane p: parity of its first dof's element
     auto roff = [&](int r, int p) -> int {
       return (1 + NX * ((j0 - 1 + r) + NY * p) + xshift) & 1;  // 3 (i0 - 1 + ...) = i0 - 1 + ... mod 2
@@ -452,7 +393,7 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
 
     // rows outside [0, NY) are never copied: zero them in every slot for this segment
     __syncthreads();
-    for (int r = 0; r < SR; ++r) {
+    for (int r = 0; r < TY + 2; ++r) {
       const int jj = j0 - 1 + r;
       if (jj >= 0 && jj < NY) continue;
       for (int q = tid; q < RING * RSP; q += NT) xs[q / RSP][r][q % RSP] = 0.0;
@@ -474,10 +415,10 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
       if (w == 0) {
         int rows = 0;
 #pragma unroll
-        for (int r = 0; r < SR; ++r) rows += (j0 - 1 + r >= 0 && j0 - 1 + r < NY) ? 1 : 0;
+        for (int r = 0; r < TY + 2; ++r) rows += (j0 - 1 + r >= 0 && j0 - 1 + r < NY) ? 1 : 0;
         mbar_arrive_expect_tx(bar, static_cast<uint32_t>(rows * (XBOX * 8 + IBOX)));
       }
-      for (int r = w; r < SR; r += TY) {
+      for (int r = w; r < TY + 2; r += TY) {
         const int jj = j0 - 1 + r;
         if (jj < 0 || jj >= NY) continue;
         const int row = jj + NY * p;
@@ -492,37 +433,32 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
       phase ^= 1u << sl;
     };
     auto mask = [&](int p) {  // zero out-of-range columns and Dirichlet dofs of landed plane p
-      if (p < 0 || p >= NZ) return;
+      if (p < 0 || p >= NZ || tid >= (TY + 2) * IWORDS) return;
       const int sl = ring(p);
-      for (int t = tid; t < SR * IWORDS; t += NT) {  // one info word per thread and pass
-        const int r = t / IWORDS, wb = 4 * (IW0 + t - IWORDS * r);  // the word's first byte
-        const int jj = j0 - 1 + r;
-        if (jj < 0 || jj >= NY) continue;
-        const uint32_t word = *reinterpret_cast<const uint32_t*>(&is[sl][r][wb]);
-        if (!(word & 0x07070707u)) continue;
-        double* row = &xs[sl][r][roff(r, p)];
+      const int r = tid / IWORDS, wb = 4 * (IW0 + tid - IWORDS * r);  // the word's first byte
+      const int jj = j0 - 1 + r;
+      if (jj < 0 || jj >= NY) return;
+      const uint32_t word = *reinterpret_cast<const uint32_t*>(&is[sl][r][wb]);
+      if (!(word & 0x07070707u)) return;
+      double* row = &xs[sl][r][roff(r, p)];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int col = wb + b - IOFF;
-          if (col < 0 || col >= TXN + 2) continue;
-          const uint32_t m = (word >> (8 * b)) & 7u;
+      for (int b = 0; b < 4; ++b) {
+        const int col = wb + b - IOFF;
+        if (col < 0 || col >= TXN + 2) continue;
+        const uint32_t m = (word >> (8 * b)) & 7u;
 #pragma unroll
-          for (int c = 0; c < 3; ++c)
-            if ((m >> c) & 1u) row[3 * col + c] = 0.0;
-        }
+        for (int c = 0; c < 3; ++c)
+          if ((m >> c) & 1u) row[3 * col + c] = 0.0;
       }
     };
 
-    double accs[RW][2][3][3];
+    double acc[2][3][3];
 #pragma unroll
-    for (int q = 0; q < RW; ++q)
+    for (int n = 0; n < 2; ++n)
 #pragma unroll
-      for (int n = 0; n < 2; ++n)
+      for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int a = 0; a < 3; ++a) accs[q][n][r][a] = 0.0;
-    const int rb = RW * ty;  // the warp's first staged row (its rows' halo row)
+        for (int a = 0; a < 3; ++a) acc[n][r][a] = 0.0;
     // one CTA barrier per PPB planes: planes pb .. pb + PPB - 1 are computed back to back (step p
     // also writes the nodes of plane p - 1), the next PPB are waited for and masked, then the
     // barrier frees the slots of planes pb - 1 .. pb + PPB - 2 for the planes RING - 1 ahead
@@ -542,51 +478,40 @@ __global__ void __launch_bounds__(NT, kMainBlocksPerSm)
         if (active && p >= 0 && p < NZ) {
           const int zc = p == 0 ? 1 : (p == NZ - 1 ? 2 : 0);
           const double* sp = &xs[ring(p)][0][0];
-          if constexpr (RW == 1) {
-            const int offs = roff(rb, p) | (roff(rb + 1, p) << 1) | (roff(rb + 2, p) << 2);
-            plane_any<RSP, 7>(P, sp, tx, rb, yf, zc, accs[0], offs);
-          } else {
-            const int offs = roff(rb, p) | (roff(rb + 1, p) << 1) | (roff(rb + 2, p) << 2) | (roff(rb + 3, p) << 3);
-            plane2_any<RSP>(P, sp, tx, rb, offs, yf, yfB, zc, accs[0], accs[RW - 1]);
-          }
+          const int offs = roff(ty, p) | (roff(ty + 1, p) << 1) | (roff(ty + 2, p) << 2);
+          plane_any<RSP, 7>(P, sp, tx, ty, yf, zc, acc, offs);
         }
+        if (active && p - 1 >= k0) {  // nodes (i, j, p-1) and (i+1, j, p-1) are complete
+          const int so = ring(p - 1);
+          const uint32_t oi0 = is[so][ty + 1][IOFF + 2 * tx + 1], oi1 = is[so][ty + 1][IOFF + 2 * tx + 2];
+          const double E0 = Es[oi0 >> 3], E1 = Es[oi1 >> 3];
+          const int64_t onode = i + (int64_t)NX * (j + (int64_t)NY * (p - 1));
+          // own nodes' staged inputs (raw x unless constrained)
+          const double* xrow = &xs[so][ty + 1][roff(ty + 1, p - 1) + 3 * (2 * tx + 1)];
+          double* yo = y + 3 * onode;
 #pragma unroll
-        for (int q = 0; q < RW; ++q) {
-          const bool act = q == 0 ? active : activeB;
-          if (act && p - 1 >= k0) {  // nodes (i, j + q, p-1) and (i+1, j + q, p-1) are complete
-            const int so = ring(p - 1), sr = rb + q + 1;
-            const uint32_t oi0 = is[so][sr][IOFF + 2 * tx + 1], oi1 = is[so][sr][IOFF + 2 * tx + 2];
-            const double E0 = Es[oi0 >> 3], E1 = Es[oi1 >> 3];
-            const int64_t onode = i + (int64_t)NX * (j + q + (int64_t)NY * (p - 1));
-            // own nodes' staged inputs (raw x unless constrained)
-            const double* xrow = &xs[so][sr][roff(sr, p - 1) + 3 * (2 * tx + 1)];
-            double* yo = y + 3 * onode;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              const bool c0 = (oi0 >> a) & 1, c1 = (oi1 >> a) & 1;
-              const double x0 = c0 ? (v0 ? __ldg(&x[3 * onode + a]) : 0.0) : xrow[a];
-              const double x1 = c1 ? (v1 ? __ldg(&x[3 * onode + 3 + a]) : 0.0) : xrow[3 + a];
-              const double y0 = c0 ? x0 : E0 * accs[q][0][0][a];
-              const double y1 = c1 ? x1 : E1 * accs[q][1][0][a];
-              if (v0) yo[a] = y0;
-              if (v1) yo[3 + a] = y1;
-              if constexpr (DOT) {
-                dsum = fma(v0 ? x0 : 0.0, y0, dsum);
-                dsum = fma(v1 ? x1 : 0.0, y1, dsum);
-              }
+          for (int a = 0; a < 3; ++a) {
+            const bool c0 = (oi0 >> a) & 1, c1 = (oi1 >> a) & 1;
+            const double x0 = c0 ? (v0 ? __ldg(&x[3 * onode + a]) : 0.0) : xrow[a];
+            const double x1 = c1 ? (v1 ? __ldg(&x[3 * onode + 3 + a]) : 0.0) : xrow[3 + a];
+            const double y0 = c0 ? x0 : E0 * acc[0][0][a];
+            const double y1 = c1 ? x1 : E1 * acc[1][0][a];
+            if (v0) yo[a] = y0;
+            if (v1) yo[3 + a] = y1;
+            if constexpr (DOT) {
+              dsum = fma(v0 ? x0 : 0.0, y0, dsum);
+              dsum = fma(v1 ? x1 : 0.0, y1, dsum);
             }
           }
         }
 #pragma unroll
-        for (int q = 0; q < RW; ++q)
+        for (int n = 0; n < 2; ++n)
 #pragma unroll
-          for (int n = 0; n < 2; ++n)
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              accs[q][n][0][a] = accs[q][n][1][a];
-              accs[q][n][1][a] = accs[q][n][2][a];
-              accs[q][n][2][a] = 0.0;
-            }
+          for (int a = 0; a < 3; ++a) {
+            acc[n][0][a] = acc[n][1][a];
+            acc[n][1][a] = acc[n][2][a];
+            acc[n][2][a] = 0.0;
+          }
       }
 #pragma unroll
       for (int q = 0; q < PPB; ++q)
@@ -1016,7 +941,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
   // 2-3 % faster (72.7 vs 74.9 us per C2 apply)
   occ = std::min(occ, kMainBlocksPerSm);
   const int64_t slots = (int64_t)std::max(occ, 1) * c.num_sms;
-  const int64_t tiles = (int64_t)((P.NXm + TXN - 1) / TXN) * ((P.NY + TR - 1) / TR);
+  const int64_t tiles = (int64_t)((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY);
   int chunks = tiles > 0 ? static_cast<int>(std::max<int64_t>(1, slots / tiles)) : 1;
   chunks = std::min(chunks, std::max(1, P.NZ / 8));
   plan->kchunk = (P.NZ + chunks - 1) / chunks;
@@ -1156,7 +1081,7 @@ StencilPlan* make_stencil_plan(System& s, const MfOp& op) {
     AFEM_CK(cudaStreamSynchronize(c.stream));
   }
   // balanced main grid: one resident wave, no more CTAs than (tile, plane) units
-  const int64_t units = (int64_t)((P.NXm + TXN - 1) / TXN) * ((P.NY + TR - 1) / TR) * P.NZ;
+  const int64_t units = (int64_t)((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY) * P.NZ;
   plan->main_blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(slots, units)));
   if (const char* e = std::getenv("AFEM_MAIN_BLOCKS")) plan->main_blocks = std::max(1, std::atoi(e));
   plan->part_main.alloc(std::max<int64_t>(plan->main_blocks, 1));
@@ -1217,7 +1142,7 @@ static void stencil_apply_launch(StencilPlan& pl, const MfOp& op, const double* 
                                  const int* skip) {
   Ctx& c = *op.sys->ctx;
   const StencilParams& P = pl.p;
-  const int ntx = (P.NXm + TXN - 1) / TXN, nty = (P.NY + TR - 1) / TR;
+  const int ntx = (P.NXm + TXN - 1) / TXN, nty = (P.NY + TY - 1) / TY;
   const int nb_main = P.NXm > 0 ? pl.main_blocks : 0;
   const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, pl.n_items == 0 ? 1 : 0, nb_main, skip};
   // measurement switch (scripts only): AFEM_STENCIL_ONLY=main|items launches one of the two kernels
@@ -1255,10 +1180,10 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
   if (kb >= ke) return;
   const DotArgs dot{nullptr, nullptr, nullptr, nullptr, 0, 0, nullptr};
   if (P.NXm > 0) {  // a piece is a few planes: smaller z chunks so the launch still fills the GPU
-    const int tiles = ((P.NXm + TXN - 1) / TXN) * ((P.NY + TR - 1) / TR);
+    const int tiles = ((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY);
     const int want = std::max(1, kMainBlocksPerSm * c.num_sms / std::max(tiles, 1));
     const int kc = std::max(4, (ke - kb + want - 1) / want);
-    const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TR - 1) / TR, (ke - kb + kc - 1) / kc);
+    const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TY - 1) / TY, (ke - kb + kc - 1) / kc);
     stencil_x_map(pl, x);
     launch(c, k_stencil_tma<false>, grid, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, kc, kb, ke, dot, 0, 0);
   }
