@@ -402,7 +402,7 @@ def ours(args, rank, world, local_rank):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record(stream)
-            du, rep = solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
+            du, rep = solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=200000)
             e1.record(stream)
             torch.cuda.synchronize()
             solve_s = e0.elapsed_time(e1) * 1e-3
@@ -441,7 +441,7 @@ def ours(args, rank, world, local_rank):
     if cg is not None:
         bh = b.cpu().numpy()
         t0 = time.perf_counter()
-        _, rep2 = solver(op, bh, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=20000)
+        _, rep2 = solver(op, bh, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=200000)
         e2e["cg_solve_s"] = time.perf_counter() - t0
         e2e["cg_iterations"] = rep2["iterations"]
 
