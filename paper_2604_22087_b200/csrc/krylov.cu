@@ -616,6 +616,44 @@ __device__ __forceinline__ void gm_reduce(const double (&acc)[kGmMax], int nv, d
   if (threadIdx.x == 0) *counter = 0u;
 }
 
+// Passes 1 and 2 are tiled: a CTA stages a tile of kGmTile rows of w in shared memory and each warp
+// streams whole basis vectors over the tile (warp w takes vectors w, w + 8, ...), so a lane keeps at
+// most kGmMax / 8 partial sums and issues kGmTile / 32 independent loads per vector — full occupancy
+// and memory-level parallelism (the per-thread form, 32 accumulators per thread at 100+ registers,
+// ran at 1.9-3.4 TB/s). Per-CTA partials per vector, then a fixed-order sum: deterministic.
+constexpr int kGmTile = 512;
+constexpr int kGmWarps = kRedThreads / 32;
+constexpr int kGmPerWarp = (kGmMax + kGmWarps - 1) / kGmWarps;
+
+// Each warp's partial sums of its vectors -> part[k * gridDim.x + block]; the last block sums them.
+__device__ __forceinline__ void gm_tile_reduce(const double (&acc)[kGmPerWarp], int nv, double* part,
+                                               unsigned int* counter, double* out) {
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < kGmPerWarp; ++q) {
+    const int k = w + kGmWarps * q;
+    double t = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0 && k < nv) part[k * gridDim.x + blockIdx.x] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int k = w; k < nv; k += kGmWarps) {  // one warp per inner product, fixed lane assignment
+    double t = 0.0;
+    for (unsigned b = lane; b < gridDim.x; b += 32) t += __ldcg(&part[k * gridDim.x + b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) out[k] = t;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
 // Step j's basis vector V_{nv-1} arrives unnormalised (pass 3 of the previous step writes
 // w - V h2 and its exact norm s): A V_{nv-1} was applied to it, so w = M^-1 src / s, and V_{nv-1} is
 // normalised in place here (s = 1 for the restart vector). Then h1[k] = V_k . w over the owned rows
@@ -624,62 +662,115 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_pass1(const double* __restri
                                                           double* w, double* V, int64_t ld, int nv, double s_last,
                                                           int64_t n, int64_t off, double* part, unsigned int* counter,
                                                           double* h1) {
-  double acc[kGmMax];
+  __shared__ double ws[kGmTile];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  double acc[kGmPerWarp];
 #pragma unroll
-  for (int k = 0; k < kGmMax; ++k) acc[k] = 0.0;
-  double* vl = V + (nv - 1) * ld;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double wi = src[i];
-    if (inv) wi *= inv[i];
-    double vlast = vl[i];
-    if (s_last != 1.0) {
-      wi /= s_last;
-      vlast /= s_last;
-      vl[i] = vlast;
+  for (int q = 0; q < kGmPerWarp; ++q) acc[q] = 0.0;
+  for (int64_t t0 = (int64_t)blockIdx.x * kGmTile; t0 < n; t0 += (int64_t)gridDim.x * kGmTile) {
+    for (int r = threadIdx.x; r < kGmTile; r += blockDim.x) {
+      const int64_t i = t0 + r;
+      double wi = 0.0;
+      if (i < n) {
+        wi = src[i];
+        if (inv) wi *= inv[i];
+        if (s_last != 1.0) wi /= s_last;
+        if (inv || s_last != 1.0) w[i] = wi;
+        if (i < off) wi = 0.0;  // not owned: no inner-product contribution
+      }
+      ws[r] = wi;
     }
-    if (inv || s_last != 1.0) w[i] = wi;
-    if (i >= off) {
+    __syncthreads();
 #pragma unroll
-      for (int k = 0; k < kGmMax - 1; ++k)
-        if (k < nv - 1) acc[k] += __ldcs(&V[k * ld + i]) * wi;
-#pragma unroll
-      for (int k = 0; k < kGmMax; ++k)
-        if (k == nv - 1) acc[k] += vlast * wi;
+    for (int q = 0; q < kGmPerWarp; ++q) {
+      const int k = wp + kGmWarps * q;
+      if (k >= nv) break;
+      double* vk = V + k * ld;
+      const bool norm = k == nv - 1 && s_last != 1.0;
+      double a = 0.0;
+#pragma unroll 4
+      for (int r = lane; r < kGmTile; r += 32) {
+        const int64_t i = t0 + r;
+        if (i >= n) break;
+        double v = norm ? vk[i] : __ldcs(&vk[i]);
+        if (norm) {
+          v /= s_last;
+          vk[i] = v;
+        }
+        a += v * ws[r];
+      }
+      acc[q] += a;
     }
+    __syncthreads();
   }
-  gm_reduce<false>(acc, nv, 0.0, part, counter, h1);
+  gm_tile_reduce(acc, nv, part, counter, h1);
 }
 
-// a load the compiler may not merge with an earlier one (keeps the first pass's values out of registers)
-__device__ __forceinline__ double gm_reload(const double* p) {
-  double v;
-  asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
-
-// w -= V h1 (in place); h2[k] = V_k . w (k < nv), owned rows.
+// w -= V h1 (in place); h2[k] = V_k . w (k < nv), owned rows. Per tile: every warp forms the
+// contributions of its vectors to all tile rows (shared-memory rows, one per warp), the rows are
+// summed over the warps in a fixed order, then the warps stream their vectors again (L1 / L2 hits)
+// against the updated tile.
 __global__ void __launch_bounds__(kRedThreads) k_gm_pass2(double* w, const double* __restrict__ V, int64_t ld, int nv,
                                                           const double* __restrict__ h1, int64_t n, int64_t off,
                                                           double* part, unsigned int* counter, double* h2) {
-  __shared__ double hs[kGmMax];
-  if (threadIdx.x < nv) hs[threadIdx.x] = h1[threadIdx.x];
-  __syncthreads();
-  double acc[kGmMax];
+  __shared__ double ws[kGmTile];
+  __shared__ double cs[kGmWarps][kGmTile];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  double hk[kGmPerWarp];
 #pragma unroll
-  for (int k = 0; k < kGmMax; ++k) acc[k] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double wi = w[i];
-#pragma unroll
-    for (int k = 0; k < kGmMax; ++k)
-      if (k < nv) wi -= hs[k] * V[k * ld + i];
-    w[i] = wi;
-    if (i >= off) {
-#pragma unroll
-      for (int k = 0; k < kGmMax; ++k)
-        if (k < nv) acc[k] += gm_reload(&V[k * ld + i]) * wi;  // second touch: L1/L2
-    }
+  for (int q = 0; q < kGmPerWarp; ++q) {
+    const int k = wp + kGmWarps * q;
+    hk[q] = k < nv ? h1[k] : 0.0;
   }
-  gm_reduce<false>(acc, nv, 0.0, part, counter, h2);
+  double acc[kGmPerWarp];
+#pragma unroll
+  for (int q = 0; q < kGmPerWarp; ++q) acc[q] = 0.0;
+  for (int64_t t0 = (int64_t)blockIdx.x * kGmTile; t0 < n; t0 += (int64_t)gridDim.x * kGmTile) {
+    // this warp's vectors' contributions h1[k] V_k over the tile
+    for (int r = lane; r < kGmTile; r += 32) {
+      const int64_t i = t0 + r;
+      double c = 0.0;
+      if (i < n) {
+#pragma unroll
+        for (int q = 0; q < kGmPerWarp; ++q) {
+          const int k = wp + kGmWarps * q;
+          if (k < nv) c += hk[q] * V[k * ld + i];
+        }
+      }
+      cs[wp][r] = c;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < kGmTile; r += blockDim.x) {
+      const int64_t i = t0 + r;
+      if (i >= n) {
+        ws[r] = 0.0;
+        continue;
+      }
+      double c = 0.0;
+#pragma unroll
+      for (int q = 0; q < kGmWarps; ++q) c += cs[q][r];  // fixed order over the warps
+      const double wi = w[i] - c;
+      w[i] = wi;
+      ws[r] = i < off ? 0.0 : wi;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kGmPerWarp; ++q) {
+      const int k = wp + kGmWarps * q;
+      if (k >= nv) break;
+      const double* vk = V + k * ld;
+      double a = 0.0;
+#pragma unroll 4
+      for (int r = lane; r < kGmTile; r += 32) {
+        const int64_t i = t0 + r;
+        if (i >= n) break;
+        a += vk[i] * ws[r];  // second touch of the tile: L1 / L2
+      }
+      acc[q] += a;
+    }
+    __syncthreads();
+  }
+  gm_tile_reduce(acc, nv, part, counter, h2);
 }
 
 // vnext = w - V h2 (left unnormalised: pass 1 of the next step divides by its norm) and

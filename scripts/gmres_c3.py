@@ -37,7 +37,6 @@ def run_one(n, iters):
     t = time.perf_counter()
     _, rep = afem.run_solver(op, b, method=afem.GMRES, precond=afem.JACOBI, rtol=1e-12, max_iter=iters, restart=30)
     dt = time.perf_counter() - t
-    xs = afem.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-12, max_iter=100)[1]
     return dict(n=n, n_dof=s.n, iterations=rep["iterations"], time_s=dt, ms_per_iteration=1e3 * dt / rep["iterations"],
                 final_rres=float(rep["residual_history"][-1]))
 
