@@ -616,27 +616,40 @@ __device__ __forceinline__ void gm_reduce(const double (&acc)[kGmMax], int nv, d
   if (threadIdx.x == 0) *counter = 0u;
 }
 
-// Passes 1 and 2 are tiled: a CTA stages a tile of kGmTile rows of w in shared memory and each warp
-// streams whole basis vectors over the tile (warp w takes vectors w, w + 8, ...), so a lane keeps at
-// most kGmMax / 8 partial sums and issues kGmTile / 32 independent loads per vector — full occupancy
-// and memory-level parallelism (the per-thread form, 32 accumulators per thread at 100+ registers,
-// ran at 1.9-3.4 TB/s). Per-CTA partials per vector, then a fixed-order sum: deterministic.
-constexpr int kGmTile = 512;
-constexpr int kGmWarps = kRedThreads / 32;
-constexpr int kGmPerWarp = (kGmMax + kGmWarps - 1) / kGmWarps;
+// Passes 1 and 2: one row per thread; the row's products with the (up to 32) basis vectors are
+// reduced across the warp by a transpose-reduction (5 halving exchange steps, 31 shuffles in all),
+// after which lane k holds the warp's sum for vector k and keeps ONE running partial sum. Every
+// load of a row is independent (all 32 in flight) and no per-vector accumulators live across the
+// row loop — the per-thread form with 32 accumulators ran at 1.9-3.4 TB/s. Fixed shuffle order and
+// fixed per-CTA / cross-CTA reduction order: deterministic.
+__device__ __forceinline__ double warp_transpose_reduce(double (&p)[kGmMax]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const double send = upper ? p[k] : p[k + o];
+      const double keep = upper ? p[k + o] : p[k];
+      p[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return p[0];  // lane L: the sum over the warp's lanes of p[L]
+}
 
-// Each warp's partial sums of its vectors -> part[k * gridDim.x + block]; the last block sums them.
-__device__ __forceinline__ void gm_tile_reduce(const double (&acc)[kGmPerWarp], int nv, double* part,
-                                               unsigned int* counter, double* out) {
+// Block sum of every lane's single partial (lane k = vector k) -> part[k * gridDim.x + block]; the
+// last block sums the partials of each vector in block order.
+__device__ __forceinline__ void gm_lane_reduce(double acc, int nv, double* part, unsigned int* counter,
+                                               double* out) {
+  __shared__ double sh[kRedThreads / 32][32];
   __shared__ bool last;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < kGmPerWarp; ++q) {
-    const int k = w + kGmWarps * q;
-    double t = acc[q];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0 && k < nv) part[k * gridDim.x + blockIdx.x] = t;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  sh[w][lane] = acc;
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double t = 0.0;
+    for (int q = 0; q < nw; ++q) t += sh[q][threadIdx.x];
+    part[threadIdx.x * gridDim.x + blockIdx.x] = t;
   }
   __threadfence();
   __syncthreads();
@@ -644,7 +657,7 @@ __device__ __forceinline__ void gm_tile_reduce(const double (&acc)[kGmPerWarp], 
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int k = w; k < nv; k += kGmWarps) {  // one warp per inner product, fixed lane assignment
+  for (int k = w; k < nv; k += nw) {
     double t = 0.0;
     for (unsigned b = lane; b < gridDim.x; b += 32) t += __ldcg(&part[k * gridDim.x + b]);
 #pragma unroll
@@ -662,115 +675,66 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_pass1(const double* __restri
                                                           double* w, double* V, int64_t ld, int nv, double s_last,
                                                           int64_t n, int64_t off, double* part, unsigned int* counter,
                                                           double* h1) {
-  __shared__ double ws[kGmTile];
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  double acc[kGmPerWarp];
-#pragma unroll
-  for (int q = 0; q < kGmPerWarp; ++q) acc[q] = 0.0;
-  for (int64_t t0 = (int64_t)blockIdx.x * kGmTile; t0 < n; t0 += (int64_t)gridDim.x * kGmTile) {
-    for (int r = threadIdx.x; r < kGmTile; r += blockDim.x) {
-      const int64_t i = t0 + r;
-      double wi = 0.0;
-      if (i < n) {
-        wi = src[i];
-        if (inv) wi *= inv[i];
-        if (s_last != 1.0) wi /= s_last;
-        if (inv || s_last != 1.0) w[i] = wi;
-        if (i < off) wi = 0.0;  // not owned: no inner-product contribution
-      }
-      ws[r] = wi;
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // whole warps iterate (rows past n contribute zeros) so the shuffles always see 32 lanes
+  const int64_t n_up = (n + 31) / 32 * 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < n_up; i += stride) {
+    const bool in = i < n;
+    double wi = 0.0;
+    if (in) {
+      wi = src[i];
+      if (inv) wi *= inv[i];
+      if (s_last != 1.0) wi /= s_last;
+      if (inv || s_last != 1.0) w[i] = wi;
     }
-    __syncthreads();
+    const double wd = in && i >= off ? wi : 0.0;
+    double p[kGmMax];
 #pragma unroll
-    for (int q = 0; q < kGmPerWarp; ++q) {
-      const int k = wp + kGmWarps * q;
-      if (k >= nv) break;
-      double* vk = V + k * ld;
-      const bool norm = k == nv - 1 && s_last != 1.0;
-      double a = 0.0;
-#pragma unroll 4
-      for (int r = lane; r < kGmTile; r += 32) {
-        const int64_t i = t0 + r;
-        if (i >= n) break;
-        double v = norm ? vk[i] : __ldcs(&vk[i]);
-        if (norm) {
+    for (int k = 0; k < kGmMax; ++k) {
+      double v = 0.0;
+      if (k < nv && in) {
+        v = __ldcs(&V[k * ld + i]);
+        if (k == nv - 1 && s_last != 1.0) {
           v /= s_last;
-          vk[i] = v;
+          V[k * ld + i] = v;
         }
-        a += v * ws[r];
       }
-      acc[q] += a;
+      p[k] = v * wd;
     }
-    __syncthreads();
+    acc += warp_transpose_reduce(p);
   }
-  gm_tile_reduce(acc, nv, part, counter, h1);
+  gm_lane_reduce(lane < nv ? acc : 0.0, nv, part, counter, h1);
 }
 
-// w -= V h1 (in place); h2[k] = V_k . w (k < nv), owned rows. Per tile: every warp forms the
-// contributions of its vectors to all tile rows (shared-memory rows, one per warp), the rows are
-// summed over the warps in a fixed order, then the warps stream their vectors again (L1 / L2 hits)
-// against the updated tile.
+// w -= V h1 (in place); h2[k] = V_k . w (k < nv), owned rows. The row's basis values stay in
+// registers between the update and the products (V is read once).
 __global__ void __launch_bounds__(kRedThreads) k_gm_pass2(double* w, const double* __restrict__ V, int64_t ld, int nv,
                                                           const double* __restrict__ h1, int64_t n, int64_t off,
                                                           double* part, unsigned int* counter, double* h2) {
-  __shared__ double ws[kGmTile];
-  __shared__ double cs[kGmWarps][kGmTile];
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  double hk[kGmPerWarp];
+  __shared__ double hs[kGmMax];
+  if (threadIdx.x < kGmMax) hs[threadIdx.x] = threadIdx.x < nv ? h1[threadIdx.x] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n_up = (n + 31) / 32 * 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - lane < n_up; i += stride) {
+    const bool in = i < n;
+    double p[kGmMax];
 #pragma unroll
-  for (int q = 0; q < kGmPerWarp; ++q) {
-    const int k = wp + kGmWarps * q;
-    hk[q] = k < nv ? h1[k] : 0.0;
+    for (int k = 0; k < kGmMax; ++k) p[k] = (k < nv && in) ? __ldcs(&V[k * ld + i]) : 0.0;
+    double wi = in ? w[i] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kGmMax; ++k) wi -= hs[k] * p[k];
+    if (in) w[i] = wi;
+    const double wd = in && i >= off ? wi : 0.0;
+#pragma unroll
+    for (int k = 0; k < kGmMax; ++k) p[k] *= wd;
+    acc += warp_transpose_reduce(p);
   }
-  double acc[kGmPerWarp];
-#pragma unroll
-  for (int q = 0; q < kGmPerWarp; ++q) acc[q] = 0.0;
-  for (int64_t t0 = (int64_t)blockIdx.x * kGmTile; t0 < n; t0 += (int64_t)gridDim.x * kGmTile) {
-    // this warp's vectors' contributions h1[k] V_k over the tile
-    for (int r = lane; r < kGmTile; r += 32) {
-      const int64_t i = t0 + r;
-      double c = 0.0;
-      if (i < n) {
-#pragma unroll
-        for (int q = 0; q < kGmPerWarp; ++q) {
-          const int k = wp + kGmWarps * q;
-          if (k < nv) c += hk[q] * V[k * ld + i];
-        }
-      }
-      cs[wp][r] = c;
-    }
-    __syncthreads();
-    for (int r = threadIdx.x; r < kGmTile; r += blockDim.x) {
-      const int64_t i = t0 + r;
-      if (i >= n) {
-        ws[r] = 0.0;
-        continue;
-      }
-      double c = 0.0;
-#pragma unroll
-      for (int q = 0; q < kGmWarps; ++q) c += cs[q][r];  // fixed order over the warps
-      const double wi = w[i] - c;
-      w[i] = wi;
-      ws[r] = i < off ? 0.0 : wi;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kGmPerWarp; ++q) {
-      const int k = wp + kGmWarps * q;
-      if (k >= nv) break;
-      const double* vk = V + k * ld;
-      double a = 0.0;
-#pragma unroll 4
-      for (int r = lane; r < kGmTile; r += 32) {
-        const int64_t i = t0 + r;
-        if (i >= n) break;
-        a += vk[i] * ws[r];  // second touch of the tile: L1 / L2
-      }
-      acc[q] += a;
-    }
-    __syncthreads();
-  }
-  gm_tile_reduce(acc, nv, part, counter, h2);
+  gm_lane_reduce(lane < nv ? acc : 0.0, nv, part, counter, h2);
 }
 
 // vnext = w - V h2 (left unnormalised: pass 1 of the next step divides by its norm) and

@@ -50,7 +50,7 @@ def main():
     if a.child:
         print(json.dumps(run_one(a.n, a.iters)))
         return
-    for mgs in (False, True):
+    for mgs in (False, True, False, True):  # alternated: the box's power state drifts over a run
         env = dict(os.environ)
         env.pop("AFEM_GMRES_MGS", None)
         if mgs:
