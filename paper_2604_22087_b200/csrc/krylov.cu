@@ -676,6 +676,7 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_pass1(const double* __restri
                                                           int64_t n, int64_t off, double* part, unsigned int* counter,
                                                           double* h1) {
   const int lane = threadIdx.x & 31;
+  const double rs = 1.0 / s_last;  // one division per thread, not two per row (fp64 division is slow)
   double acc = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   // whole warps iterate (rows past n contribute zeros) so the shuffles always see 32 lanes
@@ -686,7 +687,7 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_pass1(const double* __restri
     if (in) {
       wi = src[i];
       if (inv) wi *= inv[i];
-      if (s_last != 1.0) wi /= s_last;
+      if (s_last != 1.0) wi *= rs;
       if (inv || s_last != 1.0) w[i] = wi;
     }
     const double wd = in && i >= off ? wi : 0.0;
@@ -697,7 +698,7 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_pass1(const double* __restri
       if (k < nv && in) {
         v = __ldcs(&V[k * ld + i]);
         if (k == nv - 1 && s_last != 1.0) {
-          v /= s_last;
+          v *= rs;
           V[k * ld + i] = v;
         }
       }
