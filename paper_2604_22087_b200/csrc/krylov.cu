@@ -693,17 +693,17 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_pass1(const double* __restri
     const double wd = in && i >= off ? wi : 0.0;
     double p[kGmMax];
 #pragma unroll
-    for (int k = 0; k < kGmMax; ++k) {
-      double v = 0.0;
-      if (k < nv && in) {
-        v = __ldcs(&V[k * ld + i]);
-        if (k == nv - 1 && s_last != 1.0) {
-          v *= rs;
-          V[k * ld + i] = v;
+    for (int k = 0; k < kGmMax; ++k) p[k] = (k < nv && in) ? __ldcs(&V[k * ld + i]) : 0.0;  // all loads first
+    if (s_last != 1.0 && in) {  // normalise the last vector in place (after the loads: no aliasing barrier)
+#pragma unroll
+      for (int k = 0; k < kGmMax; ++k)
+        if (k == nv - 1) {
+          p[k] *= rs;
+          V[k * ld + i] = p[k];
         }
-      }
-      p[k] = v * wd;
     }
+#pragma unroll
+    for (int k = 0; k < kGmMax; ++k) p[k] *= wd;
     acc += warp_transpose_reduce(p);
   }
   gm_lane_reduce(lane < nv ? acc : 0.0, nv, part, counter, h1);
