@@ -1,6 +1,6 @@
 #!/bin/bash
 # C5 single-GPU points: the device-resident matrix-free apply (bench.py --n N, L2 flushed between
-# applies) of the linear hex8 fibre RVE at N in {128,160,202,254,321,404}: 6.4 M -> 199 M dofs.
+# applies; round 2: rotating buffers) of the linear hex8 fibre RVE at N in {128,...,404}: 6.4 M -> 199 M dofs.
 mkdir -p gpurun_out
 for N in 128 160 202 254 321 404; do
   timeout 900 python bench.py --n $N --steps 10 --warmup 3 --no-cpu --e2e-steps 1 --no-cg > gpurun_out/sweep_$N.json 2> gpurun_out/sweep_$N.err
