@@ -70,7 +70,6 @@ struct StencilPlan {
   DevArray<double> Ed;   // modulus per phase code (32), device copy for the item kernel
   int item_blocks = 1;
   DevArray<double> part_main, part_items;  // fused p.Ap partials (main kernel, item kernel)
-  DevArray<double> yc;   // per-item correction slots of the concurrent items launch (3 per item)
   DevArray<unsigned int> counter;
   DevArray<double> Kg;   // Khat (row-major 24 x 24)
   RowsK0 k0;             // the correction kernel's coefficients
@@ -585,8 +584,7 @@ __global__ void __launch_bounds__(kItemThreads, AFEM_ITEM_MINB) k_stencil_items(
                                                                  const double* __restrict__ Epar,
                                                                  const double* __restrict__ x,
                                                                  const uint8_t* __restrict__ info, Items it,
-                                                                 double* __restrict__ y, DotArgs dot,
-                                                                 double* __restrict__ yc) {
+                                                                 double* __restrict__ y, DotArgs dot) {
   if (dot.skip && *dot.skip) return;
   __shared__ double Es[32];
   __shared__ __align__(16) double Ks[3][24];  // every lane reads the same word: broadcasts, 16-byte pairs
@@ -624,7 +622,7 @@ __global__ void __launch_bounds__(kItemThreads, AFEM_ITEM_MINB) k_stencil_items(
       inf = __ldg(&info[node]);
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        if (!edge && !yc) yn[a] = y[3 * (int64_t)node + a];
+        if (!edge) yn[a] = y[3 * (int64_t)node + a];
         if (DOT || edge) xn3[a] = __ldg(&x[3 * (int64_t)node + a]);
       }
     }
@@ -683,8 +681,6 @@ __global__ void __launch_bounds__(kItemThreads, AFEM_ITEM_MINB) k_stencil_items(
           const double ya = con ? xn3[a] : rr3[a];
           yo[a] = ya;
           if constexpr (DOT) dsum = fma(xn3[a], ya, dsum);
-        } else if (yc) {  // concurrent with the main kernel: the correction goes to its item slot
-          yc[3 * (bt * 32 + lane) + a] = con ? 0.0 : rr3[a];
         } else if (!con) {
           yo[a] = yn[a] + rr3[a];
           if constexpr (DOT) dsum = fma(xn3[a], rr3[a], dsum);
@@ -695,19 +691,6 @@ __global__ void __launch_bounds__(kItemThreads, AFEM_ITEM_MINB) k_stencil_items(
   if constexpr (DOT)
     block_to_slot_and_finish(dsum, dot.part_items, blockIdx.x, gridDim.x, dot.part_main, dot.n_main, dot.counter,
                              dot.out);
-}
-
-// After a concurrent items launch: y_n += the correction its segment head left in yc (main kernel done).
-__global__ void k_items_fixup(const uint64_t* __restrict__ rec, const double* __restrict__ yc, double* __restrict__ y,
-                              int64_t n) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t r = __ldg(&rec[t]);
-    const int node = static_cast<int>(static_cast<uint32_t>(r));
-    const uint32_t w = static_cast<uint32_t>(r >> 32);
-    if (node < 0 || ((w >> 3) & 15) == 0 || ((w >> 7) & 1)) continue;  // not a head, or an edge column
-#pragma unroll
-    for (int a = 0; a < 3; ++a) y[3 * (int64_t)node + a] += yc[3 * t + a];
-  }
 }
 
 // Per node: info byte (Dirichlet bits | base phase << 3) and, for nodes of the main kernel whose
@@ -1152,7 +1135,7 @@ void stencil_apply(StencilPlan& pl, const MfOp& op, const double* x, double* y, 
     AFEM_CK(cudaGraphInstantiate(&slot->exec, g, 0));
   }
   AFEM_CK(cudaGraphLaunch(slot->exec, c.stream));
-  c.launches += (pl.p.NXm > 0 ? 1 : 0) + (pl.n_items > 0 ? (std::getenv("AFEM_ITEMS_SERIAL") ? 1 : 2) : 0);
+  c.launches += (pl.p.NXm > 0 ? 1 : 0) + (pl.n_items > 0 ? 1 : 0);
 }
 
 static void stencil_apply_launch(StencilPlan& pl, const MfOp& op, const double* x, double* y, double* dot_out,
@@ -1165,19 +1148,6 @@ static void stencil_apply_launch(StencilPlan& pl, const MfOp& op, const double* 
   // measurement switch (scripts only): AFEM_STENCIL_ONLY=main|items launches one of the two kernels
   static const char* only = std::getenv("AFEM_STENCIL_ONLY");
   const bool run_main = !only || only[0] == 'm', run_items = !only || only[0] == 'i';
-  // Plain apply: the correction items run CONCURRENTLY with the main kernel on a second stream
-  // (main leaves room for one item CTA per SM: 88 registers x 512 threads), each segment head
-  // parking its correction in an item slot (yc); a small fixup adds the slots into y once both are
-  // done. Same arithmetic as the sequential order (y = main + correction). The fused-dot and
-  // skip-flag variants (CG) stay sequential. AFEM_ITEMS_SERIAL=1: always sequential.
-  static const bool serial = std::getenv("AFEM_ITEMS_SERIAL") != nullptr;
-  const bool conc = !serial && !dot_out && !skip && run_main && run_items && nb_main > 0 && pl.n_items > 0;
-  if (conc) {
-    if (pl.yc.n < static_cast<size_t>(3 * pl.n_items)) pl.yc.alloc(3 * pl.n_items);
-    c.copy_streams(2);
-    AFEM_CK(cudaEventRecord(c.events[0], c.stream));
-    AFEM_CK(cudaStreamWaitEvent(c.s_in, c.events[0], 0));
-  }
   if (P.NXm > 0 && run_main) {  // balanced single wave (kchunk 0)
     stencil_x_map(pl, x);
     if (dot_out)
@@ -1189,23 +1159,12 @@ static void stencil_apply_launch(StencilPlan& pl, const MfOp& op, const double* 
   }
   if (pl.n_items > 0 && run_items) {
     const Items it{pl.it_rec.p, pl.it_zm.p, pl.n_items};
-    if (conc) {
-      // launched after main on its own stream: the block scheduler fills the SMs' spare slots
-      cudaStream_t main_stream = c.stream;
-      c.stream = c.s_in;
-      launch(c, k_stencil_items<false>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p,
-             it, y, dot, pl.yc.p);
-      c.stream = main_stream;
-      AFEM_CK(cudaEventRecord(c.events[1], c.s_in));
-      AFEM_CK(cudaStreamWaitEvent(c.stream, c.events[1], 0));
-      launch(c, k_items_fixup, grid_for(pl.n_items, 256, 148 * 8), 256, 0, pl.it_rec.p, pl.yc.p, y, pl.n_items);
-    } else if (dot_out) {
+    if (dot_out)
       launch(c, k_stencil_items<true>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p,
-             it, y, dot, nullptr);
-    } else {
+             it, y, dot);
+    else
       launch(c, k_stencil_items<false>, pl.item_blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p,
-             it, y, dot, nullptr);
-    }
+             it, y, dot);
   }
 }
 
@@ -1232,8 +1191,7 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
   if (i1 > i0) {
     const Items it{pl.it_rec.p + i0, pl.it_zm.p + i0, i1 - i0};
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((i1 - i0) / 256, (int64_t)pl.iocc * c.num_sms)));
-    launch(c, k_stencil_items<false>, blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p, it, y, dot,
-           nullptr);
+    launch(c, k_stencil_items<false>, blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p, it, y, dot);
   }
 }
 
