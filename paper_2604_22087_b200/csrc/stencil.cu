@@ -8,16 +8,18 @@
 // half / quarter families on y and z boundary faces (the void octants are dropped exactly by the
 // coefficients), and E_base(n) the majority modulus over F(n) (octants void in x count as E = 0).
 //
-// Kernels (DESIGN.md §Kernels):
-//  k_stencil_main   64x8 node tile per CTA (8 warps, one row per warp, 2 nodes per lane), marching
-//                   in z over a chunk of planes (one wave); each x-plane (one-node halo) is staged
-//                   once in shared memory in the interleaved dof layout with cp.async (zero-fill out
-//                   of the domain, Dirichlet masks applied after landing; double-buffered, one
-//                   barrier per plane) and each lane keeps the partial sums of the six column nodes
-//                   the plane touches. 153 DFMA per interior node (the 243-entry stencil minus the
-//                   90 symmetry zeros) over 30 symmetry-unique coefficients held in (uniform)
-//                   registers; y/z faces switch to the half/quarter families (warp- or CTA-uniform).
-//                   No atomics; every y entry of the covered columns is written exactly once.
+// Kernels (DESIGN.md §4):
+//  k_stencil_tma    64x4 node tile per CTA (4 warps, one row per warp, 2 nodes per lane; one wave of
+//                   4 CTAs per SM, each taking an equal contiguous range of (tile, plane) units),
+//                   marching in z. Each plane's TY + 2 staged rows (one-node halo, interleaved dofs)
+//                   and their info bytes arrive by TMA (rank-1 cp.async.bulk.tensor copies issued by
+//                   lane 0 of every warp, one mbarrier per ring slot, a 4-slot ring); out-of-range
+//                   columns and Dirichlet dofs are zeroed after landing from the staged info bytes.
+//                   Each lane keeps the partial sums of the six column nodes a plane touches. 153
+//                   DFMA per interior node (the 243-entry stencil minus the 90 symmetry zeros) over
+//                   30 symmetry-unique coefficients in uniform registers; y / z faces switch to the
+//                   half / quarter families (warp- or CTA-uniform). No atomics; every y entry of the
+//                   covered columns is written exactly once; optional fused x.y partials (CG p.Ap).
 //  k_stencil_items  one thread per (node, octant) correction: mixed-family nodes (fibre
 //                   interfaces, the x = 0 face) add dE Khat_rows x_e; the NX mod 64 edge columns are
 //                   written in exact octant form. Segmented, fixed-order shuffle sums per node.
@@ -304,7 +306,7 @@ constexpr int RING = 2 * PPB + (PPB == 1 ? 2 : 1);
 // k_stencil_tma: the main kernel with Blackwell bulk-async staging. Per CTA plane the (TY + 2)
 // rows of the 64 + 2 node window (interleaved dofs) and their info bytes arrive by TMA: rank-1
 // tensor copies (cp.async.bulk.tensor.1d; boxes start on 16-byte boundaries, zero fill outside
-// [0, n)) issued by one thread and completed on one mbarrier per ring slot — no per-thread address
+// [0, n)) issued by lane 0 of each warp and completed on one mbarrier per ring slot — no per-thread address
 // arithmetic and no registers spent on staging. x rows: the box starts at the even element at or
 // below the row's first dof, so a row lands 0 or 1 double in (its parity, known to every thread;
 // load_window reads either). Info rows come from a padded copy of the info bytes (row pitch ipx, a
@@ -316,7 +318,7 @@ constexpr int RING = 2 * PPB + (PPB == 1 ? 2 : 1);
 // dof). Ring of 4 slots: plane p is computed, p + 1 is landed and masked, p + 2 is in flight, and
 // p + 3 is issued into p - 1's slot after the plane barrier (a proxy fence orders the threads'
 // generic writes before the async-proxy overwrite). Arithmetic, output order and the fused dot are
-// those of k_stencil_main, so the two kernels are bitwise identical.
+// those of the round-1 cp.async kernel (k_stencil_main, removed), so results are bitwise unchanged.
 constexpr int RSP = 208;             // staged row pitch (doubles): 200 landed, rows 128-byte aligned for TMA
 constexpr int IRP = 128;             // staged info row pitch (bytes)
 constexpr int XBOX = 3 * (TXN + 2) + 2;  // doubles per x box (the 198-dof window + alignment slack)
