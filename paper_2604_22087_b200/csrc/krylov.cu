@@ -1,9 +1,9 @@
 // Krylov solvers on the device: Jacobi-preconditioned CG (krylov.hpp:350-408) and restarted,
 // left-preconditioned GMRES(m) (krylov.hpp:415-530). The reference orthogonalises with modified
 // Gram-Schmidt; here each Arnoldi step is CGS2 (classical Gram-Schmidt twice) in three fused
-// kernels — Jacobi + all first-pass inner products, update + all second-pass inner products + the
-// norm, update + normalisation — with one host sync per step (the Givens rotations stay on the
-// host, as in the reference).
+// kernels — Jacobi + normalisation of the previous basis vector + all first-pass inner products,
+// update + all second-pass inner products, update + the new vector's exact norm — with one host
+// sync per step (the Givens rotations stay on the host, as in the reference).
 //
 // CG keeps every scalar (rz, pAp, alpha, beta, the residual history) in device memory. One
 // iteration is four launches — operator apply, pAp reduction, the fused x/r/z update with the
