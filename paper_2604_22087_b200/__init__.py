@@ -129,6 +129,11 @@ def load():
         "afem_jacobian": ([vp, vp, vp], i32),
         "afem_diagonal": ([vp, vp, vp], i32),
         "afem_eliminate": ([vp, vp, vp, vp], i32),
+        "afem_op_create_csr": ([vp, i64, i64, vp, vp, vp], i32),
+        "afem_op_set_values": ([vp, vp], i32),
+        "afem_eliminate_csr": ([vp, i64, i64, vp, vp, vp, vp, vp, vp, vp], i32),
+        "afem_constrain_masked": ([vp, i64, vp, vp, vp, vp], i32),
+        "afem_solve_bvp_ex": ([vp, vp, vp, vp, vp, vp, i32, vp, i32], i32),
         "afem_constrain_residual": ([vp, vp, vp], i32),
         "afem_csr_apply": ([vp, vp, vp, vp], i32),
         "afem_free_norm": ([vp, vp, vp], i32),
