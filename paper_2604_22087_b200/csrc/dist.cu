@@ -276,7 +276,9 @@ void DistMfOp::apply(const double* x, double* y) {
   }
   StencilPlan* pl = local->stencil;
   const int P = pl ? stencil_pieces(*pl) : 0;
-  if (comm->size == 1 || P < 3) {
+  // measurement switch (scripts/dist_apply_probe.py): the overlapped piece schedule even at world 1
+  static const bool force_pieces = std::getenv("AFEM_DIST_FORCE_PIECES") != nullptr;
+  if ((comm->size == 1 && !force_pieces) || P < 3) {
     local->apply(x, y);
     halo_add(y, x, false);
     return;

@@ -1181,13 +1181,22 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
   const int kb = pa * pl.zpiece, ke = std::min(pb * pl.zpiece, P.NZ);
   if (kb >= ke) return;
   const DotArgs dot{nullptr, nullptr, nullptr, nullptr, 0, 0, nullptr};
-  if (P.NXm > 0) {  // a piece is a few planes: smaller z chunks so the launch still fills the GPU
-    const int tiles = ((P.NXm + TXN - 1) / TXN) * ((P.NY + TY - 1) / TY);
-    const int want = std::max(1, kMainBlocksPerSm * c.num_sms / std::max(tiles, 1));
-    const int kc = std::max(4, (ke - kb + want - 1) / want);
-    const dim3 grid((P.NXm + TXN - 1) / TXN, (P.NY + TY - 1) / TY, (ke - kb + kc - 1) / kc);
+  if (P.NXm > 0) {
+    const int ntx = (P.NXm + TXN - 1) / TXN, nty = (P.NY + TY - 1) / TY;
+    const int64_t units = (int64_t)ntx * nty * (ke - kb);
     stencil_x_map(pl, x);
-    launch(c, k_stencil_tma<false>, grid, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, kc, kb, ke, dot, 0, 0);
+    static const bool chunked = std::getenv("AFEM_PIECES_CHUNKED") != nullptr;  // A/B switch
+    if (!chunked && units >= 8 * (int64_t)pl.main_blocks) {  // a long z range (the slab interior): one balanced wave
+      launch(c, k_stencil_tma<false>, pl.main_blocks, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, kb,
+             ke, dot, ntx, nty);
+    } else {  // a piece is a few planes: smaller z chunks so the launch still fills the GPU
+      const int tiles = ntx * nty;
+      const int want = std::max(1, kMainBlocksPerSm * c.num_sms / std::max(tiles, 1));
+      const int kc = std::max(4, (ke - kb + want - 1) / want);
+      const dim3 grid(ntx, nty, (ke - kb + kc - 1) / kc);
+      launch(c, k_stencil_tma<false>, grid, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, kc, kb, ke, dot, 0,
+             0);
+    }
   }
   const int64_t i0 = pl.piece_items[pa], i1 = pl.piece_items[pb];
   if (i1 > i0) {
