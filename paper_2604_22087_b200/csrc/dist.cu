@@ -276,9 +276,15 @@ void DistMfOp::apply(const double* x, double* y) {
   }
   StencilPlan* pl = local->stencil;
   const int P = pl ? stencil_pieces(*pl) : 0;
-  // measurement switch (scripts/dist_apply_probe.py): the overlapped piece schedule even at world 1
+  // Default: the single-wave apply of the whole slab, then the plane exchange and the halo add.
+  // The overlapped piece schedule below (shared-plane pieces first, the exchange on a second stream
+  // under the interior pieces) costs more than it hides at these slab sizes: measured per rank on
+  // one B200 (scripts/dist_apply_probe.py, AFEM_DIST_FORCE_PIECES at world 1) 112.8 vs 72.5 us at
+  // 128^3 and 437.6 vs 390.1 us at 256^3, against a ~10-20 us plane exchange over NVLink.
+  // AFEM_DIST_OVERLAP=1 selects it; AFEM_DIST_FORCE_PIECES=1 also at world 1 (measurement).
+  static const bool overlap = std::getenv("AFEM_DIST_OVERLAP") != nullptr;
   static const bool force_pieces = std::getenv("AFEM_DIST_FORCE_PIECES") != nullptr;
-  if ((comm->size == 1 && !force_pieces) || P < 3) {
+  if (!force_pieces && (!overlap || comm->size == 1) || P < 3) {
     local->apply(x, y);
     halo_add(y, x, false);
     return;

@@ -360,3 +360,49 @@ def test_distributed_capability_errors(afem):
             d.run_solver(dop, b, method=method, precond=precond, rtol=1e-8, max_iter=10)
     with pytest.raises(afem.AfemError):
         d.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-8, max_iter=10)
+
+
+OVERLAP_SNIPPET = r"""
+import sys, threading, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2604_22087_b200 as afem
+NX, NY, NZ, size = 64, 10, 64, 2
+LIN = [(0, 1.0, 0.3), (0, 10.0, 0.3)]
+ctx = afem.Context(0)
+fib = afem.fibres(12345, 6)
+s = afem.System.grid(ctx, 3, NX, NY, NZ, inclusions=fib, radius=0.15, materials=LIN)
+s.set_benchmark_dirichlet(0.01)
+u = s.impose_dirichlet(np.zeros(s.n))
+x = np.random.default_rng(1).uniform(-1, 1, s.n)
+yg = afem.matrix_free_operator(s, u).apply(x)
+group = afem.ThreadGroup(size)
+plane = 3 * (NX + 1) * (NY + 1)
+res = {{}}
+def work(rank):
+    c = afem.Context(0)
+    ss, (z0, z1) = afem.slab_system(c, NX, NY, NZ, rank, size, inclusions=fib, radius=0.15, materials=LIN)
+    d = afem.Dist(c, rank, size, backend="threads", group=group)
+    d.set_benchmark_dirichlet(ss, 0.01)
+    op = d.matrix_free_operator(ss, ss.impose_dirichlet(np.zeros(ss.n)))
+    sl = slice(plane * z0, plane * (z1 + 1))
+    res[rank] = float(np.abs(op.apply(x[sl]) - yg[sl]).max() / np.abs(yg).max())
+th = [threading.Thread(target=work, args=(r,)) for r in range(size)]
+[t.start() for t in th]
+[t.join() for t in th]
+print(max(res.values()))
+"""
+
+
+def test_overlapped_slab_schedule_matches_single_domain():
+    """The overlapped piece schedule (AFEM_DIST_OVERLAP=1: shared-plane pieces, the exchange on a
+    second stream under the interior pieces) gives the single-domain apply, like the default
+    schedule (whole-slab apply, then exchange)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, AFEM_DIST_OVERLAP="1")
+    p = subprocess.run([sys.executable, "-c", OVERLAP_SNIPPET.format(root=root)], capture_output=True, text=True,
+                       env=env, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    assert float(p.stdout.strip().splitlines()[-1]) <= 1e-12
