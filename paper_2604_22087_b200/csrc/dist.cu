@@ -264,10 +264,12 @@ void DistMfOp::halo_finish(double* v, const double* x_for_mask, bool diag_mode) 
   }
 }
 
-// Halo exchange overlapped with the interior: the z pieces holding the two shared node planes are
-// applied first, the planes go to the neighbours straight from y on a second stream (NCCL
-// send/recv), the interior pieces run meanwhile on the context stream, which then waits for the
-// exchange and adds the received partial sums. Same arithmetic as apply + halo_add.
+// Halo exchange overlapped with the interior: the two shared node planes are applied first on a
+// second stream (a one-plane launch each, main kernel + their correction items), sent to the
+// neighbours from y there (NCCL send/recv), while the interior planes run as one balanced wave on
+// the context stream, which then waits for the exchange and adds the received partial sums. The
+// boundary launches fit beside the interior wave (a fifth CTA per SM), so the exchange is hidden
+// under the interior. Same arithmetic as apply + halo_add. AFEM_DIST_OVERLAP=0: apply, then halo.
 void DistMfOp::apply(const double* x, double* y) {
   if (!local) {  // assembled: local SpMV (partial sums on the shared planes) + halo
     csr_apply(*sys, vals.p, x, y);
@@ -275,16 +277,12 @@ void DistMfOp::apply(const double* x, double* y) {
     return;
   }
   StencilPlan* pl = local->stencil;
-  const int P = pl ? stencil_pieces(*pl) : 0;
-  // Default: the single-wave apply of the whole slab, then the plane exchange and the halo add.
-  // The overlapped piece schedule below (shared-plane pieces first, the exchange on a second stream
-  // under the interior pieces) costs more than it hides at these slab sizes: measured per rank on
-  // one B200 (scripts/dist_apply_probe.py, AFEM_DIST_FORCE_PIECES at world 1) 112.8 vs 72.5 us at
-  // 128^3 and 437.6 vs 390.1 us at 256^3, against a ~10-20 us plane exchange over NVLink.
-  // AFEM_DIST_OVERLAP=1 selects it; AFEM_DIST_FORCE_PIECES=1 also at world 1 (measurement).
-  static const bool overlap = std::getenv("AFEM_DIST_OVERLAP") != nullptr;
-  static const bool force_pieces = std::getenv("AFEM_DIST_FORCE_PIECES") != nullptr;
-  if (!force_pieces && (!overlap || comm->size == 1) || P < 3) {
+  const int nzn = sys->nz + 1;  // node planes of the slab
+  static const char* ov = std::getenv("AFEM_DIST_OVERLAP");
+  static const bool overlap = !(ov && ov[0] == '0');
+  // measurement switch (scripts/dist_apply_probe.py): the split schedule even without neighbours
+  static const bool force = std::getenv("AFEM_DIST_FORCE_PIECES") != nullptr;
+  if (!pl || nzn < 3 || !overlap || (comm->size == 1 && !force)) {
     local->apply(x, y);
     halo_add(y, x, false);
     return;
@@ -292,15 +290,21 @@ void DistMfOp::apply(const double* x, double* y) {
   Ctx& c = *sys->ctx;
   const int64_t np = plane;
   const bool lo = comm->rank > 0, hi = comm->rank < comm->size - 1;
-  stencil_apply_pieces(*pl, *local, x, y, 0, 1);
-  stencil_apply_pieces(*pl, *local, x, y, P - 1, P);
+  const bool lo_b = lo || force, hi_b = hi || force;
   c.copy_streams(2);
   AFEM_CK(cudaEventRecord(c.events[0], c.stream));
   AFEM_CK(cudaStreamWaitEvent(c.s_in, c.events[0], 0));
-  comm->exchange(lo ? y : nullptr, lo ? recv_lo.p : nullptr, hi ? y + (n - np) : nullptr, hi ? recv_hi.p : nullptr,
-                 static_cast<size_t>(np), c.s_in);
+  {
+    cudaStream_t main_stream = c.stream;
+    ScopeExit restore([&] { c.stream = main_stream; });
+    c.stream = c.s_in;
+    if (lo_b) stencil_apply_planes(*pl, *local, x, y, 0, 1);
+    if (hi_b) stencil_apply_planes(*pl, *local, x, y, nzn - 1, nzn);
+    comm->exchange(lo ? y : nullptr, lo ? recv_lo.p : nullptr, hi ? y + (n - np) : nullptr,
+                   hi ? recv_hi.p : nullptr, static_cast<size_t>(np), c.s_in);
+  }
   AFEM_CK(cudaEventRecord(c.events[1], c.s_in));
-  stencil_apply_pieces(*pl, *local, x, y, 1, P - 1);
+  stencil_apply_planes(*pl, *local, x, y, lo_b ? 1 : 0, hi_b ? nzn - 1 : nzn);
   AFEM_CK(cudaStreamWaitEvent(c.stream, c.events[1], 0));
   halo_finish(y, x, false);
 }

@@ -579,6 +579,7 @@ struct Items {
   const uint64_t* rec;
   const uint32_t* zm;
   int64_t n;  // multiple of 32
+  int kmin = 0, kmax = 1 << 30;  // only the items of nodes on planes [kmin, kmax) (plane-range applies)
 };
 
 template <bool DOT>
@@ -605,11 +606,15 @@ __global__ void __launch_bounds__(kItemThreads, AFEM_ITEM_MINB) k_stencil_items(
     nzm = __ldg(&it.zm[(blo + warp) * 32 + lane]);
   }
   for (int64_t bt = blo + warp; bt < bhi; bt += nw) {
-    const uint64_t rec = nrec;
+    uint64_t rec = nrec;
     const uint32_t zm = nzm;
     if (bt + nw < bhi) {  // next batch's record, one batch ahead
       nrec = __ldg(&it.rec[(bt + nw) * 32 + lane]);
       nzm = __ldg(&it.zm[(bt + nw) * 32 + lane]);
+    }
+    {  // outside the plane range: a pad (a node's items share its plane, so segments stay whole)
+      const int nd = static_cast<int>(static_cast<uint32_t>(rec));
+      if (nd >= 0 && (nd / NXY < it.kmin || nd / NXY >= it.kmax)) rec = kPadRec;
     }
     const int node = static_cast<int>(static_cast<uint32_t>(rec));
     const uint32_t w = static_cast<uint32_t>(rec >> 32);
@@ -1202,6 +1207,34 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
   if (i1 > i0) {
     const Items it{pl.it_rec.p + i0, pl.it_zm.p + i0, i1 - i0};
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((i1 - i0) / 256, (int64_t)pl.iocc * c.num_sms)));
+    launch(c, k_stencil_items<false>, blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p, it, y, dot);
+  }
+}
+
+// y over node planes [kb, ke) only (main kernel balanced over the range's units, the items of
+// those planes), on the context's current stream: the slab operator's boundary / interior split.
+void stencil_apply_planes(StencilPlan& pl, const MfOp& op, const double* x, double* y, int kb, int ke) {
+  Ctx& c = *op.sys->ctx;
+  const StencilParams& P = pl.p;
+  ke = std::min(ke, P.NZ);
+  if (kb >= ke) return;
+  const DotArgs dot{nullptr, nullptr, nullptr, nullptr, 0, 0, nullptr};
+  if (P.NXm > 0) {
+    const int ntx = (P.NXm + TXN - 1) / TXN, nty = (P.NY + TY - 1) / TY;
+    const int64_t units = (int64_t)ntx * nty * (ke - kb);
+    const int blocks = static_cast<int>(std::min<int64_t>(pl.main_blocks, units));
+    stencil_x_map(pl, x);
+    launch(c, k_stencil_tma<false>, blocks, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, kb, ke, dot,
+           ntx, nty);
+  }
+  const int pa = kb / pl.zpiece, pb = std::min(pl.npieces, (ke + pl.zpiece - 1) / pl.zpiece);
+  const int64_t i0 = pl.piece_items[pa], i1 = pl.piece_items[pb];
+  if (i1 > i0) {
+    Items it{pl.it_rec.p + i0, pl.it_zm.p + i0, i1 - i0};
+    it.kmin = kb;
+    it.kmax = ke;
+    const int blocks =
+        static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((i1 - i0) / 256, (int64_t)pl.iocc * c.num_sms)));
     launch(c, k_stencil_items<false>, blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p, it, y, dot);
   }
 }

@@ -393,15 +393,14 @@ print(max(res.values()))
 """
 
 
-def test_overlapped_slab_schedule_matches_single_domain():
-    """The overlapped piece schedule (AFEM_DIST_OVERLAP=1: shared-plane pieces, the exchange on a
-    second stream under the interior pieces) gives the single-domain apply, like the default
-    schedule (whole-slab apply, then exchange)."""
+def test_sequential_slab_schedule_matches_single_domain():
+    """AFEM_DIST_OVERLAP=0 (whole-slab apply, then the exchange and the halo add) gives the
+    single-domain apply, like the default overlapped schedule the in-process tests run."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, AFEM_DIST_OVERLAP="1")
+    env = dict(os.environ, AFEM_DIST_OVERLAP="0")
     p = subprocess.run([sys.executable, "-c", OVERLAP_SNIPPET.format(root=root)], capture_output=True, text=True,
                        env=env, timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]
