@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Per-rank cost of the slab-decomposed apply, measured on one GPU: the single-domain apply (the
-N = 1 bench path) against the overlapped piece schedule a rank runs at N > 1 (shared-plane pieces
-first, the plane exchange on a second stream, the interior pieces, the halo add), forced at NCCL
-world size 1 with AFEM_DIST_FORCE_PIECES=1 (the exchange has no peer). usage: python
+N = 1 bench path) against the overlapped schedule a rank runs at N > 1 (the shared node planes as
+one-plane launches on a second stream, followed there by the plane exchange, concurrent with the
+interior planes as one balanced wave; then the halo add), forced at NCCL world size 1 with
+AFEM_DIST_FORCE_PIECES=1 (the exchange has no peer). usage: python
 scripts/dist_apply_probe.py [--n 128]"""
 import argparse
 import json
@@ -31,7 +32,7 @@ ss, _ = afem.slab_system(ctx, n, n, n, 0, 1, inclusions=fib, radius=0.05, materi
 d.set_benchmark_dirichlet(ss, 0.01)
 dop = d.matrix_free_operator(ss, ss.impose_dirichlet(np.zeros(ss.n)))
 x = torch.rand(s.n, dtype=torch.float64, device="cuda") * 2 - 1
-for name, o in (("single_domain", op), ("slab_pieces", dop)):
+for name, o in (("single_domain", op), ("slab_overlapped", dop)):
     ys = [torch.empty_like(x) for _ in range(2)]
     for k in range(10):
         o.apply_device(x.data_ptr(), ys[k %% 2].data_ptr())
