@@ -292,19 +292,15 @@ afem_status afem_history_set(afem_system sys, const double* in);
  * PAPER.md:296-302). One process per GPU, each owning a contiguous z-slab of element layers; the
  * node plane between slabs is shared and owned by the lower rank. The only data-path collectives
  * are a one-plane exchange with each neighbour per operator apply and scalar allreduces for the
- * Krylov dot products (NCCL over NVLink). A threads backend runs the same algorithm with several
- * subdomains on one device (tests). */
+ * Krylov dot products (NCCL over NVLink). (A threads backend that runs the same algorithm with
+ * several subdomains on one device, for tests, is declared in afem_testing.h.) */
 typedef struct afem_dist_s* afem_dist;
-typedef struct afem_thread_group_s* afem_thread_group;
 
 /* Element layers [z0, z1) of rank `rank` when nz layers are split over `size` ranks. Host only. */
 afem_status afem_slab_range(int32_t nz, int32_t size, int32_t rank, int32_t* z0, int32_t* z1);
 /* 128-byte NCCL unique id (rank 0 creates it, the host broadcasts it). */
 afem_status afem_nccl_unique_id(void* out128);
 afem_status afem_dist_create_nccl(afem_ctx ctx, const void* uid128, int32_t rank, int32_t size, afem_dist* out);
-afem_status afem_thread_group_create(int32_t size, afem_thread_group* out);
-afem_status afem_thread_group_destroy(afem_thread_group g);
-afem_status afem_dist_create_threads(afem_ctx ctx, afem_thread_group g, int32_t rank, afem_dist* out);
 afem_status afem_dist_destroy(afem_dist d);
 /* benchmark_bcs of the global grid restricted to this rank's slab system (the slab's local grid
  * system from afem_system_create_grid with nz = z1 - z0 and lz scaled accordingly). */

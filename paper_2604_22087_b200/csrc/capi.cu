@@ -11,6 +11,7 @@
 #include <string>
 
 #include "../../include/afem.h"
+#include "../../include/afem_testing.h"
 #include "afem_impl.hpp"
 #include "dist.hpp"
 

@@ -9,10 +9,11 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "afem.h")
+HEADERS = [HEADER, os.path.join(ROOT, "include", "afem_testing.h")]
 
 
-def declared_symbols():
-    src = open(HEADER).read()
+def declared_symbols(headers=(HEADER,)):
+    src = "".join(open(h).read() for h in headers)
     return sorted(set(re.findall(r"^(?:afem_status|const char\*|int32_t)\s+(afem_\w+)\(", src, re.M)))
 
 
@@ -33,7 +34,7 @@ def test_header_declares_the_boundary():
 
 
 def test_library_exports_every_declared_symbol(lib):
-    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    missing = [s for s in declared_symbols(HEADERS) if not hasattr(lib, s)]
     assert not missing, missing
     assert lib.afem_abi_version() == 1
 
