@@ -256,7 +256,8 @@ void stencil_apply(StencilPlan& p, const MfOp& op, const double* x, double* y, d
 int stencil_pieces(const StencilPlan& p);
 int stencil_piece_planes(const StencilPlan& p);
 void stencil_apply_pieces(StencilPlan& p, const MfOp& op, const double* x, double* y, int pa, int pb);
-void stencil_apply_planes(StencilPlan& p, const MfOp& op, const double* x, double* y, int kb, int ke);
+void stencil_apply_planes(StencilPlan& p, const MfOp& op, const double* x, double* y, int kb, int ke,
+                          double* dot_out = nullptr, const int* skip = nullptr);
 void destroy_stencil_plan(StencilPlan* p);
 
 }  // namespace afem

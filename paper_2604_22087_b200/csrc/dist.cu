@@ -217,15 +217,30 @@ std::vector<Constraint> slab_benchmark_bcs(const System& s, int rank, int size, 
 // ------------------------------------------------------------------ distributed operator
 namespace {
 
-__global__ void k_add(double* __restrict__ v, const double* __restrict__ w, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    v[i] += w[i];
-}
-
-__global__ void k_reset_masked(double* __restrict__ v, const double* __restrict__ x, const uint8_t* __restrict__ mask,
-                               double one_or_x, int use_x, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    if (mask[i]) v[i] = use_x ? x[i] : one_or_x;
+// The received neighbour partial sums added into the two shared node planes of v in one launch
+// (index i < np: the bottom plane, else the top plane); constrained rows reset (mode 1: unit
+// diagonal, mode 2: x); dot_out != nullptr: the owned top plane's x.v is added to dot_out[0]
+// (fixed-order grid reduction; the bottom plane belongs to rank - 1).
+__global__ void k_halo_fin(double* __restrict__ v, int64_t n, int64_t np, const double* __restrict__ recv_lo,
+                           const double* __restrict__ recv_hi, const double* __restrict__ x,
+                           const uint8_t* __restrict__ mask, int mode, double* partials, unsigned* counter,
+                           double* dot_out, const int* skip) {
+  if (skip && *skip) return;
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 2 * np; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool top = i >= np;
+    const double* rv = top ? recv_hi : recv_lo;
+    if (!rv) continue;
+    const int64_t k = top ? i - np : i, d = top ? n - np + k : k;
+    double t = v[d] + rv[k];
+    if (mode && mask[d]) t = mode == 1 ? 1.0 : x[d];
+    v[d] = t;
+    if (top && dot_out) s += x[d] * t;
+  }
+  if (!dot_out) return;
+  double a[1] = {s};
+  if (grid_reduce<1>(a, partials, counter))
+    if (threadIdx.x == 0) dot_out[0] += a[0];
 }
 
 }  // namespace
@@ -245,23 +260,15 @@ void DistMfOp::halo_add(double* v, const double* x_for_mask, bool diag_mode) {
   halo_finish(v, x_for_mask, diag_mode);
 }
 
-void DistMfOp::halo_finish(double* v, const double* x_for_mask, bool diag_mode) {
+void DistMfOp::halo_finish(double* v, const double* x_for_mask, bool diag_mode, double* dot_out) {
   Ctx& c = *sys->ctx;
-  const int64_t np = plane;
   const bool lo = comm->rank > 0, hi = comm->rank < comm->size - 1;
-  double* top = v + (n - np);
-  const unsigned g = grid_for(np, 256, 148 * 4);
-  const bool reset = diag_mode || x_for_mask;  // neither: plain assembly of partial sums
-  if (lo) {
-    launch(c, k_add, g, 256, 0, v, recv_lo.p, np);
-    if (reset) launch(c, k_reset_masked, g, 256, 0, v, x_for_mask, mask(), 1.0, diag_mode ? 0 : 1, np);
-  }
-  if (hi) {
-    launch(c, k_add, g, 256, 0, top, recv_hi.p, np);
-    if (reset)
-      launch(c, k_reset_masked, g, 256, 0, top, x_for_mask ? x_for_mask + (n - np) : nullptr,
-             mask() + (n - np), 1.0, diag_mode ? 0 : 1, np);
-  }
+  if (!lo && !hi) return;
+  const int mode = diag_mode ? 1 : x_for_mask ? 2 : 0;  // neither: plain assembly of partial sums
+  const unsigned g = dot_out ? red_grid(2 * plane) : grid_for(2 * plane, 256, 148 * 4);
+  launch(c, k_halo_fin, g, dot_out ? kRedThreads : 256, 0, v, n, plane, lo ? recv_lo.p : nullptr,
+         hi ? recv_hi.p : nullptr, x_for_mask, mask(), mode, c.red_partials.p, c.red_counter.p, dot_out,
+         dot_out ? skip : nullptr);
 }
 
 // Halo exchange overlapped with the interior: the two shared node planes are applied first on a
@@ -270,7 +277,28 @@ void DistMfOp::halo_finish(double* v, const double* x_for_mask, bool diag_mode) 
 // the context stream, which then waits for the exchange and adds the received partial sums. The
 // boundary launches fit beside the interior wave (a fifth CTA per SM), so the exchange is hidden
 // under the interior. Same arithmetic as apply + halo_add. AFEM_DIST_OVERLAP=0: apply, then halo.
-void DistMfOp::apply(const double* x, double* y) {
+void DistMfOp::apply(const double* x, double* y) { apply_impl(x, y, nullptr); }
+
+// Fused owned x.y: the interior wave's stencil dot covers every owned plane but the top shared one,
+// whose rows are complete only after the halo add (k_halo_fin adds its share). Needs the overlapped
+// stencil schedule (or no neighbours); false otherwise (the caller runs an owned-dot kernel).
+bool DistMfOp::apply_dot(const double* x, double* y, double* dot_out) {
+  static const char* ov = std::getenv("AFEM_DIST_OVERLAP");
+  static const bool overlap = !(ov && ov[0] == '0');
+  static const bool force = std::getenv("AFEM_DIST_FORCE_PIECES") != nullptr;
+  static const bool disabled = std::getenv("AFEM_NO_FUSED_DOT") != nullptr;
+  if (!local || !local->stencil || disabled || force) return false;
+  if (comm->size == 1) {
+    local->set_skip(skip);
+    ScopeExit unset([&] { local->set_skip(nullptr); });
+    return local->apply_dot(x, y, dot_out);
+  }
+  if (!overlap || sys->nz + 1 < 3) return false;
+  apply_impl(x, y, dot_out);
+  return true;
+}
+
+void DistMfOp::apply_impl(const double* x, double* y, double* dot_out) {
   if (!local) {  // assembled: local SpMV (partial sums on the shared planes) + halo
     csr_apply(*sys, vals.p, x, y);
     halo_add(y, x, false);
@@ -298,15 +326,15 @@ void DistMfOp::apply(const double* x, double* y) {
     cudaStream_t main_stream = c.stream;
     ScopeExit restore([&] { c.stream = main_stream; });
     c.stream = c.s_in;
-    if (lo_b) stencil_apply_planes(*pl, *local, x, y, 0, 1);
-    if (hi_b) stencil_apply_planes(*pl, *local, x, y, nzn - 1, nzn);
+    if (lo_b) stencil_apply_planes(*pl, *local, x, y, 0, 1, nullptr, skip);
+    if (hi_b) stencil_apply_planes(*pl, *local, x, y, nzn - 1, nzn, nullptr, skip);
     comm->exchange(lo ? y : nullptr, lo ? recv_lo.p : nullptr, hi ? y + (n - np) : nullptr,
                    hi ? recv_hi.p : nullptr, static_cast<size_t>(np), c.s_in);
   }
   AFEM_CK(cudaEventRecord(c.events[1], c.s_in));
-  stencil_apply_planes(*pl, *local, x, y, lo_b ? 1 : 0, hi_b ? nzn - 1 : nzn);
+  stencil_apply_planes(*pl, *local, x, y, lo_b ? 1 : 0, hi_b ? nzn - 1 : nzn, dot_out, skip);
   AFEM_CK(cudaStreamWaitEvent(c.stream, c.events[1], 0));
-  halo_finish(y, x, false);
+  halo_finish(y, x, false, dot_out && hi ? dot_out : nullptr);
 }
 
 void DistMfOp::diagonal(double* d) { copy(*sys->ctx, diag.p, d, n); }
@@ -357,9 +385,17 @@ std::unique_ptr<DistMfOp> make_dist_csr_op(System& s, Comm* comm, const double* 
 // ------------------------------------------------------------------ distributed CG (krylov.hpp:350-408)
 namespace {
 
+// Single-reduction (Chronopoulos-Gear) preconditioned CG: the same iterates as krylov.hpp:350-408
+// in exact arithmetic, with the three inner products of an iteration — (r, u), (r, r) and
+// (u, w = A u), u = M r — summed across the ranks by ONE allreduce instead of two (p.Ap, then r.r
+// and r.z): p = u + beta p, s = w + beta s (s = A p by recurrence), x += alpha p, r -= alpha s,
+// with p.Ap = (u, w) - beta gamma / alpha_prev. Stopping rules are the reference's: recurrence
+// test on ||r|| / ||b||, p.Ap <= 0 failure, max_iter; the caller re-verifies the true residual.
 struct DcgDev {
-  double rz, pap, beta, denom, rtol, loc[2], alpha;
+  double gamma, alpha, denom, rtol;
+  double loc[3];  // (r, u), (r, r), (u, w) of the current iterate: partial, then allreduced
   int it, max_iter, done, fail, conv;
+  int fresh;  // the next step is the first after a (re)start: beta = 0, p.Ap = (u, w)
 };
 
 __global__ void k_owned_dot(const double* a, const double* b, int64_t n, double* partials, unsigned* counter,
@@ -386,98 +422,89 @@ __global__ void k_dres(const double* b, const double* ax, double* r, int64_t n, 
     if (threadIdx.x == 0) out[0] = v[0];
 }
 
-// p = z = M r; loc[0] = owned r.z
-__global__ void k_dcg_start(const double* r, const double* inv, double* p, int64_t n, int64_t off, double* partials,
-                            unsigned* counter, DcgDev* st) {
-  double s = 0.0;
+// start (or restart): u = M r, p = s = 0; loc[0] = owned (r, u), loc[1] = owned (r, r)
+__global__ void k_dcg_start(const double* r, const double* inv, double* u, double* p, double* s, int64_t n,
+                            int64_t off, double* partials, unsigned* counter, DcgDev* st) {
+  double ru = 0.0, rr = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double z = inv ? r[i] * inv[i] : r[i];
-    p[i] = z;
-    if (i >= off) s += r[i] * z;
-  }
-  double v[1] = {s};
-  if (grid_reduce<1>(v, partials, counter))
-    if (threadIdx.x == 0) st->loc[0] = v[0];
-}
-
-__global__ void k_dcg_start_finish(DcgDev* st) {
-  st->rz = st->loc[0];
-  st->done = 0;
-}
-
-__global__ void k_dcg_pap(const double* p, const double* ap, int64_t n, int64_t off, double* partials,
-                          unsigned* counter, DcgDev* st) {
-  if (st->done) return;
-  double s = 0.0;
-  for (int64_t i = off + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    s += p[i] * ap[i];
-  double v[1] = {s};
-  if (grid_reduce<1>(v, partials, counter))
-    if (threadIdx.x == 0) st->pap = v[0];
-}
-
-// r -= alpha Ap and the owned (r.r, r.z); x += alpha p is deferred to k_dcg_p, which reads p anyway
-// (the converging iteration's x update runs once after the loop, k_dcg_x_epilogue)
-__global__ void k_dcg_update(double* r, const double* ap, const double* inv, int64_t n, int64_t off,
-                             double* partials, unsigned* counter, DcgDev* st) {
-  if (st->done || !(st->pap > 0.0)) return;
-  const double a = st->rz / st->pap;
-  double rr = 0.0, rz = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double ri = r[i] - a * ap[i];
-    r[i] = ri;
+    const double ri = r[i], z = inv ? ri * inv[i] : ri;
+    u[i] = z;
+    p[i] = 0.0;
+    s[i] = 0.0;
     if (i >= off) {
+      ru += ri * z;
       rr += ri * ri;
-      rz += ri * (inv ? ri * inv[i] : ri);
     }
   }
-  double v[2] = {rr, rz};
+  double v[2] = {ru, rr};
   if (grid_reduce<2>(v, partials, counter))
     if (threadIdx.x == 0) {
       st->loc[0] = v[0];
       st->loc[1] = v[1];
-      st->alpha = a;
+      st->done = 0;
+      st->fail = 0;
+      st->conv = 0;
+      st->fresh = 1;
     }
 }
 
-__global__ void k_dcg_finish(DcgDev* st, double* hist) {
+// One iteration. Preamble (every thread, identical scalars from the allreduced loc): the previous
+// iteration's stopping test and the step's beta / alpha; then the fused vector update
+//   p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = M r
+// with the owned (r, u), (r, r) partials. The last block (every other block has read st by then)
+// commits the scalars: it, gamma, alpha, hist[it], the flags and the new partial sums.
+__global__ void k_dcg_step(double* __restrict__ x, double* __restrict__ r, double* __restrict__ u,
+                           double* __restrict__ p, double* __restrict__ s, const double* __restrict__ w,
+                           const double* __restrict__ inv, int64_t n, int64_t off, double* partials,
+                           unsigned* counter, DcgDev* st, double* hist) {
   if (st->done) return;
-  if (!(st->pap > 0.0)) {  // krylov.hpp:377-381
-    st->fail = 1;
-    st->done = 1;
-    st->alpha = 0.0;
-    return;
+  const int it = st->it;
+  const double gnew = st->loc[0], rr = st->loc[1], delta = st->loc[2];
+  const double h = sqrt(rr) / st->denom;
+  int stop = 0;  // 1 converged, 2 p.Ap <= 0, 3 max_iter
+  double beta = 0.0, pap = delta;
+  const bool fresh = st->fresh;  // (re)start: the host has tested this residual already
+  if (!fresh) {
+    if (h <= st->rtol) stop = 1;
+    else if (it >= st->max_iter) stop = 3;
+    else {
+      beta = gnew / st->gamma;
+      pap = delta - beta * gnew / st->alpha;
+    }
   }
-  const int it = st->it + 1;
-  st->it = it;
-  const double h = sqrt(st->loc[0]) / st->denom;
-  hist[it] = h;
-  if (h <= st->rtol) {
-    st->done = 1;
-    st->conv = 1;
-  } else {
-    st->beta = st->loc[1] / st->rz;
-    st->rz = st->loc[1];
-    if (it >= st->max_iter) st->done = 1;
+  if (!stop && !(pap > 0.0)) stop = 2;  // krylov.hpp:377-381
+  const double alpha = stop ? 0.0 : gnew / pap;
+  double ru = 0.0, rn = 0.0;
+  if (!stop)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      const double pi = u[i] + beta * p[i], si = w[i] + beta * s[i];
+      p[i] = pi;
+      s[i] = si;
+      x[i] += alpha * pi;
+      const double ri = r[i] - alpha * si, zi = inv ? ri * inv[i] : ri;
+      r[i] = ri;
+      u[i] = zi;
+      if (i >= off) {
+        ru += ri * zi;
+        rn += ri * ri;
+      }
+    }
+  double v[2] = {ru, rn};
+  if (grid_reduce<2>(v, partials, counter) && threadIdx.x == 0) {
+    if (!fresh) hist[it] = h;
+    st->fresh = 0;
+    if (stop) {
+      st->done = 1;
+      st->conv = stop == 1;
+      st->fail = stop == 2;
+    } else {
+      st->it = it + 1;
+      st->gamma = gnew;
+      st->alpha = alpha;
+      st->loc[0] = v[0];
+      st->loc[1] = v[1];
+    }
   }
-}
-
-// x += alpha p (deferred from k_dcg_update), then p = M r + beta p
-__global__ void k_dcg_p(const double* r, const double* inv, double* p, double* x, int64_t n, const DcgDev* st) {
-  if (st->done) return;
-  const double a = st->alpha, b = st->beta;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double pi = p[i];
-    x[i] += a * pi;
-    p[i] = (inv ? r[i] * inv[i] : r[i]) + b * pi;
-  }
-}
-
-// the converging (or last) iteration's deferred x += alpha p (alpha = 0 after a pAp failure)
-__global__ void k_dcg_x_epilogue(double* x, const double* p, int64_t n, const DcgDev* st) {
-  const double a = st->alpha;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    x[i] += a * p[i];
 }
 
 __global__ void k_inv(const double* d, double* inv, int64_t n, unsigned long long* first_zero) {
@@ -516,7 +543,7 @@ void dist_solve(DistMfOp& op, const SolverCfg& cfg, const double* b, const doubl
   Ctx& c = *op.sys->ctx;
   const int64_t n = op.n, off = op.owned_offset;
   const unsigned rg = red_grid(n), eg = grid_for(n, 256, 148 * 16);
-  DevArray<double> inv, r(n), p(n), ap(n), scratch(n), hist(cfg.max_iter + 2), scal(4);
+  DevArray<double> inv, r(n), u(n), w(n), p(n), sv(n), scratch(n), hist(cfg.max_iter + 2), scal(4);
   if (cfg.precond == 1) {
     inv.alloc(n);
     DevArray<unsigned long long> fz(1);
@@ -533,7 +560,7 @@ void dist_solve(DistMfOp& op, const SolverCfg& cfg, const double* b, const doubl
   op.comm->allreduce_sum(scal.p, 1, c.stream);
   const double bnorm = std::sqrt(fetch_dev(c, scal.p));
   const double denom = bnorm > 0.0 ? bnorm : 1.0;
-  rep.history.assign(1, dist_residual_norm(op, b, x, ap.p, r.p, scal.p) / denom);
+  rep.history.assign(1, dist_residual_norm(op, b, x, w.p, r.p, scal.p) / denom);
   DevArray<DcgDev> st(1);
   DcgDev hs{};
   hs.denom = denom;
@@ -542,30 +569,39 @@ void dist_solve(DistMfOp& op, const SolverCfg& cfg, const double* b, const doubl
   hs.done = 1;
   AFEM_CK(cudaMemcpyAsync(st.p, &hs, sizeof hs, cudaMemcpyHostToDevice, c.stream));
   double* loc = reinterpret_cast<double*>(reinterpret_cast<char*>(st.p) + offsetof(DcgDev, loc));
-  double* pap = reinterpret_cast<double*>(reinterpret_cast<char*>(st.p) + offsetof(DcgDev, pap));
+  const int* done_dev = reinterpret_cast<const int*>(reinterpret_cast<const char*>(st.p) + offsetof(DcgDev, done));
+  // w = A u with the owned (u, w) into loc[2]: fused into the stencil apply where the operator can
+  auto apply_uw = [&] {
+    if (!op.apply_dot(u.p, w.p, loc + 2)) {
+      op.apply(u.p, w.p);
+      launch(c, k_owned_dot, rg, kRedThreads, 0, u.p + off, w.p + off, n - off, c.red_partials.p, c.red_counter.p,
+             loc + 2);
+    }
+    op.comm->allreduce_sum(loc, 3, c.stream);  // the iteration's one collective
+  };
+  ScopeExit unset([&] { op.set_skip(nullptr); });
   while (true) {
     if (rep.history.back() > cfg.rtol && rep.iterations < cfg.max_iter) {
-      launch(c, k_dcg_start, rg, kRedThreads, 0, r.p, inv.p, p.p, n, off, c.red_partials.p, c.red_counter.p, st.p);
-      op.comm->allreduce_sum(loc, 1, c.stream);
-      launch(c, k_dcg_start_finish, 1, 1, 0, st.p);
+      const int it0 = rep.iterations;
+      hs.it = it0;
+      AFEM_CK(cudaMemcpyAsync(reinterpret_cast<char*>(st.p) + offsetof(DcgDev, it), &hs.it, sizeof(int),
+                              cudaMemcpyHostToDevice, c.stream));
+      launch(c, k_dcg_start, rg, kRedThreads, 0, r.p, inv.p, u.p, p.p, sv.p, n, off, c.red_partials.p,
+             c.red_counter.p, st.p);
+      op.set_skip(done_dev);  // chunk iterations past convergence skip the apply
+      apply_uw();
       int chunk = 4;
       while (true) {
         for (int k = 0; k < chunk; ++k) {
-          op.apply(p.p, ap.p);
-          launch(c, k_dcg_pap, rg, kRedThreads, 0, p.p, ap.p, n, off, c.red_partials.p, c.red_counter.p, st.p);
-          op.comm->allreduce_sum(pap, 1, c.stream);
-          launch(c, k_dcg_update, rg, kRedThreads, 0, r.p, ap.p, inv.p, n, off, c.red_partials.p, c.red_counter.p,
-                 st.p);
-          op.comm->allreduce_sum(loc, 2, c.stream);
-          launch(c, k_dcg_finish, 1, 1, 0, st.p, hist.p);
-          launch(c, k_dcg_p, eg, 256, 0, r.p, inv.p, p.p, x, n, st.p);
+          launch(c, k_dcg_step, rg, kRedThreads, 0, x, r.p, u.p, p.p, sv.p, w.p, inv.p, n, off, c.red_partials.p,
+                 c.red_counter.p, st.p, hist.p);
+          apply_uw();
         }
         hs = fetch_dev(c, st.p);
         if (hs.done) break;
         chunk = std::min(chunk * 2, 64);
       }
-      launch(c, k_dcg_x_epilogue, eg, 256, 0, x, p.p, n, st.p);
-      const int it0 = rep.iterations;
+      op.set_skip(nullptr);
       rep.iterations = hs.it;
       if (hs.it > it0) {
         rep.history.resize(hs.it + 1);
@@ -584,7 +620,7 @@ void dist_solve(DistMfOp& op, const SolverCfg& cfg, const double* b, const doubl
       break;
     }
     if (!rep.failure.empty() || rep.iterations >= cfg.max_iter) break;
-    dist_residual_norm(op, b, x, ap.p, r.p, scal.p);
+    dist_residual_norm(op, b, x, w.p, r.p, scal.p);  // recurrence drifted: restart (krylov.hpp:402-404)
   }
   AFEM_CK(cudaStreamSynchronize(c.stream));
   rep.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -43,7 +43,15 @@ struct DistMfOp : Operator {
   DevArray<double> diag, send_lo, recv_lo, send_hi, recv_hi;
   ~DistMfOp() override;
   void apply(const double* x, double* y) override;
+  // y = A x and dot_out[0] = owned x.y (before the allreduce): the interior wave's fused stencil dot
+  // plus the owned shared plane's, summed after its halo add; false where the operator cannot fuse
+  bool apply_dot(const double* x, double* y, double* dot_out) override;
   void diagonal(double* d) override;
+  const int* skip = nullptr;  // the CG loop's device done flag (stencil launches only)
+  bool set_skip(const int* flag) override {
+    skip = flag;
+    return local && local->stencil;
+  }
   bool uses_stencil() const override { return local && local->uses_stencil(); }
   const uint8_t* mask() const { return local ? local->mask.p : sys->mask.p; }
   // owned-dof inner products + allreduce (the GMRES / BiCGStab scalars, identical on every rank)
@@ -54,7 +62,8 @@ struct DistMfOp : Operator {
   void allreduce_dev(double* d, int k) override { comm->allreduce_sum(d, k, sys->ctx->stream); }
   void halo_add(double* v, const double* x_for_mask, bool diag_mode);
   // the received neighbour partials added into v's shared planes (+ unit Dirichlet rows)
-  void halo_finish(double* v, const double* x_for_mask, bool diag_mode);
+  void halo_finish(double* v, const double* x_for_mask, bool diag_mode, double* dot_out = nullptr);
+  void apply_impl(const double* x, double* y, double* dot_out);
 };
 
 std::unique_ptr<DistMfOp> make_dist_mf_op(System& s, Comm* comm, std::unique_ptr<MfOp> local);

@@ -1213,29 +1213,41 @@ void stencil_apply_pieces(StencilPlan& pl, const MfOp& op, const double* x, doub
 
 // y over node planes [kb, ke) only (main kernel balanced over the range's units, the items of
 // those planes), on the context's current stream: the slab operator's boundary / interior split.
-void stencil_apply_planes(StencilPlan& pl, const MfOp& op, const double* x, double* y, int kb, int ke) {
+// dot_out: also x.y over the range's rows (fixed-order, the plan's partials: one such launch in
+// flight per plan); skip: the CG loop's device done flag.
+void stencil_apply_planes(StencilPlan& pl, const MfOp& op, const double* x, double* y, int kb, int ke,
+                          double* dot_out, const int* skip) {
   Ctx& c = *op.sys->ctx;
   const StencilParams& P = pl.p;
   ke = std::min(ke, P.NZ);
-  if (kb >= ke) return;
-  const DotArgs dot{nullptr, nullptr, nullptr, nullptr, 0, 0, nullptr};
-  if (P.NXm > 0) {
-    const int ntx = (P.NXm + TXN - 1) / TXN, nty = (P.NY + TY - 1) / TY;
-    const int64_t units = (int64_t)ntx * nty * (ke - kb);
-    const int blocks = static_cast<int>(std::min<int64_t>(pl.main_blocks, units));
-    stencil_x_map(pl, x);
-    launch(c, k_stencil_tma<false>, blocks, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, kb, ke, dot,
-           ntx, nty);
-  }
   const int pa = kb / pl.zpiece, pb = std::min(pl.npieces, (ke + pl.zpiece - 1) / pl.zpiece);
-  const int64_t i0 = pl.piece_items[pa], i1 = pl.piece_items[pb];
-  if (i1 > i0) {
+  const int64_t i0 = kb < ke ? pl.piece_items[pa] : 0, i1 = kb < ke ? pl.piece_items[pb] : 0;
+  const int ntx = (P.NXm + TXN - 1) / TXN, nty = (P.NY + TY - 1) / TY;
+  const int64_t units = (int64_t)ntx * nty * std::max(0, ke - kb);
+  const int mblocks = P.NXm > 0 ? static_cast<int>(std::min<int64_t>(pl.main_blocks, units)) : 0;
+  const bool items = i1 > i0;
+  if (dot_out && mblocks == 0 && !items) AFEM_CK(cudaMemsetAsync(dot_out, 0, sizeof(double), c.stream));
+  if (kb >= ke) return;
+  const DotArgs dot{pl.part_main.p, pl.part_items.p, pl.counter.p, dot_out, items ? 0 : 1, mblocks, skip};
+  if (mblocks > 0) {
+    stencil_x_map(pl, x);
+    if (dot_out)
+      launch(c, k_stencil_tma<true>, mblocks, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, kb, ke, dot,
+             ntx, nty);
+    else
+      launch(c, k_stencil_tma<false>, mblocks, NT, kTmaSmem, pl.mx, pl.mi, P, pl.xshift, pl.ipx, x, y, 0, kb, ke, dot,
+             ntx, nty);
+  }
+  if (items) {
     Items it{pl.it_rec.p + i0, pl.it_zm.p + i0, i1 - i0};
     it.kmin = kb;
     it.kmax = ke;
     const int blocks =
         static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((i1 - i0) / 256, (int64_t)pl.iocc * c.num_sms)));
-    launch(c, k_stencil_items<false>, blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p, it, y, dot);
+    if (dot_out)
+      launch(c, k_stencil_items<true>, blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p, it, y, dot);
+    else
+      launch(c, k_stencil_items<false>, blocks, kItemThreads, 0, P.NX, P.NY, pl.k0, pl.Ed.p, x, pl.info.p, it, y, dot);
   }
 }
 

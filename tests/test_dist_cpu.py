@@ -118,3 +118,112 @@ def test_slab_decomposition_gloo(size):
     for rank, err, dot_err, _ in res:
         assert err < 1e-12, (rank, err)
         assert dot_err < 1e-12, (rank, dot_err)
+
+
+def _halo(y, rank, size, plane):
+    """Neighbour partial sums added into the two shared planes (dist.cu k_halo_fin's assembly)."""
+    reqs, bufs = [], {}
+    if rank > 0:
+        bufs["lo"] = torch.zeros(plane, dtype=torch.float64)
+        reqs += [dist.isend(torch.from_numpy(y[:plane].copy()), rank - 1), dist.irecv(bufs["lo"], rank - 1)]
+    if rank < size - 1:
+        bufs["hi"] = torch.zeros(plane, dtype=torch.float64)
+        reqs += [dist.isend(torch.from_numpy(y[-plane:].copy()), rank + 1), dist.irecv(bufs["hi"], rank + 1)]
+    for r in reqs:
+        r.wait()
+    if "lo" in bufs:
+        y[:plane] += bufs["lo"].numpy()
+    if "hi" in bufs:
+        y[-plane:] += bufs["hi"].numpy()
+    return y
+
+
+def _cg_worker(rank, size, port, q):
+    """dist.cu dist_solve restated over gloo: single-reduction (Chronopoulos-Gear) Jacobi-PCG on
+    the slab operator, ONE all_reduce of (r.u, r.r, u.Au) per iteration, against the oracle's
+    single-domain CG (krylov.hpp:350-408) on the global operator."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=size)
+        import paper_2604_22087_b200 as afem
+        from oracle.pyoracle import Oracle
+        orc = Oracle("restate")
+        fib, g, u, _ = _global_problem(orc)
+        b = np.random.default_rng(7).uniform(-1, 1, g.n)
+        rtol = 1e-10
+        xg, rg = g.solve(1, u, b, method=0, precond=1, rtol=rtol)
+        z0, z1 = afem.slab_range(NZ, size, rank)
+        nzl = z1 - z0
+        plane = 3 * (NX + 1) * (NY + 1)
+        sl = slice(plane * z0, plane * (z1 + 1))
+        coords, conn, phase = orc.mesh3d(NX, NY, nzl, fib, 0.3, lz=nzl / NZ)
+        loc = orc.system(3, coords, conn, phase, MATS, lite=True)
+        node, comp, val = _slab_bcs(nzl, rank, size)
+        loc.set_dirichlet(node.astype(np.int32), comp.astype(np.int32), val)
+        ul, bl = u[sl].copy(), b[sl].copy()
+        mask = np.zeros(loc.n, bool)
+        mask[3 * node + comp] = True
+        off = plane if rank > 0 else 0
+        ncoll = [0]
+
+        def apply(v):
+            y = _halo(loc.mf_apply(ul, v), rank, size, plane)
+            y[mask] = v[mask]
+            return y
+
+        def allreduce(vals):
+            ncoll[0] += 1
+            t = torch.tensor(vals, dtype=torch.float64)
+            dist.all_reduce(t)
+            return t.numpy()
+
+        diag = _halo(loc.mf_diagonal(ul), rank, size, plane)
+        diag[mask] = 1.0
+        inv = 1.0 / diag
+        bn = float(np.sqrt(allreduce([float(bl[off:] @ bl[off:])])[0]))
+        x = np.zeros(loc.n)
+        r = bl.copy()
+        uu = inv * r
+        w = apply(uu)
+        gam, rr, dlt = allreduce([r[off:] @ uu[off:], r[off:] @ r[off:], uu[off:] @ w[off:]])
+        p, s = np.zeros(loc.n), np.zeros(loc.n)
+        it, gold, aold, c0 = 0, 0.0, 0.0, ncoll[0]
+        while it < 10000:
+            if it > 0 and np.sqrt(rr) / bn <= rtol:
+                break
+            beta = gam / gold if it > 0 else 0.0
+            pap = dlt - beta * gam / aold if it > 0 else dlt
+            alpha = gam / pap
+            p = uu + beta * p
+            s = w + beta * s
+            x += alpha * p
+            r -= alpha * s
+            uu = inv * r
+            w = apply(uu)
+            gold, aold = gam, alpha
+            gam, rr, dlt = allreduce([r[off:] @ uu[off:], r[off:] @ r[off:], uu[off:] @ w[off:]])
+            it += 1
+        per_it = (ncoll[0] - c0) / max(it, 1)
+        xerr = float(np.abs(x - xg[sl]).max() / np.abs(xg).max())
+        q.put((rank, xerr, it, rg["iterations"], per_it))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - surfaced by the assertion below
+        q.put((rank, repr(e), None, None, None))
+
+
+@pytest.mark.parametrize("size", [2, 3])
+def test_single_reduction_slab_cg_gloo(size):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cg_worker, args=(r, size, port, q)) for r in range(size)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(size)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(isinstance(r[1], float) for r in res), res
+    for rank, xerr, it, it_ref, per_it in res:
+        assert xerr <= 1e-8, (rank, xerr)
+        assert abs(it - it_ref) <= 2, (rank, it, it_ref)
+        assert per_it == 1.0, (rank, per_it)  # one collective per iteration

@@ -104,6 +104,26 @@ def test_nccl_backend_single_rank(afem):
     assert rel_err(xs, xg) <= 1e-8
 
 
+def test_distributed_cg_one_collective_kernel_count(afem):
+    """The slab CG is single-reduction (one allreduce per iteration) with the (u, A u) dot fused into
+    the stencil apply: at world size 1 it launches no more kernels per iteration than the
+    single-GPU CG (apply with fused p.Ap, update, p update)."""
+    ctx, fib, s, u, x, op, b = _global(afem, nz=64)
+    l0 = ctx.launches
+    xg, rg = afem.run_solver(op, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
+    per_single = (ctx.launches - l0) / rg["iterations"]
+    d = afem.Dist(ctx, 0, 1, backend="nccl", uid=afem.nccl_unique_id())
+    sys_, _ = afem.slab_system(ctx, NX, NY, 64, 0, 1, inclusions=fib, radius=0.15, materials=LINEAR)
+    d.set_benchmark_dirichlet(sys_, STRAIN)
+    dop = d.matrix_free_operator(sys_, sys_.impose_dirichlet(np.zeros(sys_.n)))
+    l1 = ctx.launches
+    xs, rep = d.run_solver(dop, b, method=afem.CG, precond=afem.JACOBI, rtol=1e-10)
+    per_dist = (ctx.launches - l1) / rep["iterations"]
+    assert rep["converged"] and abs(rep["iterations"] - rg["iterations"]) <= max(2, rg["iterations"] // 100), (rep, rg)
+    assert rel_err(xs, xg) <= 1e-8
+    assert per_dist <= per_single, (per_dist, per_single)
+
+
 J2_MIX = [(3, 1.0, 0.3, 0.002, 0.1), (0, 10.0, 0.3)]
 
 
