@@ -504,6 +504,7 @@ struct TangentQP {
   bool iso;  // isotropic block form (linear, J2)
   NHQP<D> nh;
   double kappa, mu0;
+  double k1, k2, k3;  // Neo-Hookean block coefficients (below), once per Gauss point
 };
 
 template <int D>
@@ -533,6 +534,10 @@ __device__ __forceinline__ void tangent_qp(const DMat& m, const double (&H)[D][D
     if (!nh_state<D>(m, H, t.nh)) err |= ERR_INVERTED;
     t.kappa = m.kappa;
     t.mu0 = m.mu;
+    const double iJ = 1.0 / t.nh.J;  // hoisted out of the per-block work (same expressions, same values)
+    t.k1 = (2.0 / 3.0) * t.nh.c1 * iJ;
+    t.k2 = (t.nh.c3 - t.nh.c2) * iJ;
+    t.k3 = t.kappa + (5.0 / 3.0) * t.nh.c2 * iJ;
     return;
   }
   t.lam = m.lam;
@@ -603,10 +608,7 @@ __device__ __forceinline__ void tangent_block(const TangentQP<D>& t, const doubl
       }
       Fgn[a] = s1; Fgm[a] = s2; Cgn[a] = s3; Cgm[a] = s4;
     }
-    const double iJ = 1.0 / h.J;
-    const double k1 = (2.0 / 3.0) * h.c1 * iJ;
-    const double k2 = (h.c3 - h.c2) * iJ;
-    const double k3 = t.kappa + (5.0 / 3.0) * h.c2 * iJ;
+    const double k1 = t.k1, k2 = t.k2, k3 = t.k3;
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
