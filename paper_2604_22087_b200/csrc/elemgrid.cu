@@ -16,6 +16,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda_pipeline.h>
+
 #include "afem_impl.hpp"
 
 namespace afem {
@@ -500,17 +502,33 @@ __global__ void __launch_bounds__(128) k_grid_qp_tangent(const __grid_constant__
   }
 }
 
+// The element's nq * kQpt cached values are copied into a thread-private shared-memory column with
+// cp.async at the start of the element (all in flight together, beside the x gathers), then read per
+// Gauss point: one HBM round trip per element instead of one per Gauss point (ncu at 128^3: 59 %
+// long-scoreboard stalls on the per-Gauss-point loads at 8 warps per SM, 2.5 TB/s).
+constexpr int kJvpThreads = 128;
 template <int D>
-__global__ void __launch_bounds__(128) k_grid_jvp_cached(const __grid_constant__ GeoT<D> G, SysView s, int nx, int ny,
-                                                         const double* __restrict__ qpt,
-                                                         const uint8_t* __restrict__ mask,
-                                                         const double* __restrict__ x, double* __restrict__ ev,
-                                                         const int* skip) {
+constexpr size_t jvp_cached_smem() { return (size_t)EL<D>::nq * kQpt * kJvpThreads * sizeof(double); }
+
+template <int D>
+__global__ void __launch_bounds__(kJvpThreads) k_grid_jvp_cached(const __grid_constant__ GeoT<D> G, SysView s, int nx,
+                                                                int ny, const double* __restrict__ qpt,
+                                                                const uint8_t* __restrict__ mask,
+                                                                const double* __restrict__ x, double* __restrict__ ev,
+                                                                const int* skip) {
   if (skip && *skip) return;
   constexpr int npe = EL<D>::npe, nq = EL<D>::nq, nd = EL<D>::nd;
+  extern __shared__ double qsh[];  // [q * kQpt + k][thread]
+  double* col = qsh + threadIdx.x;
+  const int64_t ne = s.n_elem;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s.n_elem; e += (int64_t)gridDim.x * blockDim.x) {
     const DMat m = s.mats[s.phase[e]];
     const bool j2 = m.model == MODEL_J2;
+    if (j2) {
+#pragma unroll
+      for (int k = 0; k < nq * kQpt; ++k) __pipeline_memcpy_async(col + k * kJvpThreads, qpt + (int64_t)k * ne + e, 8);
+      __pipeline_commit();
+    }
     int64_t nodes[npe];
     elem_nodes<D>(e, nx, ny, nodes);
     double xe[nd];
@@ -538,11 +556,12 @@ __global__ void __launch_bounds__(128) k_grid_jvp_cached(const __grid_constant__
         }
       double P[D][D];
       if (j2) {  // lam tr(de) I + 2 mu de - g2 (n : de) n with the cached tangent
-        const int64_t ne = s.n_elem;
-        const double* t = qpt + (int64_t)q * kQpt * ne + e;
-        const double lam = __ldg(t), mu = __ldg(t + ne), g2 = __ldg(t + 2 * ne);
-        const double n00 = __ldg(t + 3 * ne), n11 = __ldg(t + 4 * ne), n22 = __ldg(t + 5 * ne);
-        const double n12 = __ldg(t + 6 * ne), n02 = __ldg(t + 7 * ne), n01 = __ldg(t + 8 * ne);
+        if (q == 0) __pipeline_wait_prior(0);
+        const double* t = col + q * kQpt * kJvpThreads;
+        constexpr int T = kJvpThreads;
+        const double lam = t[0], mu = t[T], g2 = t[2 * T];
+        const double n00 = t[3 * T], n11 = t[4 * T], n22 = t[5 * T];
+        const double n12 = t[6 * T], n02 = t[7 * T], n01 = t[8 * T];
         const double n3[3][3] = {{n00, n01, n02}, {n01, n11, n12}, {n02, n12, n22}};
         double tr = 0.0, nde = 0.0;
 #pragma unroll
@@ -606,8 +625,14 @@ void cached_apply(System& s, const double* qpt, const uint8_t* mask, const doubl
   GeoT<D> G;
   geo<D>(s, G);
   if (!s.ev.p) s.ev.alloc((size_t)s.n_elem * EL<D>::nd);
-  launch(*s.ctx, k_grid_jvp_cached<D>, grid_for(s.n_elem, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, qpt, mask,
-         x, s.ev.p, skip);
+  static const bool attr = [] {
+    AFEM_CK(cudaFuncSetAttribute(k_grid_jvp_cached<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)jvp_cached_smem<D>()));
+    return true;
+  }();
+  (void)attr;
+  launch(*s.ctx, k_grid_jvp_cached<D>, grid_for(s.n_elem, kJvpThreads, 148 * 64), kJvpThreads, jvp_cached_smem<D>(),
+         G, s.view(), s.nx, s.ny, qpt, mask, x, s.ev.p, skip);
   launch(*s.ctx, k_gather<D>, grid_for(s.n_nodes, 256, 148 * 32), 256, 0, s.view(), s.ev.p, mask, x, y, skip);
 }
 

@@ -15,6 +15,7 @@ s = afem.System.grid(ctx, 3, n, n, n, inclusions=afem.fibres(12345, 40), radius=
 s.set_benchmark_dirichlet(0.002)
 u = torch.from_numpy(s.impose_dirichlet(np.zeros(s.n))).cuda()
 op = afem.matrix_free_operator(s, u)
+torch.manual_seed(0)
 x = torch.rand(s.n, dtype=torch.float64, device="cuda")
 y = torch.empty_like(x)
 L = afem.load()
@@ -29,4 +30,4 @@ for _ in range(10):
     b.record()
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
-print(f"n={n} mf apply min {min(ts):.3f} ms median {sorted(ts)[5]:.3f} ms")
+print(f"n={n} mf apply min {min(ts):.3f} ms median {sorted(ts)[5]:.3f} ms checksum {float(y.abs().sum())!r}")
