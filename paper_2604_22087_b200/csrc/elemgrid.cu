@@ -6,7 +6,9 @@
 // gradients g_i(q) and w detJ(q) are computed once per system (GridGeo, passed as a __grid_constant__
 // parameter: uniform broadcast reads, no per-element geometry) and the element kernel evaluates the
 // constitutive update once per Gauss point, writing the element's nd-vector to a scratch array:
-//     k_grid_elem<MODE>  thread per element: gather u_e (and x_e), qp loop, ev[e] = f_e
+//     k_grid_elem<MODE>  thread per element: gather u_e (and x_e), qp loop, ev[corner][e] = f_e
+//                        (corner-major scratch: a warp's stores of one corner, and the gather's
+//                        loads of one incidence slot over consecutive nodes, are contiguous)
 //     k_gather           thread per node: y_n = sum over the node's incident (element, corner) pairs
 //                        in the reference's (batch, element) order (assembly.hpp:130-137)
 // The reduction order is the node-centric kernels' (and the reference's), so results stay
@@ -344,6 +346,15 @@ __device__ __forceinline__ void elem_nodes(int64_t e, int nx, int ny, int64_t (&
   }
 }
 
+// Element vector f_e into the corner-major scratch ev[corner][element][D]
+template <int D>
+__device__ __forceinline__ void ev_store(double* ev, int64_t n_elem, int64_t e, const double (&f)[EL<D>::nd]) {
+#pragma unroll
+  for (int k = 0; k < EL<D>::npe; ++k)
+#pragma unroll
+    for (int a = 0; a < D; ++a) ev[((int64_t)k * n_elem + e) * D + a] = f[k * D + a];
+}
+
 template <int D, int MODE>
 __global__ void __launch_bounds__(128) k_grid_elem(const __grid_constant__ GeoT<D> G, SysView s, int nx, int ny,
                                                    const double* __restrict__ u, const uint8_t* __restrict__ mask,
@@ -422,9 +433,7 @@ __global__ void __launch_bounds__(128) k_grid_elem(const __grid_constant__ GeoT<
           }
       }
     }
-    double2* o = reinterpret_cast<double2*>(ev + e * nd);
-#pragma unroll
-    for (int k = 0; k < nd / 2; ++k) o[k] = make_double2(f[2 * k], f[2 * k + 1]);
+    ev_store<D>(ev, s.n_elem, e, f);
   }
   if (err) atomicOr(s.err, err);
 }
@@ -443,7 +452,7 @@ __global__ void __launch_bounds__(256) k_gather(SysView s, const double* __restr
     for (int a = 0; a < D; ++a) acc[a] = 0.0;
     for (int64_t p = s.inc_ptr[n]; p < s.inc_ptr[n + 1]; ++p) {
       const uint32_t v = __ldg(&s.inc[p]);
-      const double* src = ev + (int64_t)(v / npe) * nd + (v % npe) * D;
+      const double* src = ev + ((int64_t)(v % npe) * s.n_elem + v / npe) * D;
 #pragma unroll
       for (int a = 0; a < D; ++a) acc[a] += __ldg(&src[a]);
     }
@@ -589,9 +598,7 @@ __global__ void __launch_bounds__(kJvpThreads) k_grid_jvp_cached(const __grid_co
           f[D * i + a] += wdet * t;
         }
     }
-    double2* o = reinterpret_cast<double2*>(ev + e * nd);
-#pragma unroll
-    for (int k = 0; k < nd / 2; ++k) o[k] = make_double2(f[2 * k], f[2 * k + 1]);
+    ev_store<D>(ev, s.n_elem, e, f);
   }
 }
 
