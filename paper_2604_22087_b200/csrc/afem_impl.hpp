@@ -202,7 +202,7 @@ void grid_mf_apply(System& s, const double* state, const uint8_t* mask, const do
 bool grid_tangent_cacheable(const System& s);
 void grid_tangent_cache(System& s, const double* u, DevArray<double>& qpt);
 void grid_mf_apply_cached(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y,
-                          const int* skip = nullptr);
+                          const int* skip = nullptr, double* dot_out = nullptr);
 
 // ---- blas.cu (deterministic reductions; results in device scalars or host)
 double dot(Ctx& c, const double* x, const double* y, int64_t n);

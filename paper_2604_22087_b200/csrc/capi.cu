@@ -58,8 +58,10 @@ void MfOp::apply(const double* x, double* y) {
 }
 bool MfOp::apply_dot(const double* x, double* y, double* dot_out) {
   static const bool disabled = std::getenv("AFEM_NO_FUSED_DOT") != nullptr;
-  if (!stencil || disabled) return false;
-  stencil_apply(*stencil, *this, x, y, dot_out, skip);
+  if (disabled) return false;
+  if (stencil) stencil_apply(*stencil, *this, x, y, dot_out, skip);
+  else if (qpt.p) grid_mf_apply_cached(*sys, qpt.p, mask.p, x, y, skip, dot_out);  // dot fused into the gather
+  else return false;
   return true;
 }
 void MfOp::diagonal(double* d) { copy(*sys->ctx, diag.p, d, n); }

@@ -21,6 +21,7 @@
 #include <cuda_pipeline.h>
 
 #include "afem_impl.hpp"
+#include "reduce.cuh"
 
 namespace afem {
 
@@ -441,10 +442,14 @@ __global__ void __launch_bounds__(128) k_grid_elem(const __grid_constant__ GeoT<
 // y_n = sum of the node's element contributions in (batch, element) order; JVP: unit rows on
 // constrained dofs (backend.hpp:146-147).
 template <int D>
+// dot_out (JVP only): also x.y over every row, into dot_out[0] (fixed-order grid reduction over
+// <= kRedBlocks * 4 blocks): the CG's p.Ap fused into the apply, so the loop does not re-read p, Ap.
 __global__ void __launch_bounds__(256) k_gather(SysView s, const double* __restrict__ ev, const uint8_t* __restrict__ mask,
                                                 const double* __restrict__ x, double* __restrict__ y,
-                                                const int* skip) {
+                                                const int* skip, double* partials, unsigned* counter,
+                                                double* dot_out) {
   if (skip && *skip) return;
+  double dsum = 0.0;
   constexpr int npe = EL<D>::npe, nd = EL<D>::nd;
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < s.n_nodes; n += (int64_t)gridDim.x * blockDim.x) {
     double acc[D];
@@ -459,9 +464,14 @@ __global__ void __launch_bounds__(256) k_gather(SysView s, const double* __restr
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       const int64_t d = D * n + a;
-      y[d] = (mask && mask[d]) ? x[d] : acc[a];
+      const double yv = (mask && mask[d]) ? x[d] : acc[a];
+      y[d] = yv;
+      if (dot_out) dsum += x[d] * yv;
     }
   }
+  if (!dot_out) return;
+  double v[1] = {dsum};
+  if (grid_reduce<1>(v, partials, counter) && threadIdx.x == 0) dot_out[0] = v[0];
 }
 
 
@@ -616,7 +626,7 @@ void run(System& s, const double* u, const uint8_t* mask, const double* x, doubl
   launch(*s.ctx, k_grid_elem<D, MODE>, grid_for(s.n_elem, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, u, mask, x,
          s.ev.p);
   launch(*s.ctx, k_gather<D>, grid_for(s.n_nodes, 256, 148 * 32), 256, 0, s.view(), s.ev.p,
-         MODE == EV_JVP ? mask : nullptr, x, y, nullptr);
+         MODE == EV_JVP ? mask : nullptr, x, y, nullptr, nullptr, nullptr, nullptr);
 }
 
 template <int D>
@@ -628,7 +638,8 @@ void cached_tangent(System& s, const double* u, DevArray<double>& qpt) {
 }
 
 template <int D>
-void cached_apply(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y, const int* skip) {
+void cached_apply(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y, const int* skip,
+                  double* dot_out) {
   GeoT<D> G;
   geo<D>(s, G);
   if (!s.ev.p) s.ev.alloc((size_t)s.n_elem * EL<D>::nd);
@@ -640,7 +651,9 @@ void cached_apply(System& s, const double* qpt, const uint8_t* mask, const doubl
   (void)attr;
   launch(*s.ctx, k_grid_jvp_cached<D>, grid_for(s.n_elem, kJvpThreads, 148 * 64), kJvpThreads, jvp_cached_smem<D>(),
          G, s.view(), s.nx, s.ny, qpt, mask, x, s.ev.p, skip);
-  launch(*s.ctx, k_gather<D>, grid_for(s.n_nodes, 256, 148 * 32), 256, 0, s.view(), s.ev.p, mask, x, y, skip);
+  Ctx& c = *s.ctx;
+  launch(c, k_gather<D>, std::min<unsigned>(grid_for(s.n_nodes, 256, 148 * 32), kRedBlocks * 4), 256, 0, s.view(),
+         s.ev.p, mask, x, y, skip, c.red_partials.p, c.red_counter.p, dot_out);
 }
 
 }  // namespace
@@ -660,9 +673,9 @@ void grid_tangent_cache(System& s, const double* u, DevArray<double>& qpt) {
 }
 
 void grid_mf_apply_cached(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y,
-                          const int* skip) {
-  if (s.dim == 2) cached_apply<2>(s, qpt, mask, x, y, skip);
-  else cached_apply<3>(s, qpt, mask, x, y, skip);
+                          const int* skip, double* dot_out) {
+  if (s.dim == 2) cached_apply<2>(s, qpt, mask, x, y, skip, dot_out);
+  else cached_apply<3>(s, qpt, mask, x, y, skip, dot_out);
 }
 
 void grid_geometry(System& s) {
