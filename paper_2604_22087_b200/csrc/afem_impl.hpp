@@ -198,7 +198,8 @@ void grid_residual(System& s, const double* u, double* r);
 void grid_diagonal(System& s, const double* u, double* d);
 void grid_jacobian(System& s, const double* u, double* values);
 void grid_history_commit(System& s, const double* u);  // 3D grids
-void grid_mf_apply(System& s, const double* state, const uint8_t* mask, const double* x, double* y);
+void grid_mf_apply(System& s, const double* state, const uint8_t* mask, const double* x, double* y,
+                   double* dot_out = nullptr);
 bool grid_tangent_cacheable(const System& s);
 void grid_tangent_cache(System& s, const double* u, DevArray<double>& qpt);
 void grid_mf_apply_cached(System& s, const double* qpt, const uint8_t* mask, const double* x, double* y,

@@ -61,6 +61,7 @@ bool MfOp::apply_dot(const double* x, double* y, double* dot_out) {
   if (disabled) return false;
   if (stencil) stencil_apply(*stencil, *this, x, y, dot_out, skip);
   else if (qpt.p) grid_mf_apply_cached(*sys, qpt.p, mask.p, x, y, skip, dot_out);  // dot fused into the gather
+  else if (grid_elem_path(*sys)) grid_mf_apply(*sys, state.p, mask.p, x, y, dot_out);  // (any law on a grid)
   else return false;
   return true;
 }

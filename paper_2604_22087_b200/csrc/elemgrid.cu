@@ -618,15 +618,17 @@ void geo(const System& s, GeoT<D>& G) {
 }
 
 template <int D, int MODE>
-void run(System& s, const double* u, const uint8_t* mask, const double* x, double* y) {
+void run(System& s, const double* u, const uint8_t* mask, const double* x, double* y, double* dot_out = nullptr) {
   GeoT<D> G;
   static_assert(sizeof(GeoT<D>) == sizeof(double) * (EL<D>::nq * EL<D>::npe * D + EL<D>::nq), "layout");
   std::memcpy(&G, s.grid_geo.data(), sizeof G);
   if (!s.ev.p) s.ev.alloc((size_t)s.n_elem * EL<D>::nd);
   launch(*s.ctx, k_grid_elem<D, MODE>, grid_for(s.n_elem, 128, 148 * 64), 128, 0, G, s.view(), s.nx, s.ny, u, mask, x,
          s.ev.p);
-  launch(*s.ctx, k_gather<D>, grid_for(s.n_nodes, 256, 148 * 32), 256, 0, s.view(), s.ev.p,
-         MODE == EV_JVP ? mask : nullptr, x, y, nullptr, nullptr, nullptr, nullptr);
+  Ctx& c = *s.ctx;
+  launch(c, k_gather<D>, std::min<unsigned>(grid_for(s.n_nodes, 256, 148 * 32), kRedBlocks * 4), 256, 0, s.view(),
+         s.ev.p, MODE == EV_JVP ? mask : nullptr, x, y, nullptr, c.red_partials.p, c.red_counter.p,
+         MODE == EV_JVP ? dot_out : nullptr);
 }
 
 template <int D>
@@ -749,9 +751,10 @@ void grid_diagonal(System& s, const double* u, double* d) {
   else run<3, EV_DIAG>(s, u, nullptr, nullptr, d);
 }
 
-void grid_mf_apply(System& s, const double* state, const uint8_t* mask, const double* x, double* y) {
-  if (s.dim == 2) run<2, EV_JVP>(s, state, mask, x, y);
-  else run<3, EV_JVP>(s, state, mask, x, y);
+void grid_mf_apply(System& s, const double* state, const uint8_t* mask, const double* x, double* y,
+                   double* dot_out) {
+  if (s.dim == 2) run<2, EV_JVP>(s, state, mask, x, y, dot_out);
+  else run<3, EV_JVP>(s, state, mask, x, y, dot_out);
 }
 
 }  // namespace afem
